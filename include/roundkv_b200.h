@@ -1,0 +1,170 @@
+/*
+ * roundkv_b200.h — C ABI of librk.so, the B200-native (sm_100a) hot path of
+ * Round Attention (arXiv 2502.15294).
+ *
+ * Each entry point replaces one interface of the reference package
+ * (/root/reference/pkg/src/roundkv/...), cited beside it.  Conventions follow
+ * the reference's only FFI (the Cython kernel, _attn_ext.pyx:84-116):
+ *   - the caller allocates every output and scratch buffer (device memory,
+ *     torch-allocated on the Python side); the library never allocates;
+ *   - all pointers are device pointers unless the name says `host`;
+ *   - every call is asynchronous on `stream` (a cudaStream_t);
+ *   - the return value is a status: RK_OK, or a negative RK_ERR_* code whose
+ *     message is available from rk_last_error() (thread-local).  The Python
+ *     layer maps the codes onto roundkv.errors (errors.py:28-41):
+ *       RK_ERR_DOMAIN -> DomainError, RK_ERR_CAPACITY -> CapacityError,
+ *       RK_ERR_CONSISTENCY -> ConsistencyError, RK_ERR_INVARIANT -> InvariantError.
+ *     Row-level invariants found on the device (a query row with no visible
+ *     key, _attn_ext.pyx:49-50,110-111) are reported through a device int32
+ *     `bad_row` (INT32_MAX = none) that the caller reads back.
+ *
+ * Layouts (row-major, element = float32 or bf16 per `kv_dtype`):
+ *   q            [rows][hq][d]            float32
+ *   KV cache     [keys][hkv][d]           token-major, as the reference's
+ *                                          per-layer payload (store.py:225-242)
+ *   out          [rows][hq][d]            float32 (== reference (n, H*d))
+ * GQA: query head h reads key head h / (hq/hkv) (HF repeat_kv convention).
+ */
+#ifndef ROUNDKV_B200_H
+#define ROUNDKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* rk_stream_t; /* identical to cudaStream_t */
+
+#define RK_ABI_VERSION 1
+
+#define RK_F32 0
+#define RK_BF16 1
+
+#define RK_OK 0
+#define RK_ERR_DOMAIN -1
+#define RK_ERR_CAPACITY -2
+#define RK_ERR_CONSISTENCY -3
+#define RK_ERR_INVARIANT -4
+#define RK_ERR_CUDA -5
+#define RK_ERR_UNSUPPORTED -6
+
+/* selection kinds (selection.py:20) */
+#define RK_SEL_FIXED 0
+#define RK_SEL_TOP_PERCENT 1
+#define RK_SEL_ADAPTIVE 2
+#define RK_SEL_ALL 3
+
+int rk_abi_version(void);
+const char* rk_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * 1. Kernel contract: attention_forward(q, k, v, q_pos, k_pos, allowed, capture)
+ *    Replaces backend.attention_forward (backend.py:46-47) ->
+ *    _attn_ext.attention_forward (_attn_ext.pyx:84-116) / _attn_np.py:50-92.
+ *    scores (nullable): [n][s] float64, head-summed and row-normalised
+ *    (capture=True).  allowed (nullable): [s] uint8.  hq % hkv == 0.
+ * ---------------------------------------------------------------------- */
+size_t rk_attention_workspace_bytes(int n, int hq, int hkv, int s, int d);
+int rk_attention_forward(const float* q, int n, int hq, int d,
+                         const void* k, const void* v, int kv_dtype, int s, int hkv,
+                         const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed,
+                         float* out, double* scores, int32_t* bad_row,
+                         void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * 2. Sparse decode attention over a round-spliced cache (the decode loop,
+ *    pipeline.py:298-313 -> engine.forward_range:244-267 with one new row).
+ *    Dialogue b's cache starts at k_cache + b*cache_stride elements and holds
+ *    seq_len[b] keys (device int32).  If k_new/v_new ([batch][hkv][d]) are
+ *    given, the row is appended at index seq_len[b] and attended (seq_len is
+ *    NOT advanced; see rk_advance_lengths).  max_seq_len bounds seq_len[b]+1
+ *    and sizes the split-K grid.
+ *    items (nullable): round-aligned work items [batch][items_stride][3] =
+ *    (key_lo, key_hi, bin) with n_items[batch]; with items the per-item
+ *    softmax statistics are left in `workspace` for rk_round_scores_finalize
+ *    (fused watershed scoring).
+ * ---------------------------------------------------------------------- */
+size_t rk_decode_workspace_bytes(int batch, int hq, int hkv, int d, int max_splits);
+int rk_decode_attention(const float* q, int batch, int hq, int d,
+                        void* k_cache, void* v_cache, int kv_dtype, int hkv,
+                        int64_t cache_stride, const int32_t* seq_len, int max_seq_len,
+                        const void* k_new, const void* v_new,
+                        const int32_t* items, const int32_t* n_items, int items_stride,
+                        float* out, void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
+/* seq_len[i] += delta for i < n (advance one decode step) */
+int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * 3. Watershed round scoring: the fused equivalent of
+ *      capture = attention_forward(q, K_{Lw-1}, ..., capture=True)[1]
+ *      raw = aggregate_round_attention(capture, rounds, "question", n,
+ *                                      active_rounds, row_offset=q_start)
+ *    (pipeline.py:225-245, stats.py:59-94, _attn_ext.pyx:75-76,113-114).
+ *    Keys [0, s) of layer Lw-1 are grouped into round-aligned work items
+ *    (key_lo, key_hi, bin); bin in [0, n_bins) is a prior round, bin ==
+ *    n_bins is the current question (denominator only).  Only the softmax
+ *    statistics are produced (no capture matrix).  raw_out has one float64 per
+ *    ACTIVE bin, in ascending bin order (active: [n_bins] uint8, nullable).
+ * ---------------------------------------------------------------------- */
+size_t rk_round_scores_workspace_bytes(int n_q, int hq, int hkv, int n_items, int d, int n_bins);
+int rk_round_scores(const float* q, int n_q, int hq, int d,
+                    const void* k, int kv_dtype, int s, int hkv,
+                    const int64_t* q_pos, const int64_t* k_pos,
+                    const int32_t* items, int n_items, int n_bins, const uint8_t* active,
+                    double* raw_out, void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
+/* Finalise scores left by rk_decode_attention(items != NULL): one dialogue
+ * row per batch entry; raw_out [batch][n_bins] (inactive bins -> 0). */
+int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int items_stride, const int32_t* items,
+                             const int32_t* n_items, int n_bins, const uint8_t* active,
+                             double* raw_out, void* workspace, rk_stream_t stream);
+
+/* Eq. 1 on a materialised capture matrix (stats.py:59-94 on the device):
+ * raw[a] = sum over rows [row_lo,row_hi) of scores[row][col] for the columns
+ * of active round a, given as two half-open spans per round (q_span, a_span). */
+int rk_aggregate_rounds(const double* scores, int64_t ld, int row_lo, int row_hi,
+                        const int64_t* spans /* [n_active][4] */, int n_active,
+                        double* raw_out, rk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * 4. normalize + select (stats.py:97-115, selection.py:63-126), one block.
+ *    masses = raw / sum(raw) with NumPy's pairwise summation order, uniform
+ *    when the sum is 0 (degenerate).  Kept positions are ascending indices
+ *    into raw.  top_percent keeps the k_top largest masses, ties to the lower
+ *    index (stable argsort); k_top is computed by the caller with the
+ *    reference expression (selection.py:93-94).  fixed / adaptive fall back to
+ *    the first argmax when nothing passes.  status_out: 0 ok, RK_ERR_DOMAIN if
+ *    any raw < 0.  Bit-exact against the reference for the same raw.
+ * ---------------------------------------------------------------------- */
+int rk_select(const double* raw, int n, int normalize, int kind, double v, int k_top, double kappa,
+              double* masses_out, int32_t* kept_out, int32_t* n_kept_out,
+              int32_t* degenerate_out, int32_t* status_out, rk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * 5. Batched host->HBM gather of kept rounds' upper-layer blocks
+ *    (store.fetch_upper store.py:254-263 + pipeline._assemble :158-169).
+ *    Copy i moves `height[i]` rows of `width[i]` bytes from pinned host
+ *    memory (src_host[i], row pitch src_pitch[i]) to device memory
+ *    (dst[i], pitch dst_pitch[i]) as DMA on `stream`; one call = one ledger
+ *    h2d event.  If done_event (a cudaEvent_t) is given it is recorded after
+ *    the last copy.
+ * ---------------------------------------------------------------------- */
+int rk_h2d_gather(int n, const void* const* src_host, const size_t* src_pitch,
+                  void* const* dst, const size_t* dst_pitch,
+                  const size_t* width, const size_t* height,
+                  rk_stream_t stream, void* done_event);
+
+/* D2H counterpart for the new round's upper block (writeback_upper :265-278). */
+int rk_d2h_scatter(int n, const void* const* src, const size_t* src_pitch,
+                   void* const* dst_host, const size_t* dst_pitch,
+                   const size_t* width, const size_t* height,
+                   rk_stream_t stream, void* done_event);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROUNDKV_B200_H */

@@ -1,0 +1,368 @@
+// Host entry points for the attention family: kernel contract, decode, round
+// scoring.  See include/roundkv_b200.h for the ABI and attn_split.cuh for the
+// main kernel.
+#include <climits>
+#include <cmath>
+
+#include "attn_dispatch.cuh"
+
+namespace rk {
+
+// ---------------------------------------------------------------- config
+static int check_heads(int hq, int hkv, int d, Shape* s) {
+  if (hq <= 0 || hkv <= 0 || hq % hkv != 0)
+    return fail(RK_ERR_DOMAIN, "query heads %d not a multiple of key heads %d", hq, hkv);
+  if (d <= 0) return fail(RK_ERR_DOMAIN, "head_dim must be positive");
+  if (!pick_shape(d, hq / hkv, s)) return fail(RK_ERR_UNSUPPORTED, "head_dim %d not supported", d);
+  return RK_OK;
+}
+
+static int dispatch_split(int kv_dtype, bool decode, bool score, int G, const Shape& s, dim3 grid,
+                          cudaStream_t st, const SplitParams& p) {
+  int r;
+  if (kv_dtype == RK_F32) r = dispatch_f32(decode, score, G, s, grid, st, p);
+  else if (kv_dtype == RK_BF16) r = dispatch_bf16(decode, score, G, s, grid, st, p);
+  else return fail(RK_ERR_DOMAIN, "kv_dtype %d unknown", kv_dtype);
+  if (r == 1) return fail(RK_ERR_UNSUPPORTED, "GQA group %d not supported (1, 2, 4, 7, 8)", G);
+  if (r == 2) return cuda_status(cudaGetLastError(), "attn_split_kernel launch");
+  return RK_OK;
+}
+
+// workspace carving ----------------------------------------------------------
+struct SplitWs {
+  unsigned* counters;
+  float *part_m, *part_l, *part_acc, *stat_m, *stat_l;
+  size_t bytes;
+};
+
+static SplitWs carve(void* base, int rows, int hq, int hkv, int splits, int d) {
+  SplitWs w{};
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t n) { size_t o = off; off = align_up(off + n, 256); return b ? b + o : nullptr; };
+  w.counters = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * rows * hkv));
+  w.part_m = reinterpret_cast<float*>(take(sizeof(float) * (size_t)rows * hq * splits));
+  w.part_l = reinterpret_cast<float*>(take(sizeof(float) * (size_t)rows * hq * splits));
+  w.part_acc = reinterpret_cast<float*>(take(sizeof(float) * (size_t)rows * hq * splits * d));
+  w.stat_m = reinterpret_cast<float*>(take(sizeof(float) * (size_t)rows * hq));
+  w.stat_l = reinterpret_cast<float*>(take(sizeof(float) * (size_t)rows * hq));
+  w.bytes = off;
+  return w;
+}
+
+static int general_splits(int n, int hkv, int s, int d, int G) {
+  Shape sh;
+  if (!pick_shape(d, G, &sh)) return 1;
+  int target = 4 * sm_count();
+  int per_row = (target + n * hkv - 1) / (n * hkv);
+  int max_useful = (s + tile_keys(sh) - 1) / tile_keys(sh);
+  int sp = per_row < max_useful ? per_row : max_useful;
+  if (sp > 256) sp = 256;
+  return sp < 1 ? 1 : sp;
+}
+
+// ---------------------------------------------------------------- capture
+// cap[i][j] = sum_h exp2(s_hij - M_ih) / L_ih  (fp64 over heads, in head order),
+// 0 where key j is not visible — head-summed probabilities, _attn_ext.pyx:75-76
+template <typename T>
+__global__ void capture_kernel(const float* __restrict__ q, const T* __restrict__ k, int n, int hq,
+                               int hkv, int d, int s, const int64_t* __restrict__ q_pos,
+                               const int64_t* __restrict__ k_pos, const uint8_t* __restrict__ allowed,
+                               const float* __restrict__ stat_m, const float* __restrict__ stat_l,
+                               float scale_log2, double* __restrict__ cap) {
+  int i = blockIdx.y;
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= s) return;
+  double acc = 0.0;
+  bool vis = k_pos[j] <= q_pos[i] && (allowed == nullptr || allowed[j]);
+  if (vis) {
+    int G = hq / hkv;
+    for (int h = 0; h < hq; ++h) {
+      const float* qp = q + ((int64_t)i * hq + h) * d;
+      const T* kp = k + ((int64_t)j * hkv + h / G) * d;
+      float dot = 0.f;
+      for (int e = 0; e < d; ++e) dot = fmaf(qp[e] * scale_log2, KV<T>::get(kp, e), dot);
+      float mm = stat_m[(int64_t)i * hq + h];
+      acc += (double)exp2f(dot - mm) / (double)stat_l[(int64_t)i * hq + h];
+    }
+  }
+  cap[(int64_t)i * s + j] = acc;
+}
+
+// row-normalise (cap /= cap.sum(axis=1), _attn_ext.pyx:113-114)
+__global__ void rownorm_kernel(double* cap, int s) {
+  __shared__ double red[256];
+  double* row = cap + (int64_t)blockIdx.x * s;
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < s; j += blockDim.x) acc += row[j];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  double tot = red[0];
+  for (int j = threadIdx.x; j < s; j += blockDim.x) row[j] = row[j] / tot;
+}
+
+__global__ void fill_i32(int32_t* p, int32_t v) { *p = v; }
+
+__global__ void advance_kernel(int32_t* len, int n, int delta) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) len[i] += delta;
+}
+
+// ---------------------------------------------------------------- score finalize
+// Per row: per head M_h, L_h over items; per bin mass = sum_h sum_items(bin)
+// l*exp2(m - M_h)/L_h (fp64); row sum over all bins (incl. current and
+// inactive, as the reference's row normalisation); massn = mass / rowsum.
+// mode 0 (multi-row question): massn -> rowmass[row][bin] then summed over rows;
+// mode 1 (batched decode): massn -> raw[row][bin] directly.
+__global__ void score_rows_kernel(const float* __restrict__ part_m, const float* __restrict__ part_l,
+                                  int nsplit, int hq, const int32_t* __restrict__ items, int items_stride,
+                                  const int32_t* __restrict__ n_items_dev, int n_items_static, int n_bins,
+                                  const uint8_t* __restrict__ active, double* __restrict__ out_rows) {
+  extern __shared__ double sh[];
+  double* mass = sh;                                   // [n_bins + 1]
+  float* Mh = reinterpret_cast<float*>(mass + n_bins + 1);   // [hq]
+  float* Lh = Mh + hq;                                 // [hq]
+  int* bin_lo = reinterpret_cast<int*>(Lh + hq);       // [n_bins + 2]
+  const int row = blockIdx.x;
+  const int32_t* tab = items + (size_t)row * items_stride * 3;
+  int n_items = n_items_dev ? n_items_dev[items_stride ? row : 0] : n_items_static;
+  const float* pm = part_m + (size_t)row * hq * nsplit;
+  const float* pl = part_l + (size_t)row * hq * nsplit;
+  for (int h = threadIdx.x; h < hq; h += blockDim.x) {
+    float mx = -INFINITY;
+    for (int it = 0; it < n_items; ++it) mx = fmaxf(mx, pm[h * nsplit + it]);
+    double L = 0.0;
+    for (int it = 0; it < n_items; ++it)
+      L += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - mx);
+    Mh[h] = mx;
+    Lh[h] = (float)L;
+  }
+  if (threadIdx.x == 0) {          // items are sorted by bin: first item of each bin
+    int it = 0;
+    for (int b = 0; b <= n_bins + 1; ++b) {
+      while (it < n_items && tab[it * 3 + 2] < b) ++it;
+      bin_lo[b] = it;
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b <= n_bins; b += blockDim.x) {
+    double acc = 0.0;
+    for (int h = 0; h < hq; ++h) {
+      double hs = 0.0;
+      for (int it = bin_lo[b]; it < bin_lo[b + 1]; ++it)
+        hs += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - Mh[h]);
+      acc += hs / (double)Lh[h];
+    }
+    mass[b] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int b = 0; b <= n_bins; ++b) tot += mass[b];
+    for (int b = 0; b < n_bins; ++b) {
+      bool on = active == nullptr || active[b];
+      out_rows[(size_t)row * n_bins + b] = on ? mass[b] / tot : 0.0;
+    }
+  }
+}
+
+// raw[a] over active bins (ascending) = sum over rows of massn[row][bin]
+__global__ void score_sum_rows_kernel(const double* __restrict__ rows_mass, int n_rows, int n_bins,
+                                      const uint8_t* __restrict__ active, double* __restrict__ raw) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_bins) return;
+  if (active && !active[b]) return;
+  int a = b;
+  if (active) {
+    a = 0;
+    for (int x = 0; x < b; ++x) a += active[x] ? 1 : 0;
+  }
+  double acc = 0.0;
+  for (int r = 0; r < n_rows; ++r) acc += rows_mass[(size_t)r * n_bins + b];
+  raw[a] = acc;
+}
+
+static size_t score_rows_smem(int n_bins, int hq) {
+  return sizeof(double) * (n_bins + 1) + sizeof(float) * 2 * hq + sizeof(int) * (n_bins + 2);
+}
+
+}  // namespace rk
+
+using namespace rk;
+
+extern "C" {
+
+size_t rk_attention_workspace_bytes(int n, int hq, int hkv, int s, int d) {
+  if (n <= 0 || hq <= 0 || hkv <= 0 || d <= 0) return 256;
+  int sp = general_splits(n, hkv, s, d, hq / hkv);
+  return carve(nullptr, n, hq, hkv, sp, d).bytes;
+}
+
+int rk_attention_forward(const float* q, int n, int hq, int d, const void* k, const void* v,
+                         int kv_dtype, int s, int hkv, const int64_t* q_pos, const int64_t* k_pos,
+                         const uint8_t* allowed, float* out, double* scores, int32_t* bad_row,
+                         void* workspace, size_t workspace_bytes, rk_stream_t stream) {
+  Shape sh;
+  int st = check_heads(hq, hkv, d, &sh);
+  if (st) return st;
+  if (n < 0 || s < 0) return fail(RK_ERR_DOMAIN, "negative row count");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (bad_row) {
+    fill_i32<<<1, 1, 0, cs>>>(bad_row, INT_MAX);
+    RK_CHECK_LAUNCH("fill bad_row");
+  }
+  if (n == 0) return RK_OK;
+  if (s == 0) {
+    if (bad_row) { fill_i32<<<1, 1, 0, cs>>>(bad_row, 0); RK_CHECK_LAUNCH("fill bad_row"); }
+    return RK_OK;
+  }
+  int sp = general_splits(n, hkv, s, d, hq / hkv);
+  SplitWs w = carve(workspace, n, hq, hkv, sp, d);
+  if (w.bytes > workspace_bytes)
+    return fail(RK_ERR_CAPACITY, "workspace %zu bytes < required %zu", workspace_bytes, w.bytes);
+  SplitParams p{};
+  p.q = q; p.k = k; p.v = v;
+  p.row_stride = (int64_t)hkv * d;
+  p.s_static = s;
+  p.q_pos = q_pos; p.k_pos = k_pos; p.allowed = allowed;
+  p.rows = n; p.hq = hq; p.hkv = hkv; p.d = d;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  p.out = out;
+  p.part_m = w.part_m; p.part_l = w.part_l; p.part_acc = w.part_acc;
+  p.counters = w.counters; p.bad_row = bad_row;
+  p.stat_m = scores ? w.stat_m : nullptr;
+  p.stat_l = scores ? w.stat_l : nullptr;
+  dim3 grid(sp, n, hkv);
+  st = dispatch_split(kv_dtype, false, false, hq / hkv, sh, grid, cs, p);
+  if (st) return st;
+  if (scores) {
+    dim3 g2((s + 255) / 256, n);
+    if (kv_dtype == RK_F32)
+      capture_kernel<float><<<g2, 256, 0, cs>>>(q, (const float*)k, n, hq, hkv, d, s, q_pos, k_pos, allowed,
+                                               w.stat_m, w.stat_l, p.scale_log2, scores);
+    else
+      capture_kernel<__nv_bfloat16><<<g2, 256, 0, cs>>>(q, (const __nv_bfloat16*)k, n, hq, hkv, d, s, q_pos,
+                                                       k_pos, allowed, w.stat_m, w.stat_l, p.scale_log2, scores);
+    RK_CHECK_LAUNCH("capture_kernel");
+    rownorm_kernel<<<n, 256, 0, cs>>>(scores, s);
+    RK_CHECK_LAUNCH("rownorm_kernel");
+  }
+  return RK_OK;
+}
+
+size_t rk_decode_workspace_bytes(int batch, int hq, int hkv, int d, int max_splits) {
+  if (batch <= 0 || hq <= 0 || hkv <= 0 || d <= 0 || max_splits <= 0) return 256;
+  return carve(nullptr, batch, hq, hkv, max_splits, d).bytes;
+}
+
+static int decode_splits(int batch, int hkv, int max_seq_len, int d, int G) {
+  Shape sh;
+  if (!pick_shape(d, G, &sh)) return 1;
+  int target = 4 * sm_count();
+  int per = (target + batch * hkv - 1) / (batch * hkv);
+  int useful = (max_seq_len + 2 * tile_keys(sh) - 1) / (2 * tile_keys(sh));
+  int sp = per < useful ? per : useful;
+  if (sp > 128) sp = 128;
+  return sp < 1 ? 1 : sp;
+}
+
+int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache, void* v_cache,
+                        int kv_dtype, int hkv, int64_t cache_stride, const int32_t* seq_len,
+                        int max_seq_len, const void* k_new, const void* v_new, const int32_t* items,
+                        const int32_t* n_items, int items_stride, float* out, void* workspace,
+                        size_t workspace_bytes, rk_stream_t stream) {
+  Shape sh;
+  int st = check_heads(hq, hkv, d, &sh);
+  if (st) return st;
+  if (batch <= 0) return RK_OK;
+  if (max_seq_len <= 0) return fail(RK_ERR_DOMAIN, "max_seq_len must be positive");
+  if ((k_new == nullptr) != (v_new == nullptr)) return fail(RK_ERR_DOMAIN, "k_new and v_new go together");
+  int sp = items ? items_stride : decode_splits(batch, hkv, max_seq_len, d, hq / hkv);
+  if (items && (items_stride <= 0 || n_items == nullptr))
+    return fail(RK_ERR_DOMAIN, "item table needs items_stride > 0 and n_items");
+  SplitWs w = carve(workspace, batch, hq, hkv, sp, d);
+  if (w.bytes > workspace_bytes)
+    return fail(RK_ERR_CAPACITY, "decode workspace %zu bytes < required %zu (splits %d)", workspace_bytes,
+                w.bytes, sp);
+  SplitParams p{};
+  p.q = q; p.k = k_cache; p.v = v_cache;
+  p.row_stride = (int64_t)hkv * d;
+  p.batch_stride = cache_stride;
+  p.seq_len = seq_len;
+  p.s_static = max_seq_len;
+  p.k_new = const_cast<void*>(k_new); p.v_new = const_cast<void*>(v_new);
+  p.items = items; p.n_items = n_items; p.items_row_stride = items ? items_stride : 0;
+  p.rows = batch; p.hq = hq; p.hkv = hkv; p.d = d;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  p.out = out;
+  p.part_m = w.part_m; p.part_l = w.part_l; p.part_acc = w.part_acc;
+  p.counters = w.counters;
+  dim3 grid(sp, batch, hkv);
+  return dispatch_split(kv_dtype, true, false, hq / hkv, sh, grid, reinterpret_cast<cudaStream_t>(stream), p);
+}
+
+int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream) {
+  if (n <= 0) return RK_OK;
+  advance_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(seq_len, n, delta);
+  RK_CHECK_LAUNCH("advance_kernel");
+  return RK_OK;
+}
+
+size_t rk_round_scores_workspace_bytes(int n_q, int hq, int hkv, int n_items, int d, int n_bins) {
+  if (n_q <= 0 || n_items <= 0) return 256;
+  size_t a = carve(nullptr, n_q, hq, hkv, n_items, d).bytes;
+  return align_up(a + sizeof(double) * (size_t)n_q * (n_bins > 0 ? n_bins : 1), 256);
+}
+
+int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int kv_dtype, int s, int hkv,
+                    const int64_t* q_pos, const int64_t* k_pos, const int32_t* items, int n_items,
+                    int n_bins, const uint8_t* active, double* raw_out, void* workspace,
+                    size_t workspace_bytes, rk_stream_t stream) {
+  Shape sh;
+  int st = check_heads(hq, hkv, d, &sh);
+  if (st) return st;
+  if (n_q <= 0 || n_items <= 0 || n_bins <= 0) return fail(RK_ERR_DOMAIN, "round scoring needs rows, items, bins");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  SplitWs w = carve(workspace, n_q, hq, hkv, n_items, d);
+  size_t need = align_up(w.bytes + sizeof(double) * (size_t)n_q * n_bins, 256);
+  if (need > workspace_bytes) return fail(RK_ERR_CAPACITY, "score workspace %zu < %zu", workspace_bytes, need);
+  double* rows_mass = reinterpret_cast<double*>(static_cast<char*>(workspace) + w.bytes);
+  SplitParams p{};
+  p.q = q; p.k = k; p.v = k;
+  p.row_stride = (int64_t)hkv * d;
+  p.s_static = s;
+  p.q_pos = q_pos; p.k_pos = k_pos;
+  p.items = items; p.items_row_stride = 0;
+  p.rows = n_q; p.hq = hq; p.hkv = hkv; p.d = d;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  p.part_m = w.part_m; p.part_l = w.part_l; p.part_acc = w.part_acc;
+  p.counters = w.counters;
+  dim3 grid(n_items, n_q, hkv);
+  st = dispatch_split(kv_dtype, false, true, hq / hkv, sh, grid, cs, p);
+  if (st) return st;
+  score_rows_kernel<<<n_q, 128, score_rows_smem(n_bins, hq), cs>>>(
+      w.part_m, w.part_l, n_items, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
+  RK_CHECK_LAUNCH("score_rows_kernel");
+  score_sum_rows_kernel<<<(n_bins + 127) / 128, 128, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
+  RK_CHECK_LAUNCH("score_sum_rows_kernel");
+  return RK_OK;
+}
+
+int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int items_stride, const int32_t* items,
+                             const int32_t* n_items, int n_bins, const uint8_t* active, double* raw_out,
+                             void* workspace, rk_stream_t stream) {
+  if (batch <= 0 || n_bins <= 0) return RK_OK;
+  if (items == nullptr || n_items == nullptr || items_stride <= 0)
+    return fail(RK_ERR_DOMAIN, "finalize needs the item table used by rk_decode_attention");
+  SplitWs w = carve(workspace, batch, hq, hkv, items_stride, d);
+  score_rows_kernel<<<batch, 128, score_rows_smem(n_bins, hq), reinterpret_cast<cudaStream_t>(stream)>>>(
+      w.part_m, w.part_l, items_stride, hq, items, items_stride, n_items, 0, n_bins, active, raw_out);
+  RK_CHECK_LAUNCH("score_rows_kernel");
+  return RK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+// normalize + select on the device (stats.py:97-115, selection.py:63-126) and
+// Eq. 1 aggregation over a materialised capture matrix (stats.py:59-94).
+//
+// Bit-exactness: the reference thresholds depend on float64 values produced by
+// NumPy reductions — raw.sum() (normalize), masses.mean() and masses.std()
+// (adaptive).  For a contiguous 1-D float64 array NumPy sums pairwise: blocks
+// of <= 128 elements with an 8-way unrolled accumulator, larger ranges split
+// at n/2 rounded down to a multiple of 8.  pw_sum below evaluates exactly that
+// tree with explicit round-to-nearest intrinsics (no FMA contraction), so the
+// same raw values give the same masses and the same kept set.
+#include "rk_common.cuh"
+
+namespace rk {
+
+template <typename F>
+__device__ double pw_sum(const F& f, int lo, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(lo + i));
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(lo + i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pw_sum(f, lo, n2), pw_sum(f, lo + n2, n - n2));
+}
+
+constexpr int kSelMax = 16384;
+
+__global__ void select_kernel(const double* __restrict__ raw, int n, int normalize, int kind, double v, int k_top,
+                              double kappa, double* __restrict__ masses, int32_t* __restrict__ kept,
+                              int32_t* __restrict__ n_kept, int32_t* __restrict__ degenerate,
+                              int32_t* __restrict__ status) {
+  __shared__ double s_total, s_cut;
+  __shared__ int s_neg, s_any;
+  __shared__ unsigned char flag[kSelMax];
+  const int t = threadIdx.x;
+  if (t == 0) { s_neg = 0; s_any = 0; }
+  __syncthreads();
+  for (int i = t; i < n; i += blockDim.x)
+    if (raw[i] < 0.0) s_neg = 1;
+  __syncthreads();
+  if (s_neg) {
+    if (t == 0) { *status = RK_ERR_DOMAIN; *n_kept = 0; }
+    return;
+  }
+  if (t == 0) {
+    s_total = normalize ? pw_sum([&](int i) { return raw[i]; }, 0, n) : 1.0;
+    *status = RK_OK;
+    *degenerate = (s_total > 0.0) ? 0 : 1;
+  }
+  __syncthreads();
+  const double total = s_total;
+  const bool ok = total > 0.0;
+  for (int i = t; i < n; i += blockDim.x)
+    masses[i] = !normalize ? raw[i] : ok ? __ddiv_rn(raw[i], total) : __ddiv_rn(1.0, (double)n);
+  __syncthreads();
+  if (kind == RK_SEL_ADAPTIVE && t == 0) {
+    // _methods._mean / _var: pairwise sum, true divide, squared deviations
+    double mean = __ddiv_rn(pw_sum([&](int i) { return masses[i]; }, 0, n), (double)n);
+    double var = __ddiv_rn(pw_sum([&](int i) {
+                             double dv = __dsub_rn(masses[i], mean);
+                             return __dmul_rn(dv, dv);
+                           }, 0, n), (double)n);
+    s_cut = __dadd_rn(mean, __dmul_rn(kappa, __dsqrt_rn(var)));
+  }
+  __syncthreads();
+  for (int i = t; i < n; i += blockDim.x) {
+    const double mi = masses[i];
+    bool f;
+    if (kind == RK_SEL_ALL) {
+      f = true;
+    } else if (kind == RK_SEL_TOP_PERCENT) {
+      // stable rank of -mass (np.argsort(-masses, kind="stable")): ties -> lower index
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const double mj = masses[j];
+        rank += (mj > mi) || (mj == mi && j < i);
+      }
+      f = rank < k_top;
+    } else if (kind == RK_SEL_FIXED) {
+      f = mi > v;
+    } else {
+      f = mi > s_cut;
+    }
+    flag[i] = f;
+    if (f) s_any = 1;
+  }
+  __syncthreads();
+  if (t == 0) {
+    int c = 0;
+    if (!s_any && n > 0) {      // _argmax_fallback: first maximum (selection.py:71-73)
+      int best = 0;
+      for (int i = 1; i < n; ++i)
+        if (masses[i] > masses[best]) best = i;
+      kept[c++] = best;
+    } else {
+      for (int i = 0; i < n; ++i)
+        if (flag[i]) kept[c++] = i;
+    }
+    *n_kept = c;
+  }
+}
+
+__global__ void aggregate_kernel(const double* __restrict__ scores, int64_t ld, int row_lo, int row_hi,
+                                 const int64_t* __restrict__ spans, double* __restrict__ raw) {
+  __shared__ double red[256];
+  const int a = blockIdx.x;
+  const int64_t q0 = spans[a * 4 + 0], q1 = spans[a * 4 + 1], a0 = spans[a * 4 + 2], a1 = spans[a * 4 + 3];
+  const int64_t wq = q1 - q0, wa = a1 - a0, w = wq + wa;
+  const int64_t total = (int64_t)(row_hi - row_lo) * w;
+  double acc = 0.0;
+  for (int64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int64_t r = idx / w, c = idx - r * w;
+    int64_t col = c < wq ? q0 + c : a0 + (c - wq);
+    acc += scores[(row_lo + r) * ld + col];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) raw[a] = red[0];
+}
+
+}  // namespace rk
+
+using namespace rk;
+
+extern "C" {
+
+int rk_select(const double* raw, int n, int normalize, int kind, double v, int k_top, double kappa, double* masses_out,
+              int32_t* kept_out, int32_t* n_kept_out, int32_t* degenerate_out, int32_t* status_out,
+              rk_stream_t stream) {
+  if (n < 0 || n > kSelMax) return fail(RK_ERR_DOMAIN, "selection over %d rounds (max %d)", n, kSelMax);
+  if (kind < RK_SEL_FIXED || kind > RK_SEL_ALL) return fail(RK_ERR_DOMAIN, "selection kind %d unknown", kind);
+  select_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      raw, n, normalize, kind, v, k_top, kappa, masses_out, kept_out, n_kept_out, degenerate_out, status_out);
+  RK_CHECK_LAUNCH("select_kernel");
+  return RK_OK;
+}
+
+int rk_aggregate_rounds(const double* scores, int64_t ld, int row_lo, int row_hi, const int64_t* spans,
+                        int n_active, double* raw_out, rk_stream_t stream) {
+  if (n_active <= 0) return RK_OK;
+  if (row_hi < row_lo) return fail(RK_ERR_DOMAIN, "row range reversed");
+  aggregate_kernel<<<n_active, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(scores, ld, row_lo, row_hi,
+                                                                                  spans, raw_out);
+  RK_CHECK_LAUNCH("aggregate_kernel");
+  return RK_OK;
+}
+
+}  // extern "C"

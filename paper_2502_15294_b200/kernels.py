@@ -1,0 +1,98 @@
+"""Thin torch-facing wrappers over the librk decode / scoring entry points.
+
+These take and return torch CUDA tensors (no host copies) and are what the
+pipeline and the batched decode engine call on the hot path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .workspace import scratch
+
+
+def kv_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.RK_BF16
+    if t.dtype == torch.float32:
+        return _lib.RK_F32
+    raise TypeError(f"KV dtype {t.dtype} unsupported (float32, bfloat16)")
+
+
+def decode_workspace(batch: int, hq: int, hkv: int, d: int, splits: int, device, tag: str = "decode"):
+    nbytes = _lib.lib.rk_decode_workspace_bytes(batch, hq, hkv, d, max(1, splits))
+    return scratch(nbytes, device, tag)
+
+
+def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, seq_len: torch.Tensor,
+                     max_seq_len: int, *, k_new=None, v_new=None, items=None, n_items=None,
+                     out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+    """Batched single-token attention over contiguous per-dialogue caches.
+
+    q (B, Hq, d) f32; k_cache/v_cache (B, S_cap, Hkv, d) or (S_cap, Hkv, d) for
+    B == 1; seq_len (B,) int32 device = cached keys per dialogue; k_new/v_new
+    (B, Hkv, d) appended at seq_len[b] and attended (seq_len not advanced).
+    items (B, n_items_max, 3) int32 device enables the fused round scoring.
+    """
+    B, hq, d = q.shape
+    if k_cache.dim() == 3:
+        stride = 0
+        hkv = k_cache.shape[1]
+    else:
+        stride = k_cache.stride(0)
+        hkv = k_cache.shape[2]
+    if out is None:
+        out = torch.empty((B, hq, d), dtype=torch.float32, device=q.device)
+    items_stride = 0 if items is None else items.shape[1]
+    if ws is None:
+        splits = items_stride if items is not None else 128
+        ws = decode_workspace(B, hq, hkv, d, splits, q.device)
+    _lib.call("rk_decode_attention", _lib.ptr(q), B, hq, d, _lib.ptr(k_cache), _lib.ptr(v_cache),
+              kv_code(k_cache), hkv, stride, _lib.ptr(seq_len), int(max_seq_len), _lib.ptr(k_new),
+              _lib.ptr(v_new), _lib.ptr(items), _lib.ptr(n_items), items_stride, _lib.ptr(out),
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
+    return out
+
+
+def decode_scores_finalize(batch: int, hq: int, hkv: int, d: int, items: torch.Tensor, n_items: torch.Tensor,
+                           n_bins: int, ws: torch.Tensor, active=None, raw: torch.Tensor | None = None,
+                           stream=None) -> torch.Tensor:
+    """Per-dialogue raw round masses (B, n_bins) from the statistics a
+    decode_attention(items=...) call left in `ws`."""
+    if raw is None:
+        raw = torch.empty((batch, n_bins), dtype=torch.float64, device=items.device)
+    _lib.call("rk_round_scores_finalize", batch, hq, hkv, d, items.shape[1], _lib.ptr(items), _lib.ptr(n_items),
+              n_bins, _lib.ptr(active), _lib.ptr(raw), _lib.ptr(ws), _lib.stream_ptr(stream))
+    return raw
+
+
+def advance_lengths(seq_len: torch.Tensor, delta: int = 1, stream=None) -> None:
+    _lib.call("rk_advance_lengths", _lib.ptr(seq_len), seq_len.numel(), int(delta), _lib.stream_ptr(stream))
+
+
+def select_device(raw: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, normalize=True, stream=None):
+    """rk_select on a device float64 vector; returns device (masses, ints) where
+    ints = [kept positions (n) | n_kept | degenerate | status]."""
+    n = raw.numel()
+    masses = torch.empty(n, dtype=torch.float64, device=raw.device)
+    ints = torch.zeros(n + 3, dtype=torch.int32, device=raw.device)
+    base = ints.data_ptr()
+    _lib.call("rk_select", _lib.ptr(raw), n, 1 if normalize else 0, _lib.SEL_KINDS[kind], float(v), int(k_top),
+              float(kappa), _lib.ptr(masses), base, base + 4 * n, base + 4 * (n + 1), base + 4 * (n + 2),
+              _lib.stream_ptr(stream))
+    return masses, ints
+
+
+def items_tensor(per_dialogue_bounds, chunk: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """Pack per-dialogue round-aligned items into (B, max_items, 3) + counts."""
+    from .stats import build_round_items
+    packs = [build_round_items(b, chunk) for b in per_dialogue_bounds]
+    width = max(1, max(len(p) for p in packs))
+    arr = np.zeros((len(packs), width, 3), dtype=np.int32)
+    for i, p in enumerate(packs):
+        arr[i, : len(p)] = p
+    counts = np.array([len(p) for p in packs], dtype=np.int32)
+    return torch.from_numpy(arr).to(device), torch.from_numpy(counts).to(device)
