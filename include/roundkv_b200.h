@@ -84,7 +84,15 @@ int rk_attention_forward(const float* q, int n, int hq, int d,
  *    items (nullable): round-aligned work items [batch][items_stride][3] =
  *    (key_lo, key_hi, bin) with n_items[batch]; with items the per-item
  *    softmax statistics are left in `workspace` for rk_round_scores_finalize
- *    (fused watershed scoring).
+ *    (fused watershed scoring; items_stride <= 512).
+ *    advance_len (nullable): advance_len[b] += 1 after the layer completes
+ *    (pass it on the last layer that reads a length array).
+ *    Successive calls on one stream overlap through programmatic dependent
+ *    launch: the next call may prefetch its K/V tiles and read seq_len while
+ *    the previous call's merge runs, so a length array must not be advanced
+ *    by the call immediately preceding a reader of the same array.
+ *    Workspace: rk_decode_workspace_bytes(batch, hq, hkv, d, max_splits)
+ *    (max_splits = max(items_stride, 148)), zero-filled once before first use.
  * ---------------------------------------------------------------------- */
 size_t rk_decode_workspace_bytes(int batch, int hq, int hkv, int d, int max_splits);
 int rk_decode_attention(const float* q, int batch, int hq, int d,
@@ -92,7 +100,8 @@ int rk_decode_attention(const float* q, int batch, int hq, int d,
                         int64_t cache_stride, const int32_t* seq_len, int max_seq_len,
                         const void* k_new, const void* v_new,
                         const int32_t* items, const int32_t* n_items, int items_stride,
-                        float* out, void* workspace, size_t workspace_bytes, rk_stream_t stream);
+                        float* out, int32_t* advance_len,
+                        void* workspace, size_t workspace_bytes, rk_stream_t stream);
 
 /* seq_len[i] += delta for i < n (advance one decode step) */
 int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream);

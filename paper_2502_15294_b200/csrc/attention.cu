@@ -5,6 +5,7 @@
 #include <cmath>
 
 #include "attn_dispatch.cuh"
+#include "decode_bulk.cuh"
 
 namespace rk {
 
@@ -255,7 +256,8 @@ int rk_attention_forward(const float* q, int n, int hq, int d, const void* k, co
 }
 
 size_t rk_decode_workspace_bytes(int batch, int hq, int hkv, int d, int max_splits) {
-  if (batch <= 0 || hq <= 0 || hkv <= 0 || d <= 0 || max_splits <= 0) return 256;
+  if (batch <= 0 || hq <= 0 || hkv <= 0 || d <= 0) return 256;
+  if (max_splits < 148 * 4) max_splits = 148 * 4;   // persistent CTAs x warps per head
   return carve(nullptr, batch, hq, hkv, max_splits, d).bytes;
 }
 
@@ -273,17 +275,33 @@ static int decode_splits(int batch, int hkv, int max_seq_len, int d, int G) {
 int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache, void* v_cache,
                         int kv_dtype, int hkv, int64_t cache_stride, const int32_t* seq_len,
                         int max_seq_len, const void* k_new, const void* v_new, const int32_t* items,
-                        const int32_t* n_items, int items_stride, float* out, void* workspace,
-                        size_t workspace_bytes, rk_stream_t stream) {
+                        const int32_t* n_items, int items_stride, float* out, int32_t* advance_len,
+                        void* workspace, size_t workspace_bytes, rk_stream_t stream) {
   Shape sh;
   int st = check_heads(hq, hkv, d, &sh);
   if (st) return st;
   if (batch <= 0) return RK_OK;
   if (max_seq_len <= 0) return fail(RK_ERR_DOMAIN, "max_seq_len must be positive");
   if ((k_new == nullptr) != (v_new == nullptr)) return fail(RK_ERR_DOMAIN, "k_new and v_new go together");
-  int sp = items ? items_stride : decode_splits(batch, hkv, max_seq_len, d, hq / hkv);
-  if (items && (items_stride <= 0 || n_items == nullptr))
-    return fail(RK_ERR_DOMAIN, "item table needs items_stride > 0 and n_items");
+  if (items && (items_stride <= 0 || items_stride > 512 || n_items == nullptr))
+    return fail(RK_ERR_DOMAIN, "item table needs 0 < items_stride <= 512 and n_items");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  const int G = hq / hkv;
+  if (bulk_supported(kv_dtype, d, hkv, G)) {
+    int sp = items ? items_stride * (8 / hkv) : bulk_splits(batch, max_seq_len, hkv);
+    SplitWs w = carve(workspace, batch, hq, hkv, sp, d);
+    if (w.bytes > workspace_bytes)
+      return fail(RK_ERR_CAPACITY, "decode workspace %zu bytes < required %zu", workspace_bytes, w.bytes);
+    BulkParams p{};
+    p.q = q; p.k = k_cache; p.v = v_cache; p.batch_stride = cache_stride;
+    p.seq_len = seq_len; p.k_new = const_cast<void*>(k_new); p.v_new = const_cast<void*>(v_new);
+    p.items = items; p.n_items = n_items; p.items_stride = items ? items_stride : 0;
+    p.B = batch; p.hq = hq; p.nsplit = sp;
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+    p.part_m = w.part_m; p.part_l = w.part_l; p.part_acc = w.part_acc;
+    return launch_decode_bulk(kv_dtype, d, hkv, G, sp, p, out, advance_len, cs, true);
+  }
+  int sp = items ? items_stride : decode_splits(batch, hkv, max_seq_len, d, G);
   SplitWs w = carve(workspace, batch, hq, hkv, sp, d);
   if (w.bytes > workspace_bytes)
     return fail(RK_ERR_CAPACITY, "decode workspace %zu bytes < required %zu (splits %d)", workspace_bytes,
@@ -302,7 +320,10 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
   p.part_m = w.part_m; p.part_l = w.part_l; p.part_acc = w.part_acc;
   p.counters = w.counters;
   dim3 grid(sp, batch, hkv);
-  return dispatch_split(kv_dtype, true, false, hq / hkv, sh, grid, reinterpret_cast<cudaStream_t>(stream), p);
+  st = dispatch_split(kv_dtype, true, false, G, sh, grid, cs, p);
+  if (st) return st;
+  if (advance_len) return rk_advance_lengths(advance_len, batch, 1, stream);
+  return RK_OK;
 }
 
 int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream) {

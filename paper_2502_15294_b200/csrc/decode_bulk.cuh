@@ -1,0 +1,31 @@
+// Host-side interface of the pipelined (cp.async.bulk + mbarrier) decode kernel.
+#pragma once
+
+#include "rk_common.cuh"
+
+namespace rk {
+
+struct BulkParams {
+  const float* q;          // [B][Hq][D]
+  const void* k;           // cache base, dialogue b at + b*batch_stride elements
+  const void* v;
+  int64_t batch_stride;
+  const int32_t* seq_len;  // [B] cached keys before this token
+  void* k_new;             // [B][HKV][D] appended row (or null)
+  void* v_new;
+  const int32_t* items;    // [B][items_stride][3] (lo, hi, bin) or null
+  const int32_t* n_items;
+  int items_stride;
+  int B, hq, nsplit;       // nsplit = partial slots per (dialogue, head)
+  float scale_log2;
+  float* part_m;           // [B][Hq][nsplit]
+  float* part_l;
+  float* part_acc;         // [B][Hq][nsplit][D]
+};
+
+bool bulk_supported(int kv_dtype, int d, int hkv, int G);
+int bulk_splits(int batch, int max_seq_len, int hkv);
+int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const BulkParams& p, float* out,
+                       int32_t* advance, cudaStream_t st, bool pdl);
+
+}  // namespace rk

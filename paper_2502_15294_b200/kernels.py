@@ -29,7 +29,7 @@ def decode_workspace(batch: int, hq: int, hkv: int, d: int, splits: int, device,
 def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, seq_len: torch.Tensor,
                      max_seq_len: int, *, k_new=None, v_new=None, items=None, n_items=None,
                      out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
-                     stream=None) -> torch.Tensor:
+                     advance: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Batched single-token attention over contiguous per-dialogue caches.
 
     q (B, Hq, d) f32; k_cache/v_cache (B, S_cap, Hkv, d) or (S_cap, Hkv, d) for
@@ -48,12 +48,12 @@ def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tens
         out = torch.empty((B, hq, d), dtype=torch.float32, device=q.device)
     items_stride = 0 if items is None else items.shape[1]
     if ws is None:
-        splits = items_stride if items is not None else 128
+        splits = items_stride if items is not None else 148
         ws = decode_workspace(B, hq, hkv, d, splits, q.device)
     _lib.call("rk_decode_attention", _lib.ptr(q), B, hq, d, _lib.ptr(k_cache), _lib.ptr(v_cache),
               kv_code(k_cache), hkv, stride, _lib.ptr(seq_len), int(max_seq_len), _lib.ptr(k_new),
               _lib.ptr(v_new), _lib.ptr(items), _lib.ptr(n_items), items_stride, _lib.ptr(out),
-              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
+              _lib.ptr(advance), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
     return out
 
 
