@@ -1,0 +1,280 @@
+"""Round-Attention decode benchmark (B200, sm_100a).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4]
+                    [--batch B] [--decode-steps T] [--impl ours|reference]
+
+A "step" is one serving TURN for every dialogue on the GPU: the question token
+through the lower layers with fused watershed scoring (layer Lw-1), device
+round selection, the kept rounds' deep-layer KV gathered from pinned host
+memory, the question's upper layers, then T answer tokens through all L
+layers (BASELINE.json north star).  `value` = decode tokens/s
+of the whole job (B * (T + 1) tokens per turn per GPU, summed over GPUs) with
+per-token activations already in HBM; `e2e` = the same with every token's
+q/k/v read from pinned host memory and every layer's attention output written
+back to host inside the timed region.  Dialogues are independent: each rank
+runs its own batch (weak scaling, no collective on the data path).
+
+Under torchrun (N > 1) every rank runs its own engine; rank 0 prints ONE JSON
+line with the max-over-ranks device time.  `--impl reference` times the
+reference's own CPU kernel (oracle/_ref, else the C port) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+WORKLOADS = {
+    # Llama-3-8B-shaped GQA, 32 rounds x 512 tokens, single-token decode (BASELINE configs[1]);
+    # 16 independent dialogues per GPU (a point of the configs[4] batch sweep); --batch 1 for one dialogue
+    "c2": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512, batch=16,
+               decode_steps=128, host_unique=4),
+    # Qwen2-7B-shaped, 64 rounds x 1K tokens (decode path; multi-row scoring lives in tests/kernels)
+    "c3": dict(num_layers=28, watershed=10, hq=28, hkv=4, head_dim=128, rounds=64, round_tokens=1024, batch=1,
+               decode_steps=128, host_unique=0),
+    # Llama-3-8B-shaped 128K context, 16 dialogues, deep layers in pinned host memory
+    "c4": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=128, round_tokens=1024, batch=16,
+               decode_steps=64, host_unique=2),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--decode-steps", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the reference's CPU kernel on the host cores (rank 0)."""
+    if rank != 0:
+        return 0
+    from oracle import cpu_baseline, refkernel
+    w = dict(WORKLOADS[args.workload])
+    if args.batch:
+        w["batch"] = args.batch
+    kind = "reference" if refkernel.available() else "port"
+    k = _kept(w)
+    cores = os.cpu_count() or 1
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline.decode_tokens_per_s(kind, L=w["num_layers"], lw=w["watershed"], hq=w["hq"],
+                                             hkv=w["hkv"], d=w["head_dim"], rounds=w["rounds"],
+                                             T=w["round_tokens"], K=k, processes=cores, seed=100 * i)
+        if i >= args.warmup:
+            samples.append(r)
+    tps = sum(s["tokens_per_s"] for s in samples) / len(samples)
+    sample = (f"{cores} dialogues x 1 decode token per step ({args.workload} shapes, GQA expanded to MHA), "
+              f"one process per core; {args.steps} steps")
+    line = {
+        "metric": "decode tokens/s", "value": tps, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * samples[-1]["wall_s"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp32 KV)", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{args.workload}: reference CPU decode path", "parallelism": f"{cores} processes"},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _kept(w):
+    from paper_2502_15294_b200.selection import top_k_count
+    return top_k_count(w["rounds"], 0.10, 1)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_15294_b200.decode_engine import EngineConfig, RoundDecodeEngine
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = dict(WORKLOADS[args.workload])
+    if args.batch:
+        w["batch"] = args.batch
+    if args.decode_steps:
+        w["decode_steps"] = args.decode_steps
+    cfg = EngineConfig(**w)
+    eng = RoundDecodeEngine(cfg, seed=1000 * rank)
+    eng.prepare(e2e=not args.no_e2e)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(e2e: bool, k: int):
+        for _ in range(args.warmup):
+            eng.run_turn(e2e=e2e)
+        barrier()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        breakdown = []
+        h2d = 0
+        with ClockSampler(local) as clk:
+            start.record(eng.compute_stream)
+            for _ in range(k):
+                _, nb = eng.run_turn(e2e=e2e)
+                h2d += nb
+            end.record(eng.compute_stream)
+            torch.cuda.synchronize()
+        breakdown.append(eng.turn_breakdown_ms())
+        barrier()
+        ms = start.elapsed_time(end)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, clk.summary(), breakdown[-1], h2d // max(k, 1)
+
+    ms, clocks, brk, h2d_bytes = timed(False, args.steps)
+    tokens_per_turn = cfg.batch * eng.turn_tokens
+    value = world * tokens_per_turn * args.steps / (ms / 1000.0)
+
+    e2e = None
+    if not args.no_e2e:
+        ms_e, _, brk_e, h2d_e = timed(True, args.steps)
+        step_in = eng.turn_tokens * (eng.q_in[0].numel() * 4 + eng.kv_in[0].numel() * 2)
+        step_out = (eng.turn_tokens - 1) * eng.out.numel() * 4
+        e2e = {"value": world * tokens_per_turn * args.steps / (ms_e / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out + eng.writeback.numel() * 2
+                                                                                      + eng.kept_host.numel() * 4),
+               "ms_per_step": ms_e / args.steps, "breakdown_ms": brk_e}
+
+    # roofline of the dominant kernel (bulk decode + merge) from the timed turns:
+    # decode-loop time per token vs algorithmic KV bytes per token
+    peak, peak_kind = measured_peaks()
+    dec_ms_per_tok = brk["decode"] / (eng.turn_tokens - 1)
+    bytes_tok = eng.kv_bytes_per_token()
+    achieved = bytes_tok / (dec_ms_per_tok / 1000.0) / 1e9
+    resident, full = eng.gpu_kv_bytes()
+
+    line = {
+        "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16 KV, fp32 accumulate", "data": "synthetic (random KV + activations)",
+        "config": {"workload": f"{args.workload}: L={cfg.num_layers} Lw={cfg.watershed} Hq={cfg.hq} "
+                               f"Hkv={cfg.hkv} d={cfg.head_dim} rounds={cfg.rounds}x{cfg.round_tokens} "
+                               f"K={eng.K} batch/GPU={cfg.batch} tokens/turn={eng.turn_tokens}",
+                   "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
+                   "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
+        "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "rk decode attention (bulk decode + merge), per token-step",
+                     "bytes_per_token": bytes_tok, "peak_source": peak_kind},
+        "h2d": {"bytes_per_turn": h2d_bytes, "ms": brk["h2d"],
+                "GBps": h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None},
+        "gpu_kv_saved": {"resident_bytes": resident, "full_cache_bytes": full, "saved_frac": 1 - resident / full},
+        "breakdown_ms": brk,
+        "clocks": clocks,
+        "kept_dialogue0": [int(x) for x in eng.last_kept[0]],
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import cpu_baseline, refkernel
+            kind = "reference" if refkernel.available() else "port"
+            cores = os.cpu_count() or 1
+            r = cpu_baseline.decode_tokens_per_s(kind, L=cfg.num_layers, lw=cfg.watershed, hq=cfg.hq,
+                                                 hkv=cfg.hkv, d=cfg.head_dim, rounds=cfg.rounds,
+                                                 T=cfg.round_tokens, K=eng.K, processes=cores)
+            line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": cores, "kind": kind,
+                                    "sample": f"{cores} dialogues x 1 decode token ({args.workload} shapes), "
+                                              f"one process per core, wall {r['wall_s']:.1f}s"}
+        except Exception as exc:  # the GPU number stands on its own
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

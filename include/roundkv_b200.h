@@ -127,8 +127,8 @@ int rk_round_scores(const float* q, int n_q, int hq, int d,
 
 /* Finalise scores left by rk_decode_attention(items != NULL): one dialogue
  * row per batch entry; raw_out [batch][n_bins] (inactive bins -> 0). */
-int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int items_stride, const int32_t* items,
-                             const int32_t* n_items, int n_bins, const uint8_t* active,
+int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int kv_dtype, int items_stride,
+                             const int32_t* items, const int32_t* n_items, int n_bins, const uint8_t* active,
                              double* raw_out, void* workspace, rk_stream_t stream);
 
 /* Eq. 1 on a materialised capture matrix (stats.py:59-94 on the device):
@@ -151,6 +151,12 @@ int rk_aggregate_rounds(const double* scores, int64_t ld, int row_lo, int row_hi
 int rk_select(const double* raw, int n, int normalize, int kind, double v, int k_top, double kappa,
               double* masses_out, int32_t* kept_out, int32_t* n_kept_out,
               int32_t* degenerate_out, int32_t* status_out, rk_stream_t stream);
+
+/* Batched form for B independent dialogues: row b of raw/masses/kept starts
+ * at b*ld; n_kept/degenerate/status are [batch]. One block per dialogue. */
+int rk_select_batch(const double* raw, int n, int ld, int batch, int normalize, int kind, double v,
+                    int k_top, double kappa, double* masses_out, int32_t* kept_out, int32_t* n_kept_out,
+                    int32_t* degenerate_out, int32_t* status_out, rk_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * 5. Batched host->HBM gather of kept rounds' upper-layer blocks

@@ -119,8 +119,10 @@ __global__ void advance_kernel(int32_t* len, int n, int delta) {
 // inactive, as the reference's row normalisation); massn = mass / rowsum.
 // mode 0 (multi-row question): massn -> rowmass[row][bin] then summed over rows;
 // mode 1 (batched decode): massn -> raw[row][bin] directly.
+// slots: partial slots per item (warps per kv-head of the bulk decode kernel,
+// 1 for the split kernel); slot of (item, slice) = item * slots + slice.
 __global__ void score_rows_kernel(const float* __restrict__ part_m, const float* __restrict__ part_l,
-                                  int nsplit, int hq, const int32_t* __restrict__ items, int items_stride,
+                                  int nsplit, int slots, int hq, const int32_t* __restrict__ items, int items_stride,
                                   const int32_t* __restrict__ n_items_dev, int n_items_static, int n_bins,
                                   const uint8_t* __restrict__ active, double* __restrict__ out_rows) {
   extern __shared__ double sh[];
@@ -133,11 +135,12 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
   int n_items = n_items_dev ? n_items_dev[items_stride ? row : 0] : n_items_static;
   const float* pm = part_m + (size_t)row * hq * nsplit;
   const float* pl = part_l + (size_t)row * hq * nsplit;
+  const int n_slots = n_items * slots;
   for (int h = threadIdx.x; h < hq; h += blockDim.x) {
     float mx = -INFINITY;
-    for (int it = 0; it < n_items; ++it) mx = fmaxf(mx, pm[h * nsplit + it]);
+    for (int it = 0; it < n_slots; ++it) mx = fmaxf(mx, pm[h * nsplit + it]);
     double L = 0.0;
-    for (int it = 0; it < n_items; ++it)
+    for (int it = 0; it < n_slots; ++it)
       L += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - mx);
     Mh[h] = mx;
     Lh[h] = (float)L;
@@ -154,7 +157,7 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
     double acc = 0.0;
     for (int h = 0; h < hq; ++h) {
       double hs = 0.0;
-      for (int it = bin_lo[b]; it < bin_lo[b + 1]; ++it)
+      for (int it = bin_lo[b] * slots; it < bin_lo[b + 1] * slots; ++it)
         hs += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - Mh[h]);
       acc += hs / (double)Lh[h];
     }
@@ -366,22 +369,25 @@ int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int k
   st = dispatch_split(kv_dtype, false, true, hq / hkv, sh, grid, cs, p);
   if (st) return st;
   score_rows_kernel<<<n_q, 128, score_rows_smem(n_bins, hq), cs>>>(
-      w.part_m, w.part_l, n_items, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
+      w.part_m, w.part_l, n_items, 1, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
   RK_CHECK_LAUNCH("score_rows_kernel");
   score_sum_rows_kernel<<<(n_bins + 127) / 128, 128, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
   RK_CHECK_LAUNCH("score_sum_rows_kernel");
   return RK_OK;
 }
 
-int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int items_stride, const int32_t* items,
-                             const int32_t* n_items, int n_bins, const uint8_t* active, double* raw_out,
-                             void* workspace, rk_stream_t stream) {
+int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int kv_dtype, int items_stride,
+                             const int32_t* items, const int32_t* n_items, int n_bins, const uint8_t* active,
+                             double* raw_out, void* workspace, rk_stream_t stream) {
   if (batch <= 0 || n_bins <= 0) return RK_OK;
   if (items == nullptr || n_items == nullptr || items_stride <= 0)
     return fail(RK_ERR_DOMAIN, "finalize needs the item table used by rk_decode_attention");
-  SplitWs w = carve(workspace, batch, hq, hkv, items_stride, d);
+  // same partial-slot layout rk_decode_attention used for this shape
+  const int slots = bulk_supported(kv_dtype, d, hkv, hq / hkv) ? 8 / hkv : 1;
+  const int nsplit = items_stride * slots;
+  SplitWs w = carve(workspace, batch, hq, hkv, nsplit, d);
   score_rows_kernel<<<batch, 128, score_rows_smem(n_bins, hq), reinterpret_cast<cudaStream_t>(stream)>>>(
-      w.part_m, w.part_l, items_stride, hq, items, items_stride, n_items, 0, n_bins, active, raw_out);
+      w.part_m, w.part_l, nsplit, slots, hq, items, items_stride, n_items, 0, n_bins, active, raw_out);
   RK_CHECK_LAUNCH("score_rows_kernel");
   return RK_OK;
 }

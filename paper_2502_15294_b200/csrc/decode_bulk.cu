@@ -18,52 +18,9 @@
 #include <cmath>
 #include <type_traits>
 
-#include "decode_bulk.cuh"
+#include "decode_common.cuh"
 
 namespace rk {
-
-constexpr int kConsumerWarps = 8;
-constexpr int kBulkThreads = (kConsumerWarps + 1) * 32;
-constexpr int kStages = 3;
-constexpr int kStageBytes = 32768;   // per operand (K or V) per stage
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32)); }
 
 template <typename T>
 __device__ __forceinline__ void lds8(const T* p, float2 (&out)[4]);
@@ -83,16 +40,6 @@ __device__ __forceinline__ void lds8<float>(const float* p, float2 (&out)[4]) {
   out[2] = make_float2(b.x, b.y);
   out[3] = make_float2(b.z, b.w);
 }
-
-constexpr int kMaxBatch = 1024;
-
-// Work segments of one CTA.  Uniform mode: the key ranges of all dialogues are
-// concatenated (length W) and CTA c owns [c*W/N, (c+1)*W/N) — one wave, equal
-// work per SM whatever the batch — split at dialogue boundaries.  Item mode:
-// CTA (x, b) owns item x of dialogue b (round-aligned, for fused scoring).
-struct Seg {
-  int b, lo, hi;
-};
 
 template <typename T, int D, int G, int HKV>
 __global__ void __launch_bounds__(kBulkThreads, 1) decode_bulk_kernel(const __grid_constant__ BulkParams p) {
@@ -115,59 +62,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_bulk_kernel(const __gr
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   T* newrow = reinterpret_cast<T*>(empty + kStages);   // [2][ROW] appended K,V row
-  __shared__ int s_pref[kMaxBatch + 1];
-  __shared__ Seg s_seg[kMaxBatch];
-  __shared__ int s_nseg;
-
+  __shared__ SegTable segs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool append = p.k_new != nullptr;
-
-  // ---- segments (lengths are stable while this kernel can run; see header)
-  if (p.items) {
-    if (threadIdx.x == 0) {
-      const int b = blockIdx.y, x = blockIdx.x;
-      s_nseg = 0;
-      if (x < p.n_items[b]) {
-        const int32_t* it = p.items + ((size_t)b * p.items_stride + x) * 3;
-        const int len = p.seq_len[b] + (append ? 1 : 0);
-        s_seg[0] = Seg{b, it[0], min((int)it[1], len)};
-        s_nseg = 1;
-      }
-    }
-  } else {
-    for (int i = threadIdx.x; i < p.B; i += blockDim.x) s_pref[i + 1] = p.seq_len[i] + (append ? 1 : 0);
-    __syncthreads();
-    if (warp == 0) {          // inclusive scan of the lengths
-      int carry = 0;
-      for (int base = 0; base < p.B; base += 32) {
-        int v = (base + lane < p.B) ? s_pref[base + lane + 1] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int t = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += t;
-        }
-        if (base + lane < p.B) s_pref[base + lane + 1] = v + carry;
-        carry += __shfl_sync(0xffffffffu, v, 31);
-      }
-      if (lane == 0) s_pref[0] = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int64_t W = s_pref[p.B], N = gridDim.x, c = blockIdx.x;
-      const int r0 = (int)(c * W / N), r1 = (int)((c + 1) * W / N);
-      int n = 0;
-      int lo = 0, hi = p.B;                    // first b with s_pref[b+1] > r0
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (s_pref[mid + 1] > r0) hi = mid; else lo = mid + 1;
-      }
-      for (int b = lo; b < p.B && s_pref[b] < r1; ++b) {
-        const int a0 = max(r0, s_pref[b]) - s_pref[b], a1 = min(r1, s_pref[b + 1]) - s_pref[b];
-        if (a0 < a1) s_seg[n++] = Seg{b, a0, a1};
-      }
-      s_nseg = n;
-    }
-  }
+  compute_segments(p, segs);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -176,7 +74,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_bulk_kernel(const __gr
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int nseg = s_nseg;
+  const Seg* s_seg = segs.seg;
+  const int nseg = segs.nseg;
   const int slot_base = (p.items ? blockIdx.x : blockIdx.x) * P;
 
   if (warp == kConsumerWarps) {
@@ -371,7 +270,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_bulk_kernel(const __gr
 // Merge the partial slots of (dialogue b, q-head h):
 //   out = sum_s acc_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
 // Uniform mode recomputes which CTAs overlapped dialogue b from the lengths
-// (same flattened partition as the decode kernel); item mode uses n_items[b].
+// (same flattened partition as the decode kernels); their slots are
+// contiguous.  Item mode uses n_items[b].  8 warps split the slots, lanes own
+// 4 consecutive dims, 4 slots' loads are issued together.
 // advance (nullable): advance[b] += 1 (lengths of the next step).
 __global__ void __launch_bounds__(256) decode_merge_kernel(const float* __restrict__ part_m,
                                                            const float* __restrict__ part_l,
@@ -386,14 +287,15 @@ __global__ void __launch_bounds__(256) decode_merge_kernel(const float* __restri
   if (advance == nullptr) pdl_trigger();
   pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __shared__ int s_c0, s_c1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = 8;
+  __shared__ int s_c0, s_c1, s_sparse;
   __shared__ int64_t s_W, s_P0, s_P1;
-  __shared__ float s_m;
-  __shared__ float s_l[8];
-  __shared__ __align__(16) float s_acc[8][256];
+  __shared__ float s_red[NW];
+  __shared__ __align__(16) float s_acc[NW][256];
+  __shared__ float s_l[NW];
   if (n_items) {
-    if (threadIdx.x == 0) { s_c0 = 0; s_c1 = n_items[b] - 1; }
+    if (threadIdx.x == 0) { s_c0 = 0; s_c1 = n_items[b] - 1; s_sparse = 0; }
   } else {
     int64_t before = 0, all = 0;
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
@@ -401,76 +303,81 @@ __global__ void __launch_bounds__(256) decode_merge_kernel(const float* __restri
       all += L;
       if (i < b) before += L;
     }
-    __shared__ int64_t red[2][256];
-    red[0][threadIdx.x] = before;
-    red[1][threadIdx.x] = all;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-      if (threadIdx.x < o) {
-        red[0][threadIdx.x] += red[0][threadIdx.x + o];
-        red[1][threadIdx.x] += red[1][threadIdx.x + o];
-      }
-      __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
     }
+    __shared__ int64_t red[2][NW];
+    if (lane == 0) { red[0][warp] = before; red[1][warp] = all; }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      const int64_t W = red[1][0], P0 = red[0][0], P1 = P0 + seq_len[b] + append, N = ncta;
+      int64_t P0 = 0, W = 0;
+      for (int w = 0; w < NW; ++w) { P0 += red[0][w]; W += red[1][w]; }
+      const int64_t P1 = P0 + seq_len[b] + append, N = ncta;
       s_W = W; s_P0 = P0; s_P1 = P1;
-      s_c0 = (int)min((long long)(N - 1), (long long)(((P0 + 1) * N - 1) / W));
-      s_c1 = (int)min((long long)(N - 1), (long long)((P1 * N - 1) / W));
+      s_c0 = W > 0 ? (int)min((long long)(N - 1), (long long)(((P0 + 1) * N - 1) / W)) : 0;
+      s_c1 = W > 0 ? (int)min((long long)(N - 1), (long long)((P1 * N - 1) / W)) : -1;
+      s_sparse = W < N;          // some CTAs own empty ranges: check each slot
     }
   }
   __syncthreads();
-  const int c0 = s_c0, c1 = s_c1;
-  const int64_t slot0 = ((int64_t)b * hq + h) * nsplit;
-  auto live = [&](int c) {
-    if (n_items) return true;
-    const int64_t r0 = (int64_t)c * s_W / ncta, r1 = (int64_t)(c + 1) * s_W / ncta;
+  const int c0 = s_c0, c1 = s_c1, sparse = s_sparse;
+  const int64_t base = ((int64_t)b * hq + h) * nsplit + (int64_t)c0 * slices;
+  const int nslot = (c1 - c0 + 1) * slices;
+  auto live = [&](int k) {
+    if (!sparse) return true;
+    const int64_t c = c0 + k / slices;
+    const int64_t r0 = c * s_W / ncta, r1 = (c + 1) * s_W / ncta;
     return max(r0, s_P0) < min(r1, s_P1);
   };
-  // max over live slots
   float mx = -INFINITY;
-  for (int c = c0 + threadIdx.x / slices; c <= c1; c += blockDim.x / slices)
-    if (threadIdx.x < (blockDim.x / slices) * slices && live(c)) mx = fmaxf(mx, part_m[slot0 + c * slices + threadIdx.x % slices]);
+  for (int k = threadIdx.x; k < nslot; k += blockDim.x)
+    if (live(k)) mx = fmaxf(mx, part_m[base + k]);
   mx = group_max<32>(mx);
-  if (lane == 0) s_l[warp] = mx;
+  if (lane == 0) s_red[warp] = mx;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float v = -INFINITY;
-    for (int w = 0; w < nw; ++w) v = fmaxf(v, s_l[w]);
-    s_m = v;
-  }
-  __syncthreads();
-  const float M = s_m, mu = (M == -INFINITY) ? 0.f : M;
-  // warp w accumulates slots w, w + nw, ...; lane owns d elements lane*4.. (+128)
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) M = fmaxf(M, s_red[w]);
+  const float mu = (M == -INFINITY) ? 0.f : M;
   float ls = 0.f;
   float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-  const int nslot = (c1 - c0 + 1) * slices;
-  for (int k = warp; k < nslot; k += nw) {
-    const int c = c0 + k / slices;
-    if (!live(c)) continue;
-    const int64_t sl = slot0 + c * slices + k % slices;
-    const float w = fast_exp2(part_m[sl] - mu);
-    ls += part_l[sl] * w;
-    const float4* src = reinterpret_cast<const float4*>(part_acc + sl * d);
-    if (lane * 4 < d) {
-      float4 v = src[lane];
-      a0.x += v.x * w; a0.y += v.y * w; a0.z += v.z * w; a0.w += v.w * w;
+  const bool d0 = lane * 4 < d, d1 = lane * 4 + 128 < d;
+  for (int k0 = warp; k0 < nslot; k0 += 4 * NW) {
+    float wgt[4], lv[4];
+    float4 v0[4], v1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u * NW;
+      const bool ok = k < nslot && live(k);
+      const int64_t sl = base + (ok ? k : 0);
+      wgt[u] = ok ? part_m[sl] : -INFINITY;
+      lv[u] = ok ? part_l[sl] : 0.f;
+      const float4* src = reinterpret_cast<const float4*>(part_acc + sl * d);
+      v0[u] = (ok && d0) ? src[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      v1[u] = (ok && d1) ? src[lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (lane * 4 + 128 < d) {
-      float4 v = src[lane + 32];
-      a1.x += v.x * w; a1.y += v.y * w; a1.z += v.z * w; a1.w += v.w * w;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float w = fast_exp2(wgt[u] - mu);
+      ls += lv[u] * w;
+      a0.x += v0[u].x * w; a0.y += v0[u].y * w; a0.z += v0[u].z * w; a0.w += v0[u].w * w;
+      a1.x += v1[u].x * w; a1.y += v1[u].y * w; a1.z += v1[u].z * w; a1.w += v1[u].w * w;
     }
   }
   if (lane == 0) s_l[warp] = ls;
-  if (lane * 4 < d) *reinterpret_cast<float4*>(&s_acc[warp][lane * 4]) = a0;
-  if (lane * 4 + 128 < d) *reinterpret_cast<float4*>(&s_acc[warp][lane * 4 + 128]) = a1;
+  if (d0) *reinterpret_cast<float4*>(&s_acc[warp][lane * 4]) = a0;
+  if (d1) *reinterpret_cast<float4*>(&s_acc[warp][lane * 4 + 128]) = a1;
   __syncthreads();
   float L = 0.f;
-  for (int w = 0; w < nw; ++w) L += s_l[w];
+#pragma unroll
+  for (int w = 0; w < NW; ++w) L += s_l[w];
   const float inv = 1.f / L;
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     float as = 0.f;
-    for (int w = 0; w < nw; ++w) as += s_acc[w][e];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) as += s_acc[w][e];
     out[((int64_t)b * hq + h) * d + e] = as * inv;
   }
   if (advance && h == 0 && threadIdx.x == 0) advance[b] += 1;
@@ -548,8 +455,7 @@ int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const Bu
   cudaError_t e = cudaSuccess;
   int r;
   if (kv_dtype == RK_BF16)
-    r = d == 64 ? bulk_by_hkv<__nv_bfloat16, 64>(hkv, G, grid, st, p, pdl, &e)
-                : bulk_by_hkv<__nv_bfloat16, 128>(hkv, G, grid, st, p, pdl, &e);
+    r = launch_decode_mma(d, hkv, G, grid, p, st, pdl, &e);
   else
     r = d == 64 ? bulk_by_hkv<float, 64>(hkv, G, grid, st, p, pdl, &e)
                 : bulk_by_hkv<float, 128>(hkv, G, grid, st, p, pdl, &e);

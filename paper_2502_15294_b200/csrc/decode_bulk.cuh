@@ -25,6 +25,8 @@ struct BulkParams {
 
 bool bulk_supported(int kv_dtype, int d, int hkv, int G);
 int bulk_splits(int batch, int max_seq_len, int hkv);
+int launch_decode_mma(int d, int hkv, int G, dim3 grid, const BulkParams& p, cudaStream_t st, bool pdl,
+                      cudaError_t* e);
 int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const BulkParams& p, float* out,
                        int32_t* advance, cudaStream_t st, bool pdl);
 

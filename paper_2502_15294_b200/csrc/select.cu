@@ -39,10 +39,17 @@ __device__ double pw_sum(const F& f, int lo, int n) {
 
 constexpr int kSelMax = 16384;
 
-__global__ void select_kernel(const double* __restrict__ raw, int n, int normalize, int kind, double v, int k_top,
-                              double kappa, double* __restrict__ masses, int32_t* __restrict__ kept,
+// one block per distribution (blockIdx.x = batch row, rows `ld` apart)
+__global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int normalize, int kind, double v,
+                              int k_top, double kappa, double* __restrict__ masses, int32_t* __restrict__ kept,
                               int32_t* __restrict__ n_kept, int32_t* __restrict__ degenerate,
                               int32_t* __restrict__ status) {
+  raw += (size_t)blockIdx.x * ld;
+  masses += (size_t)blockIdx.x * ld;
+  kept += (size_t)blockIdx.x * ld;
+  n_kept += blockIdx.x;
+  degenerate += blockIdx.x;
+  status += blockIdx.x;
   __shared__ double s_total, s_cut;
   __shared__ int s_neg, s_any;
   __shared__ unsigned char flag[kSelMax];
@@ -148,7 +155,19 @@ int rk_select(const double* raw, int n, int normalize, int kind, double v, int k
   if (n < 0 || n > kSelMax) return fail(RK_ERR_DOMAIN, "selection over %d rounds (max %d)", n, kSelMax);
   if (kind < RK_SEL_FIXED || kind > RK_SEL_ALL) return fail(RK_ERR_DOMAIN, "selection kind %d unknown", kind);
   select_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      raw, n, normalize, kind, v, k_top, kappa, masses_out, kept_out, n_kept_out, degenerate_out, status_out);
+      raw, n, n, normalize, kind, v, k_top, kappa, masses_out, kept_out, n_kept_out, degenerate_out, status_out);
+  RK_CHECK_LAUNCH("select_kernel");
+  return RK_OK;
+}
+
+int rk_select_batch(const double* raw, int n, int ld, int batch, int normalize, int kind, double v, int k_top,
+                    double kappa, double* masses_out, int32_t* kept_out, int32_t* n_kept_out,
+                    int32_t* degenerate_out, int32_t* status_out, rk_stream_t stream) {
+  if (n < 0 || n > kSelMax || ld < n) return fail(RK_ERR_DOMAIN, "selection over %d rounds (max %d)", n, kSelMax);
+  if (kind < RK_SEL_FIXED || kind > RK_SEL_ALL) return fail(RK_ERR_DOMAIN, "selection kind %d unknown", kind);
+  if (batch <= 0) return RK_OK;
+  select_kernel<<<batch, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      raw, n, ld, normalize, kind, v, k_top, kappa, masses_out, kept_out, n_kept_out, degenerate_out, status_out);
   RK_CHECK_LAUNCH("select_kernel");
   return RK_OK;
 }

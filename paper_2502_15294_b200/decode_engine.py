@@ -1,0 +1,381 @@
+"""Batched round-sparse decode engine: one GPU, B independent dialogues.
+
+This is the B200 restatement of one serving turn of `RoundPipeline.run_turn`
+(pipeline.py:192-394) for large GQA configurations, driven by synthetic
+activations (no projections: the attention path of SURVEY.md §8a, as in the
+CPU-baseline composition of BASELINE.md §3):
+
+  1. lower layers [0, Lw) hold every round's KV in HBM
+     (`lower`  [B][Lw][K|V][S_lo][Hkv][d]);
+     upper layers [Lw, L) of every round live in pinned host memory, one
+     contiguous block per round ([L-Lw][K|V][T][Hkv][d], store.py:225-242);
+  2. the question token runs the lower layers; at layer Lw-1 the decode kernel
+     works on round-aligned items and leaves per-round softmax statistics,
+     finalised into Eq. 1 masses (pipeline.py:225-245) — no capture matrix;
+  3. rk_select_batch picks the kept rounds bit-exactly (selection.py:87-97),
+     and the K ids come back to the host (the API returns a host tuple);
+  4. rk_h2d_gather copies the kept rounds' upper KV into the per-dialogue
+     working cache (`upper` [B][L-Lw][K|V][S_up][Hkv][d]) on a copy stream, one
+     event per upper layer, so upper layer l starts as soon as its rows land
+     (store.fetch_upper :254-263 + _assemble :158-169);
+  5. the question's upper layers, then `steps` decode tokens over all L
+     layers, replayed from a CUDA graph (pipeline.py:298-313);
+  6. the new round's upper rows are written back to pinned host memory
+     (writeback_upper :265-278).
+
+All attention runs in librk's pipelined bulk-copy decode kernel; the only
+host round trip per turn is the kept-round ids.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, kernels
+from .selection import SelectionPolicy, top_k_count
+
+
+@dataclass
+class EngineConfig:
+    num_layers: int = 32
+    watershed: int = 5            # L_w: layers [0, L_w) stay in HBM; scoring at L_w - 1
+    hq: int = 32
+    hkv: int = 8
+    head_dim: int = 128
+    rounds: int = 32              # prior rounds in the history
+    round_tokens: int = 512       # tokens per prior round
+    batch: int = 1                # dialogues on this GPU
+    decode_steps: int = 128       # answer tokens per turn (after the question token)
+    policy: SelectionPolicy = field(default_factory=lambda: SelectionPolicy("top_percent", fraction=0.10))
+    host_unique: int = 0          # distinct host round sets (0 = one per dialogue); >0 aliases
+    item_chunk: int = 1024        # keys per scoring work item (round-aligned)
+    input_period: int = 8         # distinct synthetic step inputs, cycled
+    plant: int = 2                # rounds per dialogue with planted relevance at L_w-1 (0 = none)
+    plant_beta: float = 0.25
+
+    @property
+    def group(self) -> int:
+        return self.hq // self.hkv
+
+
+def _ptr_array(values) -> np.ndarray:
+    return np.asarray(values, dtype=np.uint64)
+
+
+class RoundDecodeEngine:
+    def __init__(self, cfg: EngineConfig, device: str = "cuda", seed: int = 0):
+        self.cfg = c = cfg
+        self.dev = torch.device(device)
+        if c.policy.kind != "top_percent":
+            raise ValueError("the batched engine sizes its working cache for top_percent selection")
+        self.dtype = torch.bfloat16
+        L, lw, B, T, R = c.num_layers, c.watershed, c.batch, c.round_tokens, c.rounds
+        self.L_up = L - lw
+        self.K = top_k_count(R, c.policy.fraction, c.policy.min_rounds)
+        self.hist = R * T
+        self.turn_tokens = 1 + c.decode_steps                 # question token + answer tokens
+        self.s_lo = self.hist + self.turn_tokens
+        self.s_up = self.K * T + self.turn_tokens
+        self.row = c.hkv * c.head_dim                         # elements per key (all heads)
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        gd = torch.Generator(device=self.dev).manual_seed(seed + 1)
+
+        # ---- HBM tiers
+        self.lower = torch.empty((B, lw, 2, self.s_lo, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        self.upper = torch.zeros((B, self.L_up, 2, self.s_up, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        self.lower[:, :, :, : self.hist].normal_(generator=gd)
+        # ---- pinned host tier: one contiguous upper block per (dialogue set, round)
+        n_sets = B if c.host_unique <= 0 else min(B, c.host_unique)
+        self.host_sets = n_sets
+        self.host_blocks = []
+        pool = torch.randn(1 << 24, generator=g).to(self.dtype)         # 32 MiB of bf16 noise
+        offs = torch.randint(0, 1 << 23, (n_sets * R,), generator=g).tolist()
+        for u in range(n_sets):
+            blocks = []
+            for r in range(R):
+                blk = torch.empty((self.L_up, 2, T, c.hkv, c.head_dim), dtype=self.dtype, pin_memory=True)
+                flat = blk.view(-1)
+                o = offs[u * R + r]
+                for s0 in range(0, flat.numel(), 1 << 23):       # distinct window of the pool per block
+                    n = min(1 << 23, flat.numel() - s0)
+                    flat[s0:s0 + n].copy_(pool[o:o + n])
+                blocks.append(blk)
+            self.host_blocks.append(blocks)
+        self.writeback = torch.empty((B, self.L_up, 2, self.turn_tokens, c.hkv, c.head_dim), dtype=self.dtype,
+                                     pin_memory=True)
+
+        # ---- lengths (device) and their per-turn reset values
+        self.lower_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
+        self.upper_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
+        self.lower_len0 = torch.full((B,), self.hist, dtype=torch.int32, device=self.dev)
+        self.upper_len0 = torch.full((B,), self.K * T, dtype=torch.int32, device=self.dev)
+
+        # ---- round-aligned scoring items at layer L_w-1 (prior rounds + the question token)
+        bounds = [[(r * T, (r + 1) * T, r) for r in range(R)] + [(self.hist, self.hist + 1, R)]
+                  for _ in range(B)]
+        self.items, self.n_items = kernels.items_tensor(bounds, c.item_chunk, self.dev)
+        if self.items.shape[1] > 512:
+            raise ValueError("too many scoring items; raise item_chunk")
+
+        # ---- synthetic per-step activations (cycled with period input_period)
+        P = max(1, min(c.input_period, self.turn_tokens))
+        self.period = P
+        self.q_in = torch.randn((P, L, B, c.hq, c.head_dim), generator=gd, device=self.dev)
+        self.kv_in = torch.randn((P, L, 2, B, c.hkv, c.head_dim), generator=gd, device=self.dev).to(self.dtype)
+        self.out = torch.empty((L, B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+        if c.plant:
+            self._plant(gd)
+
+        # ---- scratch
+        self.raw = torch.empty((B, R), dtype=torch.float64, device=self.dev)
+        self.ws = kernels.decode_workspace(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8),
+                                           self.dev, tag="engine")
+        self.copy_stream = torch.cuda.Stream(self.dev)
+        self.compute_stream = torch.cuda.Stream(self.dev)
+        self.layer_events = [torch.cuda.Event() for _ in range(self.L_up)]
+        self.kept_host = torch.empty((B, R), dtype=torch.int32, pin_memory=True)
+        self.meta_host = torch.empty((3, B), dtype=torch.int32, pin_memory=True)
+        self.graph_a = None
+        self.graph_b = None
+        self.graph_b_e2e = None
+        self.graph_wb = None
+        self.last_kept = None
+        self.marks = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        self.copy_marks = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    # ------------------------------------------------------------------ data
+    def _plant(self, gd):
+        """Raise the question's attention on `plant` rounds per dialogue at layer
+        L_w-1: add beta * |k| * unit(mean_g q_g) to those rounds' keys, so the
+        K-boundary gap is wide (SURVEY.md §8d planted relevance)."""
+        c = self.cfg
+        lw1 = c.watershed - 1
+        q = self.q_in[0, lw1].view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)   # (B, Hkv, d)
+        u = q / q.norm(dim=-1, keepdim=True)
+        rng = np.random.default_rng(1234)
+        self.planted = []
+        for b in range(c.batch):
+            rs = sorted(rng.choice(c.rounds, size=min(c.plant, c.rounds), replace=False).tolist())
+            self.planted.append(rs)
+            for r in rs:
+                sl = self.lower[b, lw1, 0, r * c.round_tokens:(r + 1) * c.round_tokens].float()
+                sl += c.plant_beta * math.sqrt(c.head_dim) * u[b][None]
+                self.lower[b, lw1, 0, r * c.round_tokens:(r + 1) * c.round_tokens] = sl.to(self.dtype)
+
+    # ------------------------------------------------------------------ kernels
+    def _layer(self, l: int, step: int, advance: bool, items: bool = False):
+        c = self.cfg
+        p = step % self.period
+        if l < c.watershed:
+            kc, vc, ln = self.lower[:, l, 0], self.lower[:, l, 1], self.lower_len
+            cap = self.s_lo
+        else:
+            u = l - c.watershed
+            kc, vc, ln = self.upper[:, u, 0], self.upper[:, u, 1], self.upper_len
+            cap = self.s_up
+        kernels.decode_attention(self.q_in[p, l], kc, vc, ln, cap, k_new=self.kv_in[p, l, 0],
+                                 v_new=self.kv_in[p, l, 1], items=self.items if items else None,
+                                 n_items=self.n_items if items else None, out=self.out[l], ws=self.ws,
+                                 advance=ln if advance else None)
+
+    def launches_per_layer(self) -> int:
+        return 2                                            # decode + merge
+
+    def _phase_a(self):
+        """Question token through the lower layers, fused scoring, selection."""
+        c = self.cfg
+        self.lower_len.copy_(self.lower_len0)
+        self.upper_len.copy_(self.upper_len0)
+        for l in range(c.watershed):
+            self._layer(l, 0, advance=(l == c.watershed - 1), items=(l == c.watershed - 1))
+        kernels.decode_scores_finalize(c.batch, c.hq, c.hkv, c.head_dim, self.items, self.n_items, c.rounds,
+                                       self.ws, raw=self.raw, kv_dtype=self.dtype)
+        self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(
+            self.raw, "top_percent", k_top=self.K)
+
+    def _phase_b1(self, layer_wait: bool):
+        """Question token through the upper layers (each waits for its rows)."""
+        c = self.cfg
+        for l in range(c.watershed, c.num_layers):
+            if layer_wait:
+                torch.cuda.current_stream().wait_event(self.layer_events[l - c.watershed])
+            self._layer(l, 0, advance=(l == c.num_layers - 1))
+
+    def _phase_b2(self, e2e: bool = False):
+        """Answer tokens: all L layers per token."""
+        c = self.cfg
+        for t in range(1, self.turn_tokens):
+            if e2e:
+                p = t % self.period
+                self.q_in[p].copy_(self.host_q[p], non_blocking=True)
+                self.kv_in[p].copy_(self.host_kv[p], non_blocking=True)
+            for l in range(c.num_layers):
+                self._layer(l, t, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
+            if e2e:
+                self.host_out[t].copy_(self.out, non_blocking=True)
+
+    def _phase_wb(self):
+        """Writeback of the new round's upper rows to pinned host memory
+        (store.writeback_upper, pipeline.py:324-325): one strided D2H."""
+        self.writeback.copy_(self.upper[:, :, :, self.K * self.cfg.round_tokens:], non_blocking=True)
+
+    # ------------------------------------------------------------------ gather
+    def gather_plan(self, kept: np.ndarray):
+        """Per upper layer: (src, spitch, dst, dpitch, width, height) arrays, one
+        2-row (K, V) strided copy per (dialogue, kept round)."""
+        c = self.cfg
+        es = 2
+        T = c.round_tokens
+        width = T * self.row * es
+        spitch = width
+        dpitch = self.s_up * self.row * es
+        plans = []
+        for u in range(self.L_up):
+            srcs, dsts = [], []
+            for b in range(c.batch):
+                hs = b % self.host_sets
+                for i, r in enumerate(kept[b]):
+                    blk = self.host_blocks[hs][int(r)]
+                    srcs.append(blk.data_ptr() + u * 2 * T * self.row * es)
+                    dsts.append(self.upper[b, u, 0, i * T].data_ptr())
+            n = len(srcs)
+            plans.append(dict(n=n, src=_ptr_array(srcs), dst=_ptr_array(dsts),
+                              spitch=np.full(n, spitch, np.uint64), dpitch=np.full(n, dpitch, np.uint64),
+                              width=np.full(n, width, np.uint64), height=np.full(n, 2, np.uint64)))
+        return plans
+
+    def issue_gather(self, plans):
+        """rk_h2d_gather per upper layer on the copy stream, one event per layer."""
+        vp = C.c_void_p
+        s = self.copy_stream
+        total = 0
+        for u, pl in enumerate(plans):
+            ev = self.layer_events[u]
+            _lib.call("rk_h2d_gather", pl["n"], pl["src"].ctypes.data_as(vp), pl["spitch"].ctypes.data_as(vp),
+                      pl["dst"].ctypes.data_as(vp), pl["dpitch"].ctypes.data_as(vp), pl["width"].ctypes.data_as(vp),
+                      pl["height"].ctypes.data_as(vp), s.cuda_stream, ev.cuda_event)
+            total += int((pl["width"] * pl["height"]).sum())
+        return total
+
+    # ------------------------------------------------------------------ turn
+    def prepare(self, e2e: bool = False):
+        """Warm up (module attributes, workspace) and capture the CUDA graphs."""
+        c = self.cfg
+        if e2e and not hasattr(self, "host_q"):
+            self.host_q = torch.empty(self.q_in.shape, dtype=self.q_in.dtype, pin_memory=True)
+            self.host_q.copy_(self.q_in)
+            self.host_kv = torch.empty(self.kv_in.shape, dtype=self.kv_in.dtype, pin_memory=True)
+            self.host_kv.copy_(self.kv_in)
+            self.host_out = torch.empty((self.turn_tokens,) + tuple(self.out.shape), dtype=torch.float32,
+                                        pin_memory=True)
+        with torch.cuda.stream(self.compute_stream):
+            self.run_turn_eager()                     # warm-up, sets kernel attributes
+            torch.cuda.synchronize()
+            if self.graph_a is None:
+                self.graph_a = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph_a, stream=self.compute_stream):
+                    self._phase_a()
+                self.graph_b = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph_b, stream=self.compute_stream):
+                    self._phase_b2(e2e=False)
+                self.graph_wb = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph_wb, stream=self.compute_stream):
+                    self._phase_wb()
+            if e2e and self.graph_b_e2e is None:
+                self.graph_b_e2e = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self.graph_b_e2e, stream=self.compute_stream):
+                    self._phase_b2(e2e=True)
+        torch.cuda.synchronize()
+
+    def _select_to_host(self):
+        self.kept_host.copy_(self.kept_pos, non_blocking=True)
+        self.meta_host.copy_(self.sel_meta, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if int(self.meta_host[2].abs().sum()) != 0:
+            raise RuntimeError("selection reported a negative raw mass")
+        kept = []
+        for b in range(self.cfg.batch):
+            n = int(self.meta_host[0, b])
+            kept.append(self.kept_host[b, :n].numpy().copy())
+        return kept
+
+    def run_turn_eager(self):
+        """Whole turn without graphs (first call / debugging)."""
+        self._phase_a()
+        kept = self._select_to_host()
+        self.copy_stream.wait_stream(torch.cuda.current_stream())
+        self.issue_gather(self.gather_plan(kept))
+        self._phase_b1(layer_wait=True)
+        self._phase_b2()
+        self._phase_wb()
+        self.last_kept = kept
+        return kept
+
+    def run_turn(self, e2e: bool = False):
+        """One turn on the compute stream with the captured graphs.  Returns the
+        kept rounds per dialogue (host) and the H2D bytes moved.  Timing marks
+        (compute stream): 0 start, 1 after scoring+select, 2 after the
+        question's upper layers, 3 after the decode tokens, 4 after writeback;
+        copy_marks bracket the H2D gather on the copy stream."""
+        m = self.marks
+        with torch.cuda.stream(self.compute_stream):
+            m[0].record()
+            if e2e:
+                # the question token's inputs come from pinned host memory too
+                self.q_in[0].copy_(self.host_q[0], non_blocking=True)
+                self.kv_in[0].copy_(self.host_kv[0], non_blocking=True)
+            self.graph_a.replay()
+            m[1].record()
+            kept = self._select_to_host()
+            self.copy_stream.wait_stream(self.compute_stream)
+            plans = self.gather_plan(kept)
+            self.copy_marks[0].record(self.copy_stream)
+            nbytes = self.issue_gather(plans)
+            self.copy_marks[1].record(self.copy_stream)
+            self._phase_b1(layer_wait=True)
+            m[2].record()
+            (self.graph_b_e2e if e2e else self.graph_b).replay()
+            m[3].record()
+            self.graph_wb.replay()
+            m[4].record()
+        self.last_kept = kept
+        return kept, nbytes
+
+    def turn_breakdown_ms(self) -> dict:
+        """Elapsed times of the last turn (call after synchronising)."""
+        m = self.marks
+        return dict(score_select=m[0].elapsed_time(m[1]), gather_upper_prefill=m[1].elapsed_time(m[2]),
+                    decode=m[2].elapsed_time(m[3]), writeback=m[3].elapsed_time(m[4]),
+                    turn=m[0].elapsed_time(m[4]), h2d=self.copy_marks[0].elapsed_time(self.copy_marks[1]))
+
+    def kernel_launches_per_turn(self) -> int:
+        c = self.cfg
+        per_layer = 2                                   # bulk decode + merge
+        return (c.num_layers * per_layer * self.turn_tokens   # question token + answer tokens
+                + 2)                                    # score finalize + batched select
+
+    # ------------------------------------------------------------------ accounting
+    def kv_bytes_per_token(self) -> int:
+        """Algorithmic attention bytes of one decode token (all dialogues, all
+        layers): K and V of every visible key, SURVEY.md §8d."""
+        c = self.cfg
+        es = 2
+        mid = self.turn_tokens // 2
+        lower = c.watershed * (self.hist + mid) * self.row * 2 * es
+        upper = self.L_up * (self.K * c.round_tokens + mid) * self.row * 2 * es
+        return c.batch * (lower + upper)
+
+    def gpu_kv_bytes(self) -> tuple[int, int]:
+        """(resident KV bytes of the round engine, full-cache bytes) at turn end."""
+        c = self.cfg
+        es = 2
+        full = c.batch * c.num_layers * 2 * (self.hist + self.turn_tokens) * self.row * es
+        resident = c.batch * 2 * self.row * es * (c.watershed * (self.hist + self.turn_tokens)
+                                                   + self.L_up * (self.K * c.round_tokens + self.turn_tokens))
+        return resident, full

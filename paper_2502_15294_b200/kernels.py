@@ -59,14 +59,29 @@ def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tens
 
 def decode_scores_finalize(batch: int, hq: int, hkv: int, d: int, items: torch.Tensor, n_items: torch.Tensor,
                            n_bins: int, ws: torch.Tensor, active=None, raw: torch.Tensor | None = None,
-                           stream=None) -> torch.Tensor:
+                           kv_dtype: torch.dtype = torch.bfloat16, stream=None) -> torch.Tensor:
     """Per-dialogue raw round masses (B, n_bins) from the statistics a
-    decode_attention(items=...) call left in `ws`."""
+    decode_attention(items=...) call left in `ws` (same kv dtype / shape)."""
     if raw is None:
         raw = torch.empty((batch, n_bins), dtype=torch.float64, device=items.device)
-    _lib.call("rk_round_scores_finalize", batch, hq, hkv, d, items.shape[1], _lib.ptr(items), _lib.ptr(n_items),
-              n_bins, _lib.ptr(active), _lib.ptr(raw), _lib.ptr(ws), _lib.stream_ptr(stream))
+    code = _lib.RK_BF16 if kv_dtype == torch.bfloat16 else _lib.RK_F32
+    _lib.call("rk_round_scores_finalize", batch, hq, hkv, d, code, items.shape[1], _lib.ptr(items),
+              _lib.ptr(n_items), n_bins, _lib.ptr(active), _lib.ptr(raw), _lib.ptr(ws), _lib.stream_ptr(stream))
     return raw
+
+
+def select_batch(raw: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, normalize=True, stream=None):
+    """rk_select_batch over rows of a (B, n) float64 device tensor.  Returns
+    device (masses (B, n), kept (B, n) int32, meta (B, 3) int32 = n_kept,
+    degenerate, status)."""
+    B, n = raw.shape
+    masses = torch.empty((B, n), dtype=torch.float64, device=raw.device)
+    kept = torch.zeros((B, n), dtype=torch.int32, device=raw.device)
+    meta = torch.zeros((3, B), dtype=torch.int32, device=raw.device)
+    _lib.call("rk_select_batch", _lib.ptr(raw), n, raw.stride(0), B, 1 if normalize else 0, _lib.SEL_KINDS[kind],
+              float(v), int(k_top), float(kappa), _lib.ptr(masses), _lib.ptr(kept), _lib.ptr(meta[0]),
+              _lib.ptr(meta[1]), _lib.ptr(meta[2]), _lib.stream_ptr(stream))
+    return masses, kept, meta
 
 
 def advance_lengths(seq_len: torch.Tensor, delta: int = 1, stream=None) -> None:

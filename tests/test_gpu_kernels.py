@@ -169,9 +169,10 @@ def test_round_scores_vs_capture_aggregate(rng, n_q, G, dtype):
     np.testing.assert_allclose(raw.cpu().numpy(), ref, rtol=2e-5, atol=1e-9)
 
 
-def test_fused_decode_scoring_vs_oracle(rng):
+@pytest.mark.parametrize("hkv,G", [(8, 4), (4, 7), (2, 4)])
+def test_fused_decode_scoring_vs_oracle(rng, hkv, G):
     """Layer Lw-1 decode with round-aligned items = attention output + Eq. 1."""
-    B, hkv, G, d = 2, 8, 4, 128
+    B, d = 2, 128
     n_rounds = 12
     per_b = []
     lens_all = []
@@ -191,7 +192,7 @@ def test_fused_decode_scoring_vs_oracle(rng):
     items, n_items = kernels.items_tensor(bounds, 256, "cuda")
     ws = kernels.decode_workspace(B, hkv * G, hkv, d, items.shape[1], "cuda", tag="t_fused")
     out = kernels.decode_attention(q, kc, vc, sl, cap, k_new=kn, v_new=vn, items=items, n_items=n_items, ws=ws)
-    raw = kernels.decode_scores_finalize(B, hkv * G, hkv, d, items, n_items, n_rounds, ws)
+    raw = kernels.decode_scores_finalize(B, hkv * G, hkv, d, items, n_items, n_rounds, ws, kv_dtype=torch.bfloat16)
     for b in range(B):
         L = lens_all[b]
         kk = kc[b, : L + 1].float().cpu().numpy()
