@@ -201,6 +201,7 @@ def main():
             for _ in range(k):
                 _, nb = eng.run_turn(e2e=e2e)
                 h2d += nb
+            eng.compute_stream.wait_stream(eng.copy_stream)     # include the last writeback
             end.record(eng.compute_stream)
             torch.cuda.synchronize()
         breakdown.append(eng.turn_breakdown_ms())

@@ -138,13 +138,20 @@ class RoundDecodeEngine:
                                            self.dev, tag="engine")
         self.copy_stream = torch.cuda.Stream(self.dev)
         self.compute_stream = torch.cuda.Stream(self.dev)
+        # torch creates CUDA events lazily: record once so the handles exist
+        # before librk records them on the copy stream (rk_h2d_gather)
         self.layer_events = [torch.cuda.Event() for _ in range(self.L_up)]
+        for ev in self.layer_events:
+            ev.record(self.copy_stream)
+        self.decode_done = torch.cuda.Event()
+        self.decode_done.record(self.compute_stream)
+        torch.cuda.synchronize()
+        assert all(ev.cuda_event for ev in self.layer_events)
         self.kept_host = torch.empty((B, R), dtype=torch.int32, pin_memory=True)
         self.meta_host = torch.empty((3, B), dtype=torch.int32, pin_memory=True)
         self.graph_a = None
         self.graph_b = None
         self.graph_b_e2e = None
-        self.graph_wb = None
         self.last_kept = None
         self.marks = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         self.copy_marks = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -257,6 +264,7 @@ class RoundDecodeEngine:
         total = 0
         for u, pl in enumerate(plans):
             ev = self.layer_events[u]
+            assert ev.cuda_event, "gather event not created"
             _lib.call("rk_h2d_gather", pl["n"], pl["src"].ctypes.data_as(vp), pl["spitch"].ctypes.data_as(vp),
                       pl["dst"].ctypes.data_as(vp), pl["dpitch"].ctypes.data_as(vp), pl["width"].ctypes.data_as(vp),
                       pl["height"].ctypes.data_as(vp), s.cuda_stream, ev.cuda_event)
@@ -284,9 +292,6 @@ class RoundDecodeEngine:
                 self.graph_b = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self.graph_b, stream=self.compute_stream):
                     self._phase_b2(e2e=False)
-                self.graph_wb = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(self.graph_wb, stream=self.compute_stream):
-                    self._phase_wb()
             if e2e and self.graph_b_e2e is None:
                 self.graph_b_e2e = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self.graph_b_e2e, stream=self.compute_stream):
@@ -313,7 +318,11 @@ class RoundDecodeEngine:
         self.issue_gather(self.gather_plan(kept))
         self._phase_b1(layer_wait=True)
         self._phase_b2()
-        self._phase_wb()
+        self.decode_done.record()
+        self.copy_stream.wait_event(self.decode_done)
+        with torch.cuda.stream(self.copy_stream):
+            self._phase_wb()
+        torch.cuda.current_stream().wait_stream(self.copy_stream)
         self.last_kept = kept
         return kept
 
@@ -342,8 +351,13 @@ class RoundDecodeEngine:
             m[2].record()
             (self.graph_b_e2e if e2e else self.graph_b).replay()
             m[3].record()
-            self.graph_wb.replay()
-            m[4].record()
+            # writeback of the new round's upper rows on the copy stream: it
+            # overlaps the next turn's scoring; the next gather queues behind it
+            self.decode_done.record(self.compute_stream)
+        self.copy_stream.wait_event(self.decode_done)
+        with torch.cuda.stream(self.copy_stream):
+            self._phase_wb()
+            m[4].record(self.copy_stream)
         self.last_kept = kept
         return kept, nbytes
 
@@ -351,8 +365,8 @@ class RoundDecodeEngine:
         """Elapsed times of the last turn (call after synchronising)."""
         m = self.marks
         return dict(score_select=m[0].elapsed_time(m[1]), gather_upper_prefill=m[1].elapsed_time(m[2]),
-                    decode=m[2].elapsed_time(m[3]), writeback=m[3].elapsed_time(m[4]),
-                    turn=m[0].elapsed_time(m[4]), h2d=self.copy_marks[0].elapsed_time(self.copy_marks[1]))
+                    decode=m[2].elapsed_time(m[3]), writeback_copy_stream=m[3].elapsed_time(m[4]),
+                    turn=m[0].elapsed_time(m[3]), h2d=self.copy_marks[0].elapsed_time(self.copy_marks[1]))
 
     def kernel_launches_per_turn(self) -> int:
         c = self.cfg

@@ -1,0 +1,87 @@
+"""GPU parity of the batched round-sparse decode engine (one full turn):
+fused watershed scoring + device selection must pick the oracle's rounds
+bit-exactly, the H2D gather must assemble exactly the kept rounds' deep-layer
+KV, and the decode outputs after T tokens must match the oracle attention over
+(kept rounds + this turn's tokens) in the upper layers and the full history in
+the lower layers (pipeline.py:192-394 semantics)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import attention as oatt
+from oracle import rounds as orr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2502_15294_b200.decode_engine import EngineConfig, RoundDecodeEngine  # noqa: E402
+from paper_2502_15294_b200.selection import SelectionPolicy  # noqa: E402
+
+
+def _f(t):
+    return t.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+@pytest.mark.parametrize("hkv,G", [(2, 4), (4, 7)])
+def test_engine_turn_matches_oracle(graphs, hkv, G):
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=hkv * G, hkv=hkv, head_dim=128, rounds=7, round_tokens=64,
+                       batch=3, decode_steps=5, policy=SelectionPolicy("top_percent", fraction=0.3),
+                       item_chunk=32, input_period=3, plant=2, plant_beta=0.3)
+    eng = RoundDecodeEngine(cfg, seed=3)
+    lw, L, T, R = cfg.watershed, cfg.num_layers, cfg.round_tokens, cfg.rounds
+    lower0 = _f(eng.lower[:, :, :, : eng.hist])          # history before the turn
+    if graphs:
+        eng.prepare(e2e=False)
+        kept, _ = eng.run_turn()
+        kept, _ = eng.run_turn()                          # steady state: second replay
+    else:
+        with torch.cuda.stream(eng.compute_stream):
+            kept = eng.run_turn_eager()
+    torch.cuda.synchronize()
+    P = eng.period
+    steps = eng.turn_tokens
+    for b in range(cfg.batch):
+        # ---- selection: oracle capture at layer Lw-1 for the question token
+        q0 = _f(eng.q_in[0, lw - 1, b])[None]
+        kq = np.concatenate([lower0[b, lw - 1, 0], _f(eng.kv_in[0, lw - 1, 0, b])[None]])
+        _, cap = oatt.attention_forward_gqa(q0, kq, kq, [eng.hist], np.arange(eng.hist + 1), capture=True)
+        raw = np.array([cap[0, r * T:(r + 1) * T].sum() for r in range(R)])
+        want = orr.select(orr.normalize(raw), orr.SelectionPolicy("top_percent", fraction=0.3))
+        assert tuple(int(x) for x in kept[b]) == want
+        assert set(eng.planted[b]) <= set(want)
+        # ---- last token: lower layer 0 over history + the turn's rows, upper layer L-1 over kept + rows
+        tl = steps - 1
+        for l in (0, lw - 1, lw, L - 1):
+            rows_k = np.stack([_f(eng.kv_in[t % P, l, 0, b]) for t in range(steps)])
+            rows_v = np.stack([_f(eng.kv_in[t % P, l, 1, b]) for t in range(steps)])
+            if l < lw:
+                K = np.concatenate([lower0[b, l, 0], rows_k])
+                V = np.concatenate([lower0[b, l, 1], rows_v])
+            else:
+                hs = b % eng.host_sets
+                blocks = [eng.host_blocks[hs][int(r)][l - lw] for r in kept[b]]
+                K = np.concatenate([_f(bk[0]) for bk in blocks] + [rows_k])
+                V = np.concatenate([_f(bk[1]) for bk in blocks] + [rows_v])
+            q = _f(eng.q_in[tl % P, l, b])[None]
+            ref, _ = oatt.attention_forward_gqa(q, K, V, [len(K) - 1], np.arange(len(K)))
+            got = _f(eng.out[l, b]).reshape(1, -1)
+            err = np.abs(got - ref).max() / np.abs(ref).max()
+            assert err < 1e-4, (l, err)
+        # ---- writeback holds this turn's upper rows
+        wb = _f(eng.writeback[b])
+        up = _f(eng.upper[b, :, :, eng.K * T: eng.K * T + steps])
+        np.testing.assert_array_equal(wb, up)
+
+
+def test_engine_accounting():
+    cfg = EngineConfig(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512, batch=1,
+                       decode_steps=2, plant=0)
+    eng = RoundDecodeEngine(cfg)
+    resident, full = eng.gpu_kv_bytes()
+    assert 1 - resident / full > 0.54                      # >= 54 % GPU KV saved (north star)
+    assert eng.K == 4
