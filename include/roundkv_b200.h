@@ -92,7 +92,7 @@ int rk_attention_forward(const float* q, int n, int hq, int d,
  *    the previous call's merge runs, so a length array must not be advanced
  *    by the call immediately preceding a reader of the same array.
  *    Workspace: rk_decode_workspace_bytes(batch, hq, hkv, d, max_splits)
- *    (max_splits = max(items_stride, 148)), zero-filled once before first use.
+ *    (max_splits = max(items_stride * 8/hkv, 592)); no zeroing needed.
  * ---------------------------------------------------------------------- */
 size_t rk_decode_workspace_bytes(int batch, int hq, int hkv, int d, int max_splits);
 int rk_decode_attention(const float* q, int batch, int hq, int d,

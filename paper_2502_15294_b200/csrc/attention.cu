@@ -240,6 +240,8 @@ int rk_attention_forward(const float* q, int n, int hq, int d, const void* k, co
   p.counters = w.counters; p.bad_row = bad_row;
   p.stat_m = scores ? w.stat_m : nullptr;
   p.stat_l = scores ? w.stat_l : nullptr;
+  // the arrival counters must be zero; the arena is shared by calls of other shapes
+  RK_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(unsigned) * (size_t)n * hkv, cs), "counter reset");
   dim3 grid(sp, n, hkv);
   st = dispatch_split(kv_dtype, false, false, hq / hkv, sh, grid, cs, p);
   if (st) return st;
@@ -322,6 +324,7 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
   p.out = out;
   p.part_m = w.part_m; p.part_l = w.part_l; p.part_acc = w.part_acc;
   p.counters = w.counters;
+  RK_CUDA(cudaMemsetAsync(w.counters, 0, sizeof(unsigned) * (size_t)batch * hkv, cs), "counter reset");
   dim3 grid(sp, batch, hkv);
   st = dispatch_split(kv_dtype, true, false, G, sh, grid, cs, p);
   if (st) return st;
