@@ -1,0 +1,57 @@
+"""Multi-row watershed scoring at the C3 shape (Qwen2-7B-shaped layer Lw-1:
+Hq=28, Hkv=4, d=128, 64 rounds x 1024 history keys, n_q question rows).
+
+    python tools/bench_scoring.py [--nq 128,512,1024] [--json out.json]
+Run with RK_SCORE_TC=0 to time the CUDA-core split kernel instead.
+"""
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2502_15294_b200 import stats  # noqa: E402
+
+PEAK_TF = 1633.6          # MEASURED_PEAKS bf16 burst
+ap = argparse.ArgumentParser()
+ap.add_argument("--nq", default="128,512,1024")
+ap.add_argument("--rounds", type=int, default=64)
+ap.add_argument("--T", type=int, default=1024)
+ap.add_argument("--json")
+a = ap.parse_args()
+hq, hkv, d = 28, 4, 128
+rows = []
+for nq in [int(x) for x in a.nq.split(",")]:
+    hist = a.rounds * a.T
+    s = hist + nq
+    k = torch.randn(s, hkv, d, device="cuda").bfloat16()
+    q = torch.randn(nq, hq, d, device="cuda")
+    qp = torch.arange(hist, s, device="cuda")
+    kp = torch.arange(s, device="cuda")
+    bounds = [(r * a.T, (r + 1) * a.T, r) for r in range(a.rounds)] + [(hist, s, a.rounds)]
+    for _ in range(2):
+        stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = sorted(ts)[len(ts) // 2]
+    visible = nq * hist + nq * (nq + 1) / 2            # causal keys per head
+    flop = 2.0 * hq * d * nq * s                        # algorithmic QK^T (all tiles)
+    exps = hq * visible
+    r = dict(n_q=nq, keys=s, ms=ms, algo_tflops=flop / ms / 1e9, frac_bf16_peak=flop / ms / 1e9 / PEAK_TF,
+             tensor_tflops_issued=2 * flop / ms / 1e9, gexp_s=exps / ms / 1e6,
+             path="tcgen05" if os.environ.get("RK_SCORE_TC", "1") != "0" else "cuda-core")
+    rows.append(r)
+    print(json.dumps(r), flush=True)
+if a.json:
+    Path(a.json).write_text(json.dumps(rows, indent=1))
