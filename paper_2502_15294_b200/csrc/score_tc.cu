@@ -258,17 +258,19 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
         if (lane == 0) bar_arrive(&s_empty[buf]);    // TMEM buffer may be overwritten
         // causal / range mask: key j visible iff j < hi and pos(j) <= pos(row)
         const bool all_vis = (j0 + BN <= hi) && (p.k_pos[min(j0 + BN, hi) - 1] <= qpos);
-        if (!all_vis) {
+        float tmax = -INFINITY;
+        if (all_vis) {
+#pragma unroll
+          for (int i = 0; i < BN; ++i) tmax = fmaxf(tmax, sc[i]);
+        } else {
 #pragma unroll
           for (int i = 0; i < BN; ++i) {
             const int j = j0 + i;
-            const bool vis = j < hi && p.k_pos[min(j, hi - 1)] <= qpos;
+            const bool vis = j < hi && p.k_pos[j] <= qpos;
             sc[i] = vis ? sc[i] : -INFINITY;
+            tmax = fmaxf(tmax, sc[i]);
           }
         }
-        float tmax = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < BN; ++i) tmax = fmaxf(tmax, sc[i]);
         const float mn = fmaxf(m, tmax);
         const float mu = (mn == -INFINITY) ? 0.f : mn;
         float acc = l * fast_exp2(m - mu);
