@@ -35,8 +35,9 @@ sys.path.insert(0, str(REPO))
 
 WORKLOADS = {
     # Llama-3-8B-shaped GQA, 32 rounds x 512 tokens, single-token decode (BASELINE configs[1]);
-    # 16 independent dialogues per GPU (a point of the configs[4] batch sweep); --batch 1 for one dialogue
-    "c2": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512, batch=16,
+    # 32 independent dialogues per GPU served as 2 groups of 16 (8 GPUs x 32 = the 256-dialogue end of
+    # the configs[4] batch sweep); --batch 1 --groups 1 for a single dialogue
+    "c2": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512, batch=32,
                decode_steps=128, host_unique=4),
     # Qwen2-7B-shaped, 64 rounds x 1K tokens (decode path; multi-row scoring lives in tests/kernels)
     "c3": dict(num_layers=28, watershed=10, hq=28, hkv=4, head_dim=128, rounds=64, round_tokens=1024, batch=1,
@@ -58,6 +59,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--groups", type=int, default=None,
+                    help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
 
 
@@ -169,7 +172,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2502_15294_b200.decode_engine import EngineConfig, RoundDecodeEngine
+    from paper_2502_15294_b200.decode_engine import EngineConfig, GroupedDecoder
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -180,7 +183,8 @@ def main():
     if args.decode_steps:
         w["decode_steps"] = args.decode_steps
     cfg = EngineConfig(**w)
-    eng = RoundDecodeEngine(cfg, seed=1000 * rank)
+    groups = args.groups if args.groups else (2 if cfg.batch >= 2 and cfg.batch % 2 == 0 else 1)
+    eng = GroupedDecoder(cfg, groups=groups, seed=1000 * rank)
     eng.prepare(e2e=not args.no_e2e)
 
     def barrier():
@@ -189,48 +193,37 @@ def main():
         torch.cuda.synchronize()
 
     def timed(e2e: bool, k: int):
-        for _ in range(args.warmup):
-            eng.run_turn(e2e=e2e)
+        eng.run_turns(args.warmup, e2e=e2e)
         barrier()
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        breakdown = []
-        h2d = 0
         with ClockSampler(local) as clk:
-            start.record(eng.compute_stream)
-            for _ in range(k):
-                _, nb = eng.run_turn(e2e=e2e)
-                h2d += nb
-            eng.compute_stream.wait_stream(eng.copy_stream)     # include the last writeback
-            end.record(eng.compute_stream)
-            torch.cuda.synchronize()
-        breakdown.append(eng.turn_breakdown_ms())
+            ms, h2d, brk, kept = eng.run_turns(k, e2e=e2e)
         barrier()
-        ms = start.elapsed_time(end)
         if world > 1:
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, clk.summary(), breakdown[-1], h2d // max(k, 1)
+        return ms, clk.summary(), brk, h2d, kept
 
-    ms, clocks, brk, h2d_bytes = timed(False, args.steps)
+    ms, clocks, brk, h2d_bytes, kept0 = timed(False, args.steps)
     tokens_per_turn = cfg.batch * eng.turn_tokens
     value = world * tokens_per_turn * args.steps / (ms / 1000.0)
+    g0 = eng.groups[0]
 
     e2e = None
     if not args.no_e2e:
-        ms_e, _, brk_e, h2d_e = timed(True, args.steps)
-        step_in = eng.turn_tokens * (eng.q_in[0].numel() * 4 + eng.kv_in[0].numel() * 2)
-        step_out = (eng.turn_tokens - 1) * eng.out.numel() * 4
+        ms_e, _, brk_e, h2d_e, _ = timed(True, args.steps)
+        step_in = sum(e.turn_tokens * (e.q_in[0].numel() * 4 + e.kv_in[0].numel() * 2) for e in eng.groups)
+        step_out = sum((e.turn_tokens - 1) * e.out.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
+                       for e in eng.groups)
         e2e = {"value": world * tokens_per_turn * args.steps / (ms_e / 1000.0), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out + eng.writeback.numel() * 2
-                                                                                      + eng.kept_host.numel() * 4),
-               "ms_per_step": ms_e / args.steps, "breakdown_ms": brk_e}
+               "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out),
+               "ms_per_step": ms_e / args.steps, "breakdown_ms_group0": brk_e}
 
     # roofline of the dominant kernel (bulk decode + merge) from the timed turns:
     # decode-loop time per token vs algorithmic KV bytes per token
     peak, peak_kind = measured_peaks()
-    dec_ms_per_tok = brk["decode"] / (eng.turn_tokens - 1)
+    # decode kernels of all groups over the union of their decode windows (last turn)
+    dec_ms_per_tok = eng.last_decode_window_ms / (eng.turn_tokens - 1)
     bytes_tok = eng.kv_bytes_per_token()
     achieved = bytes_tok / (dec_ms_per_tok / 1000.0) / 1e9
     resident, full = eng.gpu_kv_bytes()
@@ -241,19 +234,21 @@ def main():
         "vs_baseline": None, "dtype": "bf16 KV, fp32 accumulate", "data": "synthetic (random KV + activations)",
         "config": {"workload": f"{args.workload}: L={cfg.num_layers} Lw={cfg.watershed} Hq={cfg.hq} "
                                f"Hkv={cfg.hkv} d={cfg.head_dim} rounds={cfg.rounds}x{cfg.round_tokens} "
-                               f"K={eng.K} batch/GPU={cfg.batch} tokens/turn={eng.turn_tokens}",
+                               f"K={g0.K} batch/GPU={cfg.batch} in {groups} groups tokens/turn={eng.turn_tokens}",
                    "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
                    "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "rk decode attention (bulk decode + merge), per token-step",
+                     "traffic": None, "kernel": "rk decode attention (bulk decode + merge): KV bytes of all groups' "
+                                                "decode tokens / union of their decode windows (CUDA events, last timed turn)",
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},
-        "h2d": {"bytes_per_turn": h2d_bytes, "ms": brk["h2d"],
-                "GBps": h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None},
+        "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],
+                "GBps": g0.last_h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None,
+                "link": "PCIe Gen5 x16 (~63 GB/s/dir theoretical)"},
         "gpu_kv_saved": {"resident_bytes": resident, "full_cache_bytes": full, "saved_frac": 1 - resident / full},
-        "breakdown_ms": brk,
+        "breakdown_ms_group0": brk,
         "clocks": clocks,
-        "kept_dialogue0": [int(x) for x in eng.last_kept[0]],
+        "kept_dialogue0": [int(x) for x in kept0[0]],
     }
     if e2e:
         line["e2e"] = e2e
@@ -264,7 +259,7 @@ def main():
             cores = os.cpu_count() or 1
             r = cpu_baseline.decode_tokens_per_s(kind, L=cfg.num_layers, lw=cfg.watershed, hq=cfg.hq,
                                                  hkv=cfg.hkv, d=cfg.head_dim, rounds=cfg.rounds,
-                                                 T=cfg.round_tokens, K=eng.K, processes=cores)
+                                                 T=cfg.round_tokens, K=g0.K, processes=cores)
             line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": cores, "kind": kind,
                                     "sample": f"{cores} dialogues x 1 decode token ({args.workload} shapes), "
                                               f"one process per core, wall {r['wall_s']:.1f}s"}

@@ -347,6 +347,7 @@ class RoundDecodeEngine:
             self.copy_marks[0].record(self.copy_stream)
             nbytes = self.issue_gather(plans)
             self.copy_marks[1].record(self.copy_stream)
+            self.last_h2d_bytes = nbytes
             self._phase_b1(layer_wait=True)
             m[2].record()
             (self.graph_b_e2e if e2e else self.graph_b).replay()
@@ -393,3 +394,82 @@ class RoundDecodeEngine:
         resident = c.batch * 2 * self.row * es * (c.watershed * (self.hist + self.turn_tokens)
                                                    + self.L_up * (self.K * c.round_tokens + self.turn_tokens))
         return resident, full
+
+
+class GroupedDecoder:
+    """B dialogues served as G independent groups, each a RoundDecodeEngine on
+    its own compute + copy streams, driven by one host thread per group.
+
+    A group's turn has one host round trip (the kept ids) and an H2D gather
+    that the decode cannot start without; with two or more groups in flight the
+    gather and selection of one group overlap the decode kernels of the others,
+    and the groups' programmatic-launch chains fill each other's per-layer
+    latency gaps.  Dialogues stay independent: no data crosses groups.
+    """
+
+    def __init__(self, cfg: EngineConfig, groups: int = 2, device: str = "cuda", seed: int = 0):
+        import dataclasses
+        if cfg.batch % groups:
+            raise ValueError(f"batch {cfg.batch} not divisible by groups {groups}")
+        sub = dataclasses.replace(cfg, batch=cfg.batch // groups,
+                                  host_unique=max(1, cfg.host_unique // groups) if cfg.host_unique else 0)
+        self.cfg = cfg
+        self.groups = [RoundDecodeEngine(sub, device=device, seed=seed + 97 * g) for g in range(groups)]
+
+    def prepare(self, e2e: bool = False):
+        for eng in self.groups:
+            eng.prepare(e2e=e2e)
+
+    def run_turns(self, turns: int, e2e: bool = False):
+        """`turns` turns of every group, groups concurrent.  Returns (device ms
+        from the first start to the last end, h2d bytes per turn (all groups),
+        group-0 breakdown, kept of group 0's last turn)."""
+        import threading
+        starts = [torch.cuda.Event(enable_timing=True) for _ in self.groups]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in self.groups]
+        h2d = [0] * len(self.groups)
+        errors = []
+
+        def work(g):
+            eng = self.groups[g]
+            try:
+                starts[g].record(eng.compute_stream)
+                for _ in range(turns):
+                    _, nb = eng.run_turn(e2e=e2e)
+                    h2d[g] += nb
+                eng.compute_stream.wait_stream(eng.copy_stream)
+                ends[g].record(eng.compute_stream)
+            except Exception as exc:  # surfaced in the caller
+                errors.append(exc)
+
+        torch.cuda.synchronize()
+        threads = [threading.Thread(target=work, args=(g,)) for g in range(len(self.groups))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+        torch.cuda.synchronize()
+        ref = starts[0]                                    # events are comparable across streams
+        ms = max(ref.elapsed_time(e) for e in ends) - min(ref.elapsed_time(s) for s in starts)
+        # decode window of the last turn: union of the groups' decode loops
+        d0 = min(ref.elapsed_time(e.marks[2]) for e in self.groups)
+        d1 = max(ref.elapsed_time(e.marks[3]) for e in self.groups)
+        self.last_decode_window_ms = d1 - d0
+        return ms, sum(h2d) // max(turns, 1), self.groups[0].turn_breakdown_ms(), self.groups[0].last_kept
+
+    # aggregate accounting over groups
+    @property
+    def turn_tokens(self):
+        return self.groups[0].turn_tokens
+
+    def kv_bytes_per_token(self):
+        return sum(e.kv_bytes_per_token() for e in self.groups)
+
+    def gpu_kv_bytes(self):
+        r = [e.gpu_kv_bytes() for e in self.groups]
+        return sum(x[0] for x in r), sum(x[1] for x in r)
+
+    def kernel_launches_per_turn(self):
+        return sum(e.kernel_launches_per_turn() for e in self.groups)
