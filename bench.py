@@ -173,6 +173,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2502_15294_b200.decode_engine import EngineConfig, GroupedDecoder
+    from paper_2502_15294_b200.sharding import dialogues_for_rank, max_over_ranks
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -183,8 +184,10 @@ def main():
     if args.decode_steps:
         w["decode_steps"] = args.decode_steps
     cfg = EngineConfig(**w)
+    # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
+    shard = dialogues_for_rank(cfg.batch * world, world, rank)
     groups = args.groups if args.groups else (2 if cfg.batch >= 2 and cfg.batch % 2 == 0 else 1)
-    eng = GroupedDecoder(cfg, groups=groups, seed=1000 * rank)
+    eng = GroupedDecoder(cfg, groups=groups, seed=1000 * shard[0])
     eng.prepare(e2e=not args.no_e2e)
 
     def barrier():
@@ -198,10 +201,7 @@ def main():
         with ClockSampler(local) as clk:
             ms, h2d, brk, kept = eng.run_turns(k, e2e=e2e)
         barrier()
-        if world > 1:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = max_over_ranks(ms)                  # the job ends with its slowest rank
         return ms, clk.summary(), brk, h2d, kept
 
     ms, clocks, brk, h2d_bytes, kept0 = timed(False, args.steps)
