@@ -222,7 +222,7 @@ def main():
     # roofline of the dominant kernel (bulk decode + merge) from the timed turns:
     # decode-loop time per token vs algorithmic KV bytes per token
     peak, peak_kind = measured_peaks()
-    # decode kernels of all groups over the union of their decode windows (last turn)
+    # decode kernels of all groups over the union of their decode windows (mean over the timed turns)
     dec_ms_per_tok = eng.last_decode_window_ms / (eng.turn_tokens - 1)
     bytes_tok = eng.kv_bytes_per_token()
     achieved = bytes_tok / (dec_ms_per_tok / 1000.0) / 1e9
@@ -240,7 +240,7 @@ def main():
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel": "rk decode attention (bulk decode + merge): KV bytes of all groups' "
-                                                "decode tokens / union of their decode windows (CUDA events, last timed turn)",
+                                                "decode tokens / union of their decode windows (CUDA events, mean over the timed turns)",
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},
         "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],
                 "GBps": g0.last_h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None,

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_bulk_kernel(const __gr
 // contiguous.  Item mode uses n_items[b].  8 warps split the slots, lanes own
 // 4 consecutive dims, 4 slots' loads are issued together.
 // advance (nullable): advance[b] += 1 (lengths of the next step).
-__global__ void __launch_bounds__(256) decode_merge_kernel(const float* __restrict__ part_m,
+__global__ void __launch_bounds__(128) decode_merge_kernel(const float* __restrict__ part_m,
                                                            const float* __restrict__ part_l,
                                                            const float* __restrict__ part_acc,
                                                            const int32_t* __restrict__ seq_len, int append,
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) decode_merge_kernel(const float* __restri
   pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NW = 8;
+  constexpr int NW = 4;      // 128 threads: fits beside a resident decode CTA (registers)
   __shared__ int s_c0, s_c1, s_sparse;
   __shared__ int64_t s_W, s_P0, s_P1;
   __shared__ float s_red[NW];
@@ -463,7 +463,7 @@ int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const Bu
   if (e != cudaSuccess) return cuda_status(e, "decode_bulk_kernel launch");
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.B, p.hq);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(128);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -63,6 +63,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // let the merge kernel become resident now: it only reads the partials after
+  // griddepcontrol.wait (full completion of this grid), so its launch latency
+  // hides under this kernel's streaming
+  pdl_trigger();
   const int nseg = segs.nseg;
   const __nv_bfloat16* kbase = reinterpret_cast<const __nv_bfloat16*>(p.k);
   const __nv_bfloat16* vbase = reinterpret_cast<const __nv_bfloat16*>(p.v);
@@ -238,7 +242,6 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
       }
     }
   }
-  pdl_trigger();
 }
 
 template <int D, int G, int HKV>

@@ -154,6 +154,7 @@ class RoundDecodeEngine:
         self.graph_b_e2e = None
         self.last_kept = None
         self.marks = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        self.window_log = None        # list of (start, end) decode-loop events per turn when enabled
         self.copy_marks = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
     # ------------------------------------------------------------------ data
@@ -350,8 +351,15 @@ class RoundDecodeEngine:
             self.last_h2d_bytes = nbytes
             self._phase_b1(layer_wait=True)
             m[2].record()
+            if self.window_log is not None:          # per-turn decode window (bench roofline)
+                a = torch.cuda.Event(enable_timing=True)
+                a.record(self.compute_stream)
             (self.graph_b_e2e if e2e else self.graph_b).replay()
             m[3].record()
+            if self.window_log is not None:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record(self.compute_stream)
+                self.window_log.append((a, b))
             # writeback of the new round's upper rows on the copy stream: it
             # overlaps the next turn's scoring; the next gather queues behind it
             self.decode_done.record(self.compute_stream)
@@ -442,6 +450,8 @@ class GroupedDecoder:
             except Exception as exc:  # surfaced in the caller
                 errors.append(exc)
 
+        for eng in self.groups:
+            eng.window_log = []
         torch.cuda.synchronize()
         threads = [threading.Thread(target=work, args=(g,)) for g in range(len(self.groups))]
         for t in threads:
@@ -453,10 +463,15 @@ class GroupedDecoder:
         torch.cuda.synchronize()
         ref = starts[0]                                    # events are comparable across streams
         ms = max(ref.elapsed_time(e) for e in ends) - min(ref.elapsed_time(s) for s in starts)
-        # decode window of the last turn: union of the groups' decode loops
-        d0 = min(ref.elapsed_time(e.marks[2]) for e in self.groups)
-        d1 = max(ref.elapsed_time(e.marks[3]) for e in self.groups)
-        self.last_decode_window_ms = d1 - d0
+        # decode window per turn index: union of the groups' decode loops, averaged over the turns
+        wins = []
+        for t in range(turns):
+            d0 = min(ref.elapsed_time(e.window_log[t][0]) for e in self.groups)
+            d1 = max(ref.elapsed_time(e.window_log[t][1]) for e in self.groups)
+            wins.append(d1 - d0)
+        self.last_decode_window_ms = sum(wins) / len(wins)
+        for eng in self.groups:
+            eng.window_log = None
         return ms, sum(h2d) // max(turns, 1), self.groups[0].turn_breakdown_ms(), self.groups[0].last_kept
 
     # aggregate accounting over groups
