@@ -227,6 +227,11 @@ def main():
     bytes_tok = eng.kv_bytes_per_token()
     achieved = bytes_tok / (dec_ms_per_tok / 1000.0) / 1e9
     resident, full = eng.gpu_kv_bytes()
+    traffic = None      # DRAM bytes per token-step from the committed ncu capture of this kernel (same shapes)
+    tp = REPO / "profiles" / "r01_traffic_c2_tokenstep.json"
+    if tp.exists() and args.workload == "c2":
+        t = json.loads(tp.read_text())
+        traffic = t["per_dialogue_token_bytes"] * cfg.batch
 
     line = {
         "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -239,7 +244,7 @@ def main():
                    "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "rk decode attention (bulk decode + merge): KV bytes of all groups' "
+                     "traffic": traffic, "kernel": "rk decode attention (bulk decode + merge): KV bytes of all groups' "
                                                 "decode tokens / union of their decode windows (CUDA events, mean over the timed turns)",
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},
         "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],
