@@ -222,10 +222,12 @@ def main():
     # roofline of the dominant kernel (bulk decode + merge) from the timed turns:
     # decode-loop time per token vs algorithmic KV bytes per token
     peak, peak_kind = measured_peaks()
-    # decode kernels of all groups over the union of their decode windows (mean over the timed turns)
-    dec_ms_per_tok = eng.last_decode_window_ms / (eng.turn_tokens - 1)
+    # decode kernels (bulk decode + merge) of all groups: algorithmic KV bytes of
+    # every timed decode token / the union of the decode-loop intervals on the
+    # device timeline (CUDA events on each group's compute stream)
     bytes_tok = eng.kv_bytes_per_token()
-    achieved = bytes_tok / (dec_ms_per_tok / 1000.0) / 1e9
+    achieved = eng.last_decode_bytes / (eng.last_decode_busy_ms / 1000.0) / 1e9
+    step_bw = bytes_tok * eng.turn_tokens * args.steps / (ms / 1000.0) / 1e9
     resident, full = eng.gpu_kv_bytes()
     traffic = None      # DRAM bytes per token-step from the committed ncu capture of this kernel (same shapes)
     tp = REPO / "profiles" / "r01_traffic_c2_tokenstep.json"
@@ -244,8 +246,10 @@ def main():
                    "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "rk decode attention (bulk decode + merge): KV bytes of all groups' "
-                                                "decode tokens / union of their decode windows (CUDA events, mean over the timed turns)",
+                     "traffic": traffic, "kernel": "rk decode attention (decode_mma + merge): KV bytes of every timed decode token / "
+                                                "union of the groups' decode-loop intervals (CUDA events)",
+                     "decode_busy_ms": eng.last_decode_busy_ms, "launches": eng.last_decode_launches,
+                     "whole_step_GBps": step_bw, "whole_step_frac": step_bw / peak,
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},
         "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],
                 "GBps": g0.last_h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None,

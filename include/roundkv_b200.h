@@ -178,6 +178,29 @@ int rk_d2h_scatter(int n, const void* const* src, const size_t* src_pitch,
                    const size_t* width, const size_t* height,
                    rk_stream_t stream, void* done_event);
 
+/* ------------------------------------------------------------------------
+ * 6. Question prefill attention on the tensor cores (tcgen05), with the
+ *    watershed round scoring fused in.  The multi-row form of section 1
+ *    (forward_range over the question rows, pipeline.py:225-230 lower layers
+ *    over the full history, :292-296 upper layers over kept + current; the
+ *    kernel contract _attn_ext.pyx:20-81) for bf16 K/V, head_dim 128 and
+ *    n_q * hq/hkv >= 64; rk_attention_forward uses the same kernel for those
+ *    shapes.  If raw_out is given, items [n_items][3] = (key_lo, key_hi, bin)
+ *    must be round-aligned and cover the keys (as for rk_round_scores) and
+ *    raw_out receives the Eq. 1 masses of the active bins
+ *    (aggregate_round_attention, stats.py:59-94) from the same pass — no
+ *    capture matrix, no second pass over K.  Without raw_out, items may be
+ *    NULL (uniform split).  bad_row: INT32_MAX or the first row with no
+ *    visible key (-> InvariantError).
+ * ---------------------------------------------------------------------- */
+size_t rk_prefill_workspace_bytes(int n_q, int hq, int hkv, int s, int d, int n_items, int n_bins);
+int rk_prefill_attention(const float* q, int n_q, int hq, int d,
+                         const void* k, const void* v, int kv_dtype, int s, int hkv,
+                         const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed,
+                         const int32_t* items, int n_items, int n_bins, const uint8_t* active,
+                         float* out, double* raw_out, int32_t* bad_row,
+                         void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,9 @@ _SIGS = {
     "rk_select_batch": (_i, [_p, _i, _i, _i, _i, _i, _d, _i, _d, _p, _p, _p, _p, _p, _p]),
     "rk_h2d_gather": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "rk_d2h_scatter": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "rk_prefill_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
+    "rk_prefill_attention": (_i, [_p, _i, _i, _i, _p, _p, _i, _i, _i, _p, _p, _p, _p, _i, _i, _p, _p, _p, _p, _p,
+                                  _sz, _p]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

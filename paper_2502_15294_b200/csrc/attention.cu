@@ -6,6 +6,7 @@
 
 #include "attn_dispatch.cuh"
 #include "decode_bulk.cuh"
+#include "prefill_tc.cuh"
 #include <cstdlib>
 
 namespace rk {
@@ -204,6 +205,34 @@ static size_t score_rows_smem(int n_bins, int hq) {
   return sizeof(double) * (n_bins + 1) + sizeof(float) * 2 * hq + sizeof(int) * (n_bins + 2);
 }
 
+// the tensor-core multi-row path (prefill_tc.cu) serves bf16 K/V, d = 128,
+// >= 64 stacked rows; RK_PREFILL_TC=0 forces the CUDA-core split kernel
+static bool use_prefill_tc(int kv_dtype, int d, int n, int G) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("RK_PREFILL_TC");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env && prefill_tc_supported(kv_dtype, d, n, G);
+}
+
+// capture matrix from merged (stat_m, stat_l): head-summed, row-normalised
+static int launch_capture(const float* q, int n, int hq, int hkv, int d, int s, const void* k, int kv_dtype,
+                          const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed, const float* stat_m,
+                          const float* stat_l, float scale_log2, double* scores, cudaStream_t cs) {
+  dim3 g2((s + 255) / 256, n);
+  if (kv_dtype == RK_F32)
+    capture_kernel<float><<<g2, 256, 0, cs>>>(q, (const float*)k, n, hq, hkv, d, s, q_pos, k_pos, allowed,
+                                             stat_m, stat_l, scale_log2, scores);
+  else
+    capture_kernel<__nv_bfloat16><<<g2, 256, 0, cs>>>(q, (const __nv_bfloat16*)k, n, hq, hkv, d, s, q_pos,
+                                                     k_pos, allowed, stat_m, stat_l, scale_log2, scores);
+  RK_CHECK_LAUNCH("capture_kernel");
+  rownorm_kernel<<<n, 256, 0, cs>>>(scores, s);
+  RK_CHECK_LAUNCH("rownorm_kernel");
+  return RK_OK;
+}
+
 }  // namespace rk
 
 using namespace rk;
@@ -213,7 +242,13 @@ extern "C" {
 size_t rk_attention_workspace_bytes(int n, int hq, int hkv, int s, int d) {
   if (n <= 0 || hq <= 0 || hkv <= 0 || d <= 0) return 256;
   int sp = general_splits(n, hkv, s, d, hq / hkv);
-  return carve(nullptr, n, hq, hkv, sp, d).bytes;
+  size_t a = carve(nullptr, n, hq, hkv, sp, d).bytes;
+  // the tensor-core path (bf16 K/V only; the kv dtype is not an argument here)
+  if (hq % hkv == 0 && prefill_tc_supported(RK_BF16, d, n, hq / hkv)) {
+    size_t b = prefill_plan(n, hq, hkv, s, 0, false).total;
+    if (b > a) a = b;
+  }
+  return a;
 }
 
 int rk_attention_forward(const float* q, int n, int hq, int d, const void* k, const void* v,
@@ -232,6 +267,17 @@ int rk_attention_forward(const float* q, int n, int hq, int d, const void* k, co
   if (n == 0) return RK_OK;
   if (s == 0) {
     if (bad_row) { fill_i32<<<1, 1, 0, cs>>>(bad_row, 0); RK_CHECK_LAUNCH("fill bad_row"); }
+    return RK_OK;
+  }
+  const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  if (use_prefill_tc(kv_dtype, d, n, hq / hkv)) {
+    // tensor-core multi-row path (prefill_tc.cu); statistics feed the capture
+    float *stat_m = nullptr, *stat_l = nullptr;
+    st = launch_prefill_tc(q, n, hq, k, v, s, hkv, q_pos, k_pos, allowed, nullptr, 0, false, out, bad_row,
+                           workspace, workspace_bytes, nullptr, nullptr, &stat_m, &stat_l, cs);
+    if (st) return st;
+    if (scores) return launch_capture(q, n, hq, hkv, d, s, k, kv_dtype, q_pos, k_pos, allowed, stat_m, stat_l,
+                                      scale_log2, scores, cs);
     return RK_OK;
   }
   int sp = general_splits(n, hkv, s, d, hq / hkv);
@@ -255,18 +301,9 @@ int rk_attention_forward(const float* q, int n, int hq, int d, const void* k, co
   dim3 grid(sp, n, hkv);
   st = dispatch_split(kv_dtype, false, false, hq / hkv, sh, grid, cs, p);
   if (st) return st;
-  if (scores) {
-    dim3 g2((s + 255) / 256, n);
-    if (kv_dtype == RK_F32)
-      capture_kernel<float><<<g2, 256, 0, cs>>>(q, (const float*)k, n, hq, hkv, d, s, q_pos, k_pos, allowed,
-                                               w.stat_m, w.stat_l, p.scale_log2, scores);
-    else
-      capture_kernel<__nv_bfloat16><<<g2, 256, 0, cs>>>(q, (const __nv_bfloat16*)k, n, hq, hkv, d, s, q_pos,
-                                                       k_pos, allowed, w.stat_m, w.stat_l, p.scale_log2, scores);
-    RK_CHECK_LAUNCH("capture_kernel");
-    rownorm_kernel<<<n, 256, 0, cs>>>(scores, s);
-    RK_CHECK_LAUNCH("rownorm_kernel");
-  }
+  if (scores)
+    return launch_capture(q, n, hq, hkv, d, s, k, kv_dtype, q_pos, k_pos, allowed, w.stat_m, w.stat_l,
+                          p.scale_log2, scores, cs);
   return RK_OK;
 }
 
@@ -423,6 +460,50 @@ int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int kv_dtype, in
   score_rows_kernel<<<batch, 128, score_rows_smem(n_bins, hq), reinterpret_cast<cudaStream_t>(stream)>>>(
       w.part_m, w.part_l, nsplit, slots, hq, items, items_stride, n_items, 0, n_bins, active, raw_out);
   RK_CHECK_LAUNCH("score_rows_kernel");
+  return RK_OK;
+}
+
+size_t rk_prefill_workspace_bytes(int n_q, int hq, int hkv, int s, int d, int n_items, int n_bins) {
+  if (n_q <= 0 || hq <= 0 || hkv <= 0 || d <= 0 || hq % hkv) return 256;
+  size_t a = prefill_plan(n_q, hq, hkv, s, n_items > 0 ? n_items : 0, n_bins > 0).total;
+  if (n_bins > 0) a = align_up(a + sizeof(double) * (size_t)n_q * n_bins, 256);
+  return a;
+}
+
+int rk_prefill_attention(const float* q, int n_q, int hq, int d, const void* k, const void* v, int kv_dtype,
+                         int s, int hkv, const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed,
+                         const int32_t* items, int n_items, int n_bins, const uint8_t* active, float* out,
+                         double* raw_out, int32_t* bad_row, void* workspace, size_t workspace_bytes,
+                         rk_stream_t stream) {
+  Shape sh;
+  int st = check_heads(hq, hkv, d, &sh);
+  if (st) return st;
+  if (n_q <= 0 || s <= 0) return fail(RK_ERR_DOMAIN, "prefill needs rows and keys");
+  if (!prefill_tc_supported(kv_dtype, d, n_q, hq / hkv))
+    return fail(RK_ERR_UNSUPPORTED, "prefill path needs bf16 K/V, head_dim 128 and >= 64 stacked rows");
+  const bool stats = raw_out != nullptr;
+  if (stats && (items == nullptr || n_items <= 0 || n_bins <= 0))
+    return fail(RK_ERR_DOMAIN, "round scoring needs the round-aligned item table and n_bins");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (bad_row) {
+    fill_i32<<<1, 1, 0, cs>>>(bad_row, INT_MAX);
+    RK_CHECK_LAUNCH("fill bad_row");
+  }
+  PrefillPlan pl = prefill_plan(n_q, hq, hkv, s, items ? n_items : 0, stats);
+  size_t need = stats ? align_up(pl.total + sizeof(double) * (size_t)n_q * n_bins, 256) : pl.total;
+  if (need > workspace_bytes) return fail(RK_ERR_CAPACITY, "prefill workspace %zu < %zu", workspace_bytes, need);
+  float *item_m = nullptr, *item_l = nullptr;
+  st = launch_prefill_tc(q, n_q, hq, k, v, s, hkv, q_pos, k_pos, allowed, items, items ? n_items : 0, stats, out,
+                         bad_row, workspace, pl.total, &item_m, &item_l, nullptr, nullptr, cs);
+  if (st) return st;
+  if (stats) {
+    double* rows_mass = reinterpret_cast<double*>(static_cast<char*>(workspace) + pl.total);
+    score_rows_kernel<<<n_q, 128, score_rows_smem(n_bins, hq), cs>>>(
+        item_m, item_l, n_items, 1, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
+    RK_CHECK_LAUNCH("score_rows_kernel");
+    score_sum_rows_kernel<<<(n_bins + 127) / 128, 128, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
+    RK_CHECK_LAUNCH("score_sum_rows_kernel");
+  }
   return RK_OK;
 }
 

@@ -20,12 +20,9 @@
 // query so the masses match the fp64 oracle to ~1e-6 relative.
 // Work unit = (M tile, item); units are dealt to CTAs as contiguous ranges so a
 // CTA reloads Q only when its range crosses an M tile.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <cmath>
 
-#include "rk_common.cuh"
+#include "tc_common.cuh"
 
 namespace rk {
 namespace tc {
@@ -47,71 +44,8 @@ struct Params {
   float* part_l;
 };
 
-__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void bar_init(uint64_t* b, unsigned n) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(n));
-}
-__device__ __forceinline__ void bar_expect(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra W_%=;\n}" ::"r"(sa(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(sa(dst)), "l"(map), "r"(c0), "r"(c1), "r"(sa(bar))
-      : "memory");
-}
-// K-major, SWIZZLE_128B canonical layout: 8-row groups 1024 B apart (SBO), LBO unused (1)
-__device__ __forceinline__ uint64_t umma_desc(const void* p) {
-  uint64_t d = 0;
-  d |= (uint64_t)((sa(p) >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset
-  d |= (uint64_t)1 << 46;                           // version (sm100)
-  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
-  return d;
-}
-// kind::f16 instruction descriptor: F32 accumulate, BF16 A/B, K-major, N=128, M=128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(tmem_d), "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(addr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
+// kind::f16, F32 accumulate, BF16 A/B, both K-major, M = N = 128
+constexpr uint32_t kIdesc = idesc_f16(BM, BN);
 
 // unit u -> (mtile, item); mtile = kvh * mtiles + mt
 __device__ __forceinline__ void unit_of(const Params& p, int u, int& mtile, int& item) {
@@ -219,7 +153,7 @@ score_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
             for (int k = 0; k < BK / 16; ++k) {
               const uint8_t* a = qs + (2 * hl + k / 4) * SUB + 32 * (k % 4);
               const uint8_t* b = ks + s * KT_BYTES + (k / 4) * SUB + 32 * (k % 4);
-              umma(d, umma_desc(a), umma_desc(b), (hl | k) ? 1u : 0u);
+              umma(d, umma_desc(a), umma_desc(b), kIdesc, (hl | k) ? 1u : 0u);
             }
           umma_commit(&k_empty[s]);                 // smem stage free when these MMAs finish
           umma_commit(&s_full[buf]);                // scores ready for the epilogue
@@ -312,34 +246,6 @@ __global__ void prep_q_kernel(const float* __restrict__ q, int n_q, int hq, int 
     qs[(((int64_t)kvh * 2 + 0) * mpad + R) * BK + e] = h;
     qs[(((int64_t)kvh * 2 + 1) * mpad + R) * BK + e] = l;
   }
-}
-
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// 2-D bf16 map: inner = `inner` elements (row pitch `pitch_bytes`), outer = rows;
-// box = 64 elements x 128 rows, 128-byte swizzle
-static int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch_bytes) {
-  auto fn = encode_fn();
-  if (!fn) return fail(RK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {inner, rows};
-  cuuint64_t strides[1] = {pitch_bytes};
-  cuuint32_t box[2] = {64, 128};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(RK_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return RK_OK;
 }
 
 }  // namespace tc

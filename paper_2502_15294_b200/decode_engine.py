@@ -463,13 +463,24 @@ class GroupedDecoder:
         torch.cuda.synchronize()
         ref = starts[0]                                    # events are comparable across streams
         ms = max(ref.elapsed_time(e) for e in ends) - min(ref.elapsed_time(s) for s in starts)
-        # decode window per turn index: union of the groups' decode loops, averaged over the turns
-        wins = []
-        for t in range(turns):
-            d0 = min(ref.elapsed_time(e.window_log[t][0]) for e in self.groups)
-            d1 = max(ref.elapsed_time(e.window_log[t][1]) for e in self.groups)
-            wins.append(d1 - d0)
-        self.last_decode_window_ms = sum(wins) / len(wins)
+        # decode-busy time: the union on the device timeline of every group's
+        # decode-loop intervals over the timed turns (groups drift against each
+        # other, so intervals are merged on the timeline, not per turn index)
+        iv = sorted((ref.elapsed_time(a), ref.elapsed_time(b)) for e in self.groups for (a, b) in e.window_log)
+        busy, cur0, cur1 = 0.0, None, None
+        for a, b in iv:
+            if cur1 is None or a > cur1:
+                if cur1 is not None:
+                    busy += cur1 - cur0
+                cur0, cur1 = a, b
+            else:
+                cur1 = max(cur1, b)
+        if cur1 is not None:
+            busy += cur1 - cur0
+        self.last_decode_busy_ms = busy
+        self.last_decode_bytes = turns * sum((e.turn_tokens - 1) * e.kv_bytes_per_token() for e in self.groups)
+        self.last_decode_launches = turns * sum(e.cfg.num_layers * e.launches_per_layer() * (e.turn_tokens - 1)
+                                                for e in self.groups)
         for eng in self.groups:
             eng.window_log = None
         return ms, sum(h2d) // max(turns, 1), self.groups[0].turn_breakdown_ms(), self.groups[0].last_kept

@@ -111,3 +111,35 @@ def items_tensor(per_dialogue_bounds, chunk: int, device) -> tuple[torch.Tensor,
         arr[i, : len(p)] = p
     counts = np.array([len(p) for p in packs], dtype=np.int32)
     return torch.from_numpy(arr).to(device), torch.from_numpy(counts).to(device)
+
+
+def prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: torch.Tensor, k_pos: torch.Tensor,
+                      *, allowed: torch.Tensor | None = None, items: torch.Tensor | None = None, n_bins: int = 0,
+                      active: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                      raw: torch.Tensor | None = None, bad_row: torch.Tensor | None = None, stream=None):
+    """Question-prefill attention on the tensor cores (rk_prefill_attention).
+
+    q (n_q, Hq, 128) f32; k/v (S, Hkv, 128) bf16; q_pos (n_q,) / k_pos (S,)
+    int64 device; allowed (S,) uint8 or None.  With `items` ((n_items, 3)
+    int32 round-aligned (lo, hi, bin)) and n_bins > 0 the Eq. 1 masses of the
+    active bins come back in `raw` (float64) from the same pass.  Returns
+    (out (n_q, Hq, 128) f32, raw or None, bad_row (1,) int32 device).
+    """
+    n_q, hq, d = q.shape
+    s, hkv = k.shape[0], k.shape[1]
+    dev = q.device
+    if out is None:
+        out = torch.empty((n_q, hq, d), dtype=torch.float32, device=dev)
+    n_items = 0 if items is None else items.shape[0]
+    if n_bins > 0 and raw is None:
+        n_out = n_bins if active is None else int(active.sum().item())
+        raw = torch.zeros(max(1, n_out), dtype=torch.float64, device=dev)
+    if bad_row is None:
+        bad_row = torch.empty(1, dtype=torch.int32, device=dev)
+    nbytes = _lib.lib.rk_prefill_workspace_bytes(n_q, hq, hkv, s, d, n_items, n_bins if raw is not None else 0)
+    ws = scratch(nbytes, dev, "prefill")
+    _lib.call("rk_prefill_attention", _lib.ptr(q), n_q, hq, d, _lib.ptr(k), _lib.ptr(v), kv_code(k), s, hkv,
+              _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(allowed), _lib.ptr(items), n_items,
+              n_bins if raw is not None else 0, _lib.ptr(active), _lib.ptr(out), _lib.ptr(raw), _lib.ptr(bad_row),
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
+    return out, raw, bad_row
