@@ -12,26 +12,34 @@
 // scoring costs no extra pass over K.
 //
 // Per work unit (M tile of 128 stacked query rows (g, i) of one kv-head, key
-// chunk = a run of items) the CTA streams 64-key tiles of K and V:
-//   S  = Q_hi K^T + Q_lo K^T            tcgen05.mma m128n64k16 x 16, TMEM
-//   P  = exp2(S - m) (online, lazy rescale), split P = P_hi + P_lo (bf16)
-//   O += P_hi V + P_lo V                tcgen05.mma m128n128k16 x 8, TMEM,
-//                                        V read MN-major straight from its TMA tile
+// chunk = a run of items) the CTA streams 128-key tiles of K and V:
+//   S  = Q_hi K^T + Q_lo K^T            tcgen05.mma m128n128k16 x 16 -> TMEM
+//   P  = exp2(S - m) (online, lazy rescale), split P = P_hi + P_lo (bf16),
+//        written back over its own S columns in TMEM (bf16x2 per column)
+//   O += P_hi V + P_lo V                tcgen05.mma m128n128k16 x 8, A = P from
+//                                        TMEM, B = V read MN-major from its TMA tile
 // The q and P splits keep ~16 mantissa bits (fp32-class outputs; the reference
-// tolerance is 1e-3 relative, fp64 accumulation on its side).
+// tolerance is 1e-3 relative, fp64 accumulation on its side).  Three S/P
+// buffers let QK run a tile ahead of the softmax, and the softmax never
+// waits for the previous tile's PV (only the rare O rescale does).
 //
-// CTA roles (192 threads, one CTA per SM, persistent over a contiguous range
+// CTA roles (352 threads, one CTA per SM, persistent over a contiguous range
 // of units so Q is reloaded only when the range crosses an M tile):
-//   warps 0-3  softmax / epilogue: thread = TMEM lane = stacked row; reads S
-//              with tcgen05.ld, masks, online softmax, writes P (swizzled
-//              smem) and the per-item scoring statistics; rescales O in TMEM
-//              when its running max moves by more than 2^8; at unit end reads
-//              O and writes the unit's partial (m, l, O) for the merge;
-//   warp 4     TMA producer: Q hi/lo [128 x 128] per M tile, K and V
-//              [64 keys x 128] per tile (4-stage ring, SWIZZLE_128B);
-//   warp 5     TMEM allocation + single-thread MMA issue, QK of tile t issued
-//              ahead of PV of tile t-1 so the tensor pipe has work while the
-//              softmax runs.
+//   warps 0-7  softmax / epilogue: TMEM lane quarter = warp & 3 (a thread owns
+//              one stacked row), column half = warp >> 2 — the two warps of a
+//              row (same SMSP) agree on the row max through a 64-thread named
+//              barrier per tile.  They read S with tcgen05.ld, mask, run the
+//              online softmax (packed f32x2 math), write P with tcgen05.st and
+//              the per-item scoring statistics; rescale their half of O in
+//              TMEM when the running max moves by more than 2^8; at unit end
+//              read O and write the unit's partial (m, l, O) for the merge;
+//   warp 8     TMEM allocation + single-thread MMA issue;
+//   warp 9     TMA producer of Q hi/lo [128 x 128] per M tile and K [128 keys
+//              x 128] per tile (2-stage ring, freed after its QK); the warp
+//              also reduces each tile's key positions to one maximum so fully
+//              visible tiles skip the per-key causal mask;
+//   warp 10    TMA producer of V [128 keys x 128] per tile (2-stage ring, freed
+//              after its PV).  All tiles SWIZZLE_128B.
 #include <cmath>
 
 #include <algorithm>
@@ -44,20 +52,26 @@ namespace pf {
 
 using namespace tc;
 
-constexpr int BM = 128, BN = 64, D = 128;
-constexpr int STAGES = 4;
+constexpr int BM = 128, BN = 128, D = 128;   // rows, keys per tile, head dim
+constexpr int STAGES = 2;                // K ring and V ring depth
+constexpr int MR = 8;                    // tile-visibility metadata ring
+constexpr int NB = 3;                    // S/P buffers in TMEM (3 x 128 columns + O = 512)
+constexpr int LA = NB - 1;               // QK runs LA tiles ahead (its buffer is freed by the PV queued before)
 constexpr int QBOX = BM * 64 * 2;        // 128 rows x 64 bf16, swizzled: 16 KB
 constexpr int Q_BYTES = 4 * QBOX;        // q_hi, q_lo x two 64-dim halves
-constexpr int KBOX = BN * 64 * 2;        // 64 keys x 64 bf16: 8 KB
-constexpr int KV_STAGE = 4 * KBOX;       // K (2 boxes) + V (2 boxes): 32 KB
-constexpr int P_BYTES = 2 * QBOX;        // P_hi, P_lo: 128 rows x 64 keys each
-constexpr int THREADS = 192;
-constexpr size_t SMEM = 1024 + Q_BYTES + P_BYTES + STAGES * KV_STAGE + 256;
+constexpr int KBOX = BN * 64 * 2;        // 128 keys x 64 bf16: 16 KB
+constexpr int KV_STAGE = 2 * KBOX;       // one K or V tile (2 boxes): 32 KB
+constexpr int kSoftmaxWarps = 8, kMmaWarp = 8, kProducerWarp = 9, kVProducerWarp = 10;
+constexpr int THREADS = 352;
+constexpr int BAR_BYTES = 512;           // mbarriers, TMEM slot, per-stage tile maxima
+constexpr int XCH_BYTES = (2 * 256 + 3 * 128) * 4;  // row-max exchange (2 tiles x 2 halves) + item / unit sums
+constexpr size_t SMEM = 1024 + Q_BYTES + 2 * STAGES * KV_STAGE + BAR_BYTES + XCH_BYTES;
+constexpr uint32_t TMEM_COLS = 512;      // S/P buffers NB x 128 at 0.., O (128) at NB * 128 (= 384)
 constexpr float TAU = 8.f;               // lazy rescale threshold (log2 units)
-constexpr float FALLBACK = 100.f;        // item statistics recomputed when a tile sits this far below m
+constexpr float FALLBACK = 100.f;        // item statistics recomputed when keys sit this far below m
 
-constexpr uint32_t kIdescQK = idesc_f16(BM, BN);             // S[128 x 64]  = Q K^T
-constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);        // O[128 x 128] += P V, V MN-major
+constexpr uint32_t kIdescQK = idesc_f16(BM, BN);             // S[128 x 128] = Q K^T (both K-major, smem)
+constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);        // O[128 x 128] += P V (P from TMEM, V MN-major)
 
 struct Params {
   int n_q, hq, hkv, G, mpad, mtiles;
@@ -85,23 +99,137 @@ __device__ __forceinline__ void item_range(const Params& p, int it, int& lo, int
   }
 }
 
+// Units are chunk-major: at any moment the persistent CTAs work on the M tiles
+// of (about) one key chunk, so the chunk's K/V (all kv-heads: the rows are
+// contiguous) is fetched from DRAM once and served to every M tile from L2.
+__device__ __forceinline__ int unit_chunk(const Params& p, int u) { return u / (p.hkv * p.mtiles); }
+
 __device__ __forceinline__ void unit_of(const Params& p, int u, int& mtile, int& it0, int& it1) {
-  mtile = u / p.n_chunks;
-  const int c = u - mtile * p.n_chunks;
+  const int c = unit_chunk(p, u);
+  mtile = u - c * (p.hkv * p.mtiles);
   it0 = c * p.items_per_chunk;
   it1 = min(p.n_items, it0 + p.items_per_chunk);
 }
 
-__device__ __forceinline__ int ntiles(int lo, int hi) { return hi > lo ? (hi - lo + BN - 1) / BN : 0; }
+// Walks the 128-key tiles of the CTA's units in order (units without keys are skipped).
+struct TileIter {
+  const Params* p;
+  int u, u1, it, it1, lo, hi, j0, mtile;
+  bool first, valid;
+  __device__ void init(const Params& P, int ua, int ub) {
+    p = &P;
+    u = ua - 1;
+    u1 = ub;
+    valid = true;
+    next_unit();
+  }
+  __device__ void next_unit() {
+    while (true) {
+      if (++u >= u1) {
+        valid = false;
+        return;
+      }
+      unit_of(*p, u, mtile, it, it1);
+      for (; it < it1; ++it) {
+        item_range(*p, it, lo, hi);
+        if (hi > lo) {
+          j0 = lo;
+          first = true;
+          return;
+        }
+      }
+    }
+  }
+  __device__ void advance() {
+    first = false;
+    j0 += BN;
+    if (j0 < hi) return;
+    for (++it; it < it1; ++it) {
+      item_range(*p, it, lo, hi);
+      if (hi > lo) {
+        j0 = lo;
+        return;
+      }
+    }
+    next_unit();
+  }
+};
 
-// exp2 of a pair and packing into (hi, lo) bf16x2 words
-__device__ __forceinline__ void split_pack(float a, float b, uint32_t& hi, uint32_t& lo) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  float2 hf = __bfloat1622float2(h);
-  __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
-  hi = *reinterpret_cast<uint32_t*>(&h);
-  lo = *reinterpret_cast<uint32_t*>(&l);
+#ifdef PF_PROF
+// [role][slot] accumulated cycles; role 0 softmax (warp 0 lane 0), 1 MMA, 2 K producer, 3 V producer
+__device__ unsigned long long g_pf_prof[4][16];
+#define PWAIT(bar, par, role, slot)                                                     \
+  do {                                                                                  \
+    const long long _t0 = clock64();                                                    \
+    bar_wait(bar, par);                                                                 \
+    if ((threadIdx.x & 31) == 0 && (role != 0 || threadIdx.x == 0))                     \
+      atomicAdd(&g_pf_prof[role][slot], (unsigned long long)(clock64() - _t0));         \
+  } while (0)
+#else
+#define PWAIT(bar, par, role, slot) bar_wait(bar, par)
+#endif
+
+__device__ __forceinline__ void tma_2d_s(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(sa(bar))
+      : "memory");
 }
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// SWIZZLE_128B descriptor from a 32-bit shared address (see tc::umma_desc);
+// later k-slices add (byte offset >> 4) to the start-address field
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo_bytes) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// tcgen05.mma with A from TMEM (kind::f16, A K-major: row = lane, 2 bf16 per column)
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+        "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 __global__ void __launch_bounds__(THREADS, 1)
 prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
@@ -109,18 +237,27 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* qs = smem;                               // [hi d0-63 | hi d64-127 | lo d0-63 | lo d64-127]
-  uint8_t* ps = qs + Q_BYTES;                       // [P_hi | P_lo], 128 rows x 64 keys each
-  uint8_t* kvs = ps + P_BYTES;                      // STAGES x [K d0-63 | K d64-127 | V d0-63 | V d64-127]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kvs + STAGES * KV_STAGE);
-  uint64_t* kv_full = bars;                         // [STAGES]
-  uint64_t* kv_empty = bars + STAGES;               // [STAGES]
-  uint64_t* q_full = bars + 2 * STAGES;
+  uint8_t* ks = qs + Q_BYTES;                       // STAGES x [K d0-63 | K d64-127]
+  uint8_t* vs = ks + STAGES * KV_STAGE;             // STAGES x [V d0-63 | V d64-127]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vs + STAGES * KV_STAGE);
+  uint64_t* k_full = bars;                          // [STAGES] TMA -> MMA
+  uint64_t* k_empty = k_full + STAGES;              // [STAGES] QK done -> producer
+  uint64_t* v_full = k_empty + STAGES;              // [STAGES] TMA -> MMA
+  uint64_t* v_empty = v_full + STAGES;              // [STAGES] PV done -> producer
+  uint64_t* meta_full = v_empty + STAGES;           // [MR] producer -> softmax (tile_max)
+  uint64_t* q_full = meta_full + MR;
   uint64_t* q_empty = q_full + 1;
-  uint64_t* s_full = q_full + 2;                    // [2]
-  uint64_t* s_empty = q_full + 4;                   // [2]
-  uint64_t* p_full = q_full + 6;                    // P tile written (4 warp arrivals)
-  uint64_t* pv_done = q_full + 7;                   // PV of the last issued tile complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 8);
+  uint64_t* s_full = q_full + 2;                    // [NB] QK done -> softmax
+  uint64_t* p_full = s_full + NB;                   // [NB] P written (8 softmax warps) -> MMA
+  uint64_t* buf_free = p_full + NB;                 // [NB] PV done: S/P buffer reusable, O stable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(buf_free + NB);
+  // per tile (ring of MR): the largest effective key position of the tile
+  // (masked or out-of-item keys count as +inf), published through meta_full
+  int64_t* tile_max = reinterpret_cast<int64_t*>(buf_free + NB + 1);
+  float* xmax = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + BAR_BYTES);   // [2][2][128]
+  float* xm_it = xmax + 512;                        // [128]
+  float* xl_it = xm_it + 128;                       // [128]
+  float* xl_u = xl_it + 128;                        // [128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
@@ -128,209 +265,263 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      bar_init(&kv_full[s], 1);
-      bar_init(&kv_empty[s], 1);
+      bar_init(&k_full[s], 1);
+      bar_init(&k_empty[s], 1);
+      bar_init(&v_full[s], 1);
+      bar_init(&v_empty[s], 1);
     }
+    for (int s = 0; s < MR; ++s) bar_init(&meta_full[s], 1);
     bar_init(q_full, 1);
     bar_init(q_empty, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       bar_init(&s_full[b], 1);
-      bar_init(&s_empty[b], 4);
+      bar_init(&p_full[b], kSoftmaxWarps);
+      bar_init(&buf_free[b], 1);
     }
-    bar_init(p_full, 4);
-    bar_init(pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {   // 256 TMEM columns: S double buffer (2 x 64) + O (128)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(sa(tmem_slot)));
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)),
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  fence_before();
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_o = tmem + 2 * BN;
+  const uint32_t tmem_o = tmem + NB * BN;
+#ifdef PF_PROF
+  const long long prof_t0 = clock64();
+#endif
 
-  if (warp == 4) {
-    // ================= TMA producer
+  if (warp == kProducerWarp) {
+    // ================= K (+ Q) producer (lane 0 issues; the warp computes tile visibility)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&qmap) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&kmap) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&vmap) : "memory");
-      int cur_mtile = -1, qn = 0, t = 0;
-      for (int u = u0; u < u1; ++u) {
-        int mtile, it0, it1;
-        unit_of(p, u, mtile, it0, it1);
-        const int kvh = mtile / p.mtiles, mt = mtile - kvh * p.mtiles;
-        int nt = 0;
-        for (int it = it0; it < it1; ++it) {
-          int lo, hi;
-          item_range(p, it, lo, hi);
-          nt += ntiles(lo, hi);
+    }
+    const uint32_t qs_a = sa(qs), ks_a = sa(ks);
+    TileIter ti, ta;                                // ta runs PF tiles ahead: key-position prefetch
+    ti.init(p, u0, u1);
+    ta.init(p, u0, u1);
+    constexpr int PF = 3;
+    int64_t pk[PF][BN / 32];                        // prefetched effective positions, pk[0] = current tile
+    // shift the ring by one tile and load the tile `ta` points at into its tail
+    auto fetch = [&]() {
+#pragma unroll
+      for (int sl = 0; sl + 1 < PF; ++sl)
+#pragma unroll
+        for (int i = 0; i < BN / 32; ++i) pk[sl][i] = pk[sl + 1][i];
+#pragma unroll
+      for (int i = 0; i < BN / 32; ++i) pk[PF - 1][i] = INT64_MAX;
+      if (ta.valid) {
+        const int nv = min(BN, ta.hi - ta.j0);
+#pragma unroll
+        for (int i = 0; i < BN / 32; ++i) {
+          const int jj = 32 * i + lane;
+          if (jj < nv && (!p.allowed || p.allowed[ta.j0 + jj])) pk[PF - 1][i] = p.k_pos[ta.j0 + jj];
         }
-        if (nt == 0) continue;
-        if (mtile != cur_mtile) {
-          if (qn > 0) bar_wait(q_empty, (qn - 1) & 1);
+        ta.advance();
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < PF; ++i) fetch();
+    int cur_mtile = -1, qn = 0;
+    for (int t = 0; ti.valid; ++t, ti.advance()) {
+      const int kvh = ti.mtile / p.mtiles, mt = ti.mtile - kvh * p.mtiles;
+      if (ti.mtile != cur_mtile) {
+        if (qn > 0) PWAIT(q_empty, (qn - 1) & 1, 2, 1);
+        if (elect_one()) {
           bar_expect(q_full, Q_BYTES);
           const int row0 = kvh * 2 * p.mpad + mt * BM;
-          tma_2d(qs + 0 * QBOX, &qmap, 0, row0, q_full);
-          tma_2d(qs + 1 * QBOX, &qmap, 64, row0, q_full);
-          tma_2d(qs + 2 * QBOX, &qmap, 0, row0 + p.mpad, q_full);
-          tma_2d(qs + 3 * QBOX, &qmap, 64, row0 + p.mpad, q_full);
-          cur_mtile = mtile;
-          ++qn;
+          tma_2d_s(qs_a + 0 * QBOX, &qmap, 0, row0, q_full);
+          tma_2d_s(qs_a + 1 * QBOX, &qmap, 64, row0, q_full);
+          tma_2d_s(qs_a + 2 * QBOX, &qmap, 0, row0 + p.mpad, q_full);
+          tma_2d_s(qs_a + 3 * QBOX, &qmap, 64, row0 + p.mpad, q_full);
         }
-        for (int it = it0; it < it1; ++it) {
-          int lo, hi;
-          item_range(p, it, lo, hi);
-          for (int j0 = lo; j0 < hi; j0 += BN, ++t) {
-            const int s = t % STAGES;
-            if (t >= STAGES) bar_wait(&kv_empty[s], ((t / STAGES) - 1) & 1);
-            uint8_t* st = kvs + s * KV_STAGE;
-            bar_expect(&kv_full[s], KV_STAGE);
-            tma_2d(st + 0 * KBOX, &kmap, kvh * D, j0, &kv_full[s]);
-            tma_2d(st + 1 * KBOX, &kmap, kvh * D + 64, j0, &kv_full[s]);
-            tma_2d(st + 2 * KBOX, &vmap, kvh * D, j0, &kv_full[s]);
-            tma_2d(st + 3 * KBOX, &vmap, kvh * D + 64, j0, &kv_full[s]);
-          }
-        }
+        __syncwarp();
+        cur_mtile = ti.mtile;
+        ++qn;
       }
-    }
-  } else if (warp == 5) {
-    // ================= MMA issuer (one thread)
-    if (lane == 0) {
-      int cur_mtile = -1, qn = 0, t = 0;
-      int pending = -1;            // global index of the tile whose PV is not issued yet
-      bool pending_first = false;  // that tile opens its unit (PV overwrites O)
-      auto issue_pv = [&](int tp, bool first) {
-        bar_wait(p_full, tp & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint8_t* vst = kvs + (tp % STAGES) * KV_STAGE + 2 * KBOX;
+      const int s = t % STAGES, j0 = ti.j0;
+      // effective positions of the tile's keys, loaded PF tiles ago
+      int64_t kmax = INT64_MIN;
 #pragma unroll
-        for (int hl = 0; hl < 2; ++hl)
+      for (int i = 0; i < BN / 32; ++i) kmax = pk[0][i] > kmax ? pk[0][i] : kmax;
+      fetch();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t x = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmax = x > kmax ? x : kmax;
+      }
+      if (t >= STAGES) PWAIT(&k_empty[s], ((t / STAGES) - 1) & 1, 2, 0);
+      if (elect_one()) {
+        tile_max[t % MR] = kmax;
+        bar_arrive(&meta_full[t % MR]);               // release: tile_max visible with the phase
+        bar_expect(&k_full[s], KV_STAGE);
+        tma_2d_s(ks_a + s * KV_STAGE, &kmap, kvh * D, j0, &k_full[s]);
+        tma_2d_s(ks_a + s * KV_STAGE + KBOX, &kmap, kvh * D + 64, j0, &k_full[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == kVProducerWarp) {
+    // ================= V producer: V of tile t once PV_{t-STAGES} freed its slot
+    // (a separate warp so the K loads, needed a tile earlier, never queue behind it)
+    TileIter ti;
+    ti.init(p, u0, u1);
+    const uint32_t vs_a = sa(vs);
+    for (int t = 0; ti.valid; ++t, ti.advance()) {
+      const int kvh = ti.mtile / p.mtiles, s = t % STAGES;
+      if (t >= STAGES) PWAIT(&v_empty[s], ((t / STAGES) - 1) & 1, 3, 0);
+      if (elect_one()) {
+        bar_expect(&v_full[s], KV_STAGE);
+        tma_2d_s(vs_a + s * KV_STAGE, &vmap, kvh * D, ti.j0, &v_full[s]);
+        tma_2d_s(vs_a + s * KV_STAGE + KBOX, &vmap, kvh * D + 64, ti.j0, &v_full[s]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == kMmaWarp) {
+    // ================= MMA issuer.  The whole warp runs the (uniform) control
+    // flow and one elected lane issues, so descriptors live in uniform
+    // registers; each tile's descriptors are built once and advanced by
+    // compile-time offsets.  Order: QK of the LA tiles ahead, then per tile t:
+    // PV_t (after its P), QK_{t+LA} into the buffer PV_{t-1} frees — the
+    // issuer never waits on the PV it just issued, and the tensor pipe always
+    // holds queued work.  (LA = NB - 1: QK_{t+LA} reuses the buffer of PV_{t-1},
+    // which sits ahead of PV_t in the tensor queue and is normally done.)
+    TileIter qi, pi;
+    qi.init(p, u0, u1);
+    pi.init(p, u0, u1);
+    const uint32_t qs_a = sa(qs), ks_a = sa(ks), vs_a = sa(vs);
+    int tq = 0, tp = 0, cur_mtile = -1, qn = 0;
+    auto issue_qk = [&]() {
+      if (qi.mtile != cur_mtile) {
+        if (qn > 0 && elect_one()) umma_commit(q_empty);   // Q slot free once the QKs issued so far finish
+        __syncwarp();
+        PWAIT(q_full, qn & 1, 1, 0);
+        cur_mtile = qi.mtile;
+        ++qn;
+      }
+      const int b = tq % NB, s = tq % STAGES;
+      if (tq >= NB) PWAIT(&buf_free[b], ((tq / NB) - 1) & 1, 1, 1);
+      PWAIT(&k_full[s], (tq / STAGES) & 1, 1, 2);
+      fence_after();
+      if (elect_one()) {
+        const uint32_t dS = tmem + b * BN;
+        const uint64_t a0 = desc_sw128(qs_a, 16);
+        const uint64_t b0 = desc_sw128(ks_a + s * KV_STAGE, 16);
+#pragma unroll
+        for (int hl = 0; hl < 2; ++hl)          // q_hi, q_lo
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            umma(dS, a0 + (uint64_t)((((2 * hl + k / 4) * QBOX) + 32 * (k % 4)) >> 4),
+                 b0 + (uint64_t)((((k / 4) * KBOX) + 32 * (k % 4)) >> 4), kIdescQK, (hl | k) ? 1u : 0u);
+          }
+        umma_commit(&k_empty[s]);                    // K slot free once this QK completes
+        umma_commit(&s_full[b]);
+      }
+      __syncwarp();
+      ++tq;
+      qi.advance();
+    };
+    for (int i = 0; i < LA && qi.valid; ++i) issue_qk();
+    while (pi.valid) {
+      const int b = tp % NB, s = tp % STAGES;
+      PWAIT(&p_full[b], (tp / NB) & 1, 1, 3);
+      PWAIT(&v_full[s], (tp / STAGES) & 1, 1, 4);
+      fence_after();
+      if (elect_one()) {
+        const uint64_t b0 = desc_sw128(vs_a + s * KV_STAGE, KBOX);   // V MN-major: d-halves LBO apart
+        const uint32_t a0 = tmem + b * BN;                             // P_hi | P_lo (16 keys = 8 columns)
+        const bool first = pi.first;
+#pragma unroll
+        for (int hl = 0; hl < 2; ++hl)          // P_hi, P_lo
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk) {
-            const uint8_t* a = ps + hl * QBOX + 32 * kk;          // P (K-major: keys along the row)
-            const uint8_t* b = vst + kk * 16 * 128;              // V (MN-major: d along the row)
-            umma(tmem_o, umma_desc(a), umma_desc(b, KBOX), kIdescPV, (first && hl == 0 && kk == 0) ? 0u : 1u);
+            umma_ts(tmem_o, a0 + hl * (BN / 2) + kk * 8, b0 + (uint64_t)((kk * 16 * 128) >> 4), kIdescPV,
+                    (first && hl == 0 && kk == 0) ? 0u : 1u);
           }
-        umma_commit(&kv_empty[tp % STAGES]);
-        umma_commit(pv_done);
-      };
-      for (int u = u0; u < u1; ++u) {
-        int mtile, it0, it1;
-        unit_of(p, u, mtile, it0, it1);
-        bool first_tile = true;
-        for (int it = it0; it < it1; ++it) {
-          int lo, hi;
-          item_range(p, it, lo, hi);
-          for (int j0 = lo; j0 < hi; j0 += BN, ++t) {
-            if (mtile != cur_mtile) {
-              if (qn > 0) umma_commit(q_empty);      // Q slot free once the QKs issued so far finish
-              bar_wait(q_full, qn & 1);
-              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-              cur_mtile = mtile;
-              ++qn;
-            }
-            const int s = t % STAGES, buf = t & 1;
-            bar_wait(&kv_full[s], (t / STAGES) & 1);
-            if (t >= 2) bar_wait(&s_empty[buf], ((t / 2) - 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t dS = tmem + buf * BN;
-            const uint8_t* kst = kvs + s * KV_STAGE;
-#pragma unroll
-            for (int hl = 0; hl < 2; ++hl)
-#pragma unroll
-              for (int k = 0; k < D / 16; ++k) {
-                const uint8_t* a = qs + (2 * hl + k / 4) * QBOX + 32 * (k % 4);
-                const uint8_t* b = kst + (k / 4) * KBOX + 32 * (k % 4);
-                umma(dS, umma_desc(a), umma_desc(b), kIdescQK, (hl | k) ? 1u : 0u);
-              }
-            umma_commit(&s_full[buf]);
-            if (pending >= 0) issue_pv(pending, pending_first);
-            pending = t;
-            pending_first = first_tile;
-            first_tile = false;
-          }
-        }
+        umma_commit(&v_empty[s]);
+        umma_commit(&buf_free[b]);
       }
-      if (pending >= 0) issue_pv(pending, pending_first);
+      __syncwarp();
+      ++tp;
+      pi.advance();
+      if (qi.valid) issue_qk();
     }
   } else {
-    // ================= softmax / epilogue: warps 0-3, thread = TMEM lane = stacked row
-    const int r = warp * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    uint8_t* prow_hi = ps + r * 128;
-    uint8_t* prow_lo = ps + QBOX + r * 128;
-    const int sw = r & 7;
+    // ================= softmax / epilogue: warps 0-7.  TMEM lane quarter q4 =
+    // warp & 3 (rows 32*q4 ..), column half = warp >> 2: each row's 64 scores
+    // and 128 O columns are split over two warps (same SMSP), which agree on
+    // the row max through a 64-thread named barrier per tile.
+    const int q4 = warp & 3, half = warp >> 2;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const int bar_id = 1 + q4;
     int t = 0;
-    int pv_seen = 0;               // PV completions consumed
     for (int u = u0; u < u1; ++u) {
       int mtile, it0, it1;
       unit_of(p, u, mtile, it0, it1);
       const int kvh = mtile / p.mtiles, mt = mtile - kvh * p.mtiles;
-      const int c = u - mtile * p.n_chunks;
+      const int c = unit_chunk(p, u);
       const int R = mt * BM + r;
       const bool real = R < p.G * p.n_q;
       const int g = real ? R / p.n_q : 0, qi = real ? R - g * p.n_q : 0;
       const int h = kvh * p.G + g;
       const int64_t qpos = p.q_pos[qi];
-      float m_run = -INFINITY, l_run = 0.f;   // O's reference max and running sum
+      float m_run = -INFINITY, l_half = 0.f;  // O's reference max (shared by the pair), this half's sum
       bool any_tile = false;
       for (int it = it0; it < it1; ++it) {
         int lo, hi;
         item_range(p, it, lo, hi);
-        float m_it = -INFINITY, l_it = 0.f;    // this item's scoring statistics
+        float m_it = -INFINITY, l_it = 0.f;    // this half's scoring statistics of the item
         for (int j0 = lo; j0 < hi; j0 += BN, ++t) {
-          const int buf = t & 1;
-          // ---- visibility of the tile's keys (warp-cooperative, positions shared by all rows)
-          const int nv = min(BN, hi - j0);
-          int64_t kp0 = INT64_MAX, kp1 = INT64_MAX;
-          if (lane < nv) {
-            kp0 = p.k_pos[j0 + lane];
-            if (p.allowed && !p.allowed[j0 + lane]) kp0 = INT64_MAX;
-          }
-          if (lane + 32 < nv) {
-            kp1 = p.k_pos[j0 + 32 + lane];
-            if (p.allowed && !p.allowed[j0 + 32 + lane]) kp1 = INT64_MAX;
-          }
-          int64_t kmax = kp0 > kp1 ? kp0 : kp1;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const int64_t x = __shfl_xor_sync(0xffffffffu, kmax, o);
-            kmax = x > kmax ? x : kmax;
-          }
-          const bool all_vis = kmax <= qpos;           // INT64_MAX (masked / past the item) fails
+          const int b = t % NB;
+          // ---- visibility: the producer's tile maximum
+          PWAIT(&meta_full[t % MR], (t / MR) & 1, 0, 0);
+          const bool all_vis = tile_max[t % MR] <= qpos;   // +inf (masked / past the item) fails
 
-          bar_wait(&s_full[buf], (t / 2) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          float sc[BN];
+          PWAIT(&s_full[b], (t / NB) & 1, 0, 1);
+          fence_after();
+          constexpr int HK = BN / 2;                    // keys per column half
+          float sc[HK];
           {
             float v0[32], v1[32];
-            tmem_ld32(tmem + lane_base + buf * BN, v0);
-            tmem_ld32(tmem + lane_base + buf * BN + 32, v1);
+            tmem_ld32(tmem + lane_base + b * BN + HK * half, v0);
+            tmem_ld32(tmem + lane_base + b * BN + HK * half + 32, v1);
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               sc[i] = v0[i];
               sc[32 + i] = v1[i];
             }
           }
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) bar_arrive(&s_empty[buf]);
 
-          if (!__all_sync(0xffffffffu, all_vis)) {
+          if (!__all_sync(0xffffffffu, all_vis)) {     // diagonal / masked tile: per-key check
+            const int nv = min(BN, hi - j0);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int64_t a = __shfl_sync(0xffffffffu, kp0, i);
-              const int64_t b = __shfl_sync(0xffffffffu, kp1, i);
-              if (a > qpos) sc[i] = -INFINITY;
-              if (b > qpos) sc[32 + i] = -INFINITY;
+            for (int c = 0; c < HK / 32; ++c) {
+              const int jj = HK * half + 32 * c + lane;
+              int64_t kp = INT64_MAX;
+              if (jj < nv && (!p.allowed || p.allowed[j0 + jj])) kp = p.k_pos[j0 + jj];
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (__shfl_sync(0xffffffffu, kp, i) > qpos) sc[32 * c + i] = -INFINITY;
             }
           }
-          float tmax = -INFINITY;
+          float hmax = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < BN; ++i) tmax = fmaxf(tmax, sc[i]);
+          for (int i = 0; i < HK; ++i) hmax = fmaxf(hmax, sc[i]);
+          xmax[(t & 1) * 256 + half * 128 + r] = hmax;
+          fence_before();                                // our S reads precede the partner's P writes
+#ifdef PF_PROF
+          { const long long _t0 = clock64(); named_sync(bar_id, 64);
+            if (threadIdx.x == 0) atomicAdd(&g_pf_prof[0][4], (unsigned long long)(clock64() - _t0)); }
+#else
+          named_sync(bar_id, 64);
+#endif
+          fence_after();
+          const float tmax = fmaxf(hmax, xmax[(t & 1) * 256 + (half ^ 1) * 128 + r]);
           // ---- lazy online softmax: move the reference max only when it grows by > TAU
           const bool first = !any_tile;
           float m_new = m_run;
@@ -339,23 +530,32 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           const float mu = (m_new == -INFINITY) ? 0.f : m_new;
           const float fac = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mu);
           const bool rescale = !first && (m_new != m_run);
-          float rs = 0.f;
-          uint32_t hw[BN / 2], lw[BN / 2];
+          float2 acc2 = make_float2(0.f, 0.f);
+          uint32_t hw[HK / 2], lw[HK / 2];
+          const float2 nmu = make_float2(-mu, -mu), one = make_float2(1.f, 1.f), mone = make_float2(-1.f, -1.f);
 #pragma unroll
-          for (int i = 0; i < BN; i += 2) {
-            const float a = fast_exp2(sc[i] - mu), b = fast_exp2(sc[i + 1] - mu);
-            rs += a + b;
-            split_pack(a, b, hw[i / 2], lw[i / 2]);
+          for (int i = 0; i < HK; i += 2) {
+            const float2 dlt = ffma2(make_float2(sc[i], sc[i + 1]), one, nmu);
+            const float2 e = make_float2(fast_exp2(dlt.x), fast_exp2(dlt.y));
+            acc2 = ffma2(e, one, acc2);
+            __nv_bfloat162 hb = __floats2bfloat162_rn(e.x, e.y);
+            const uint32_t hu = *reinterpret_cast<uint32_t*>(&hb);
+            const float2 lo2 = ffma2(make_float2(__uint_as_float(hu << 16), __uint_as_float(hu & 0xffff0000u)),
+                                     mone, e);
+            __nv_bfloat162 lb = __floats2bfloat162_rn(lo2.x, lo2.y);
+            hw[i / 2] = hu;
+            lw[i / 2] = *reinterpret_cast<uint32_t*>(&lb);
           }
-          l_run = (rescale ? l_run * fac : l_run) + rs;
-          // ---- per-item scoring statistics (exact (m, l) pair of the item's keys)
-          if (p.item_m && tmax != -INFINITY) {
+          const float rs = acc2.x + acc2.y;
+          l_half = (rescale ? l_half * fac : l_half) + rs;
+          // ---- per-item scoring statistics (exact (m, l) pair of this half's keys)
+          if (p.item_m && hmax != -INFINITY) {
             float tm = mu, tl = rs;
-            if (tmax < mu - FALLBACK) {        // tile far below the reference: recompute exactly
-              tm = tmax;
+            if (hmax < mu - FALLBACK) {        // keys far below the reference: recompute exactly
+              tm = hmax;
               tl = 0.f;
 #pragma unroll
-              for (int i = 0; i < BN; ++i) tl += fast_exp2(sc[i] - tmax);
+              for (int i = 0; i < HK; ++i) tl += fast_exp2(sc[i] - hmax);
             }
             if (m_it == -INFINITY) {
               m_it = tm;
@@ -366,75 +566,97 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
               m_it = M;
             }
           }
-          // ---- P (and O) may be touched once the previous tile's PV is complete
-          if (t > 0 && pv_seen < t) {
-            bar_wait(pv_done, (t - 1) & 1);
-            pv_seen = t;
-          }
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          // ---- O rescale (rare): O is stable once PV_{t-1} has completed
           if (__any_sync(0xffffffffu, rescale)) {
+            const int tl1 = t - 1;
+            PWAIT(&buf_free[tl1 % NB], (tl1 / NB) & 1, 0, 2);
+            fence_after();
             const float f = rescale ? fac : 1.f;
+            const float2 f2 = make_float2(f, f);
 #pragma unroll
-            for (int cc = 0; cc < D / 32; ++cc) {
+            for (int cc = 0; cc < 2; ++cc) {
               float o[32];
-              tmem_ld32(tmem_o + lane_base + 32 * cc, o);
+              const uint32_t oa = tmem_o + lane_base + 64 * half + 32 * cc;
+              tmem_ld32(oa, o);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] *= f;
-              tmem_st32(tmem_o + lane_base + 32 * cc, o);
+              for (int i = 0; i < 32; i += 2) {
+                const float2 x = fmul2(make_float2(o[i], o[i + 1]), f2);
+                o[i] = x.x;
+                o[i + 1] = x.y;
+              }
+              tmem_st32(oa, o);
             }
           }
           m_run = m_new;
           any_tile = true;
-#pragma unroll
-          for (int ch = 0; ch < BN / 8; ++ch) {
-            const int off = ((ch ^ sw) << 4);
-            *reinterpret_cast<uint4*>(prow_hi + off) =
-                make_uint4(hw[4 * ch], hw[4 * ch + 1], hw[4 * ch + 2], hw[4 * ch + 3]);
-            *reinterpret_cast<uint4*>(prow_lo + off) =
-                make_uint4(lw[4 * ch], lw[4 * ch + 1], lw[4 * ch + 2], lw[4 * ch + 3]);
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          // ---- P over its own S columns: [P_hi keys 0-63 | P_lo keys 0-63], bf16x2 per column
+          tmem_st32u(tmem + lane_base + b * BN + (HK / 2) * half, hw);            // P_hi columns
+          tmem_st32u(tmem + lane_base + b * BN + BN / 2 + (HK / 2) * half, lw);   // P_lo columns
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          fence_before();
           __syncwarp();
-          if (lane == 0) bar_arrive(p_full);
+          if (lane == 0) bar_arrive(&p_full[b]);
         }
-        if (p.item_m && real) {
-          const int64_t o = ((int64_t)qi * p.hq + h) * p.n_items + it;
-          p.item_m[o] = m_it;
-          p.item_l[o] = l_it;
+        if (p.item_m) {                        // combine the halves' item statistics
+          if (half == 1) {
+            xm_it[r] = m_it;
+            xl_it[r] = l_it;
+          }
+          named_sync(bar_id, 64);
+          if (half == 0 && real) {
+            const float m1 = xm_it[r], l1 = xl_it[r];
+            float M = fmaxf(m_it, m1), L = 0.f;
+            if (M != -INFINITY) {
+              L = (l_it > 0.f ? l_it * fast_exp2(m_it - M) : 0.f) + (l1 > 0.f ? l1 * fast_exp2(m1 - M) : 0.f);
+            }
+            const int64_t o = ((int64_t)qi * p.hq + h) * p.n_items + it;
+            p.item_m[o] = M;
+            p.item_l[o] = L;
+          }
+          named_sync(bar_id, 64);
         }
       }
-      // ---- unit end: O of the last tile, partial (m, l, O) for the merge
+      // ---- unit end: O after the last PV, partial (m, l, O) for the merge
       const int64_t po = ((int64_t)qi * p.hq + h) * p.n_chunks + c;
       if (any_tile) {
-        bar_wait(pv_done, (t - 1) & 1);
-        pv_seen = t;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int tl1 = t - 1;
+        PWAIT(&buf_free[tl1 % NB], (tl1 / NB) & 1, 0, 3);
+        fence_after();
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
+        for (int cc = 0; cc < 2; ++cc) {
           float o[32];
-          tmem_ld32(tmem_o + lane_base + 32 * cc, o);
+          tmem_ld32(tmem_o + lane_base + 64 * half + 32 * cc, o);
           if (real) {
-            float4* dst = reinterpret_cast<float4*>(p.part_o + po * D + 32 * cc);
+            float4* dst = reinterpret_cast<float4*>(p.part_o + po * D + 64 * half + 32 * cc);
 #pragma unroll
             for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
           }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        fence_before();
       } else if (real) {
-        float4* dst = reinterpret_cast<float4*>(p.part_o + po * D);
-        for (int i = 0; i < D / 4; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4* dst = reinterpret_cast<float4*>(p.part_o + po * D + 64 * half);
+        for (int i = 0; i < 16; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (real) {
+      if (half == 1) xl_u[r] = l_half;
+      named_sync(bar_id, 64);
+      if (half == 0 && real) {
         p.part_m[po] = m_run;
-        p.part_l[po] = l_run;
+        p.part_l[po] = l_half + xl_u[r];
       }
+      named_sync(bar_id, 64);
     }
   }
+#ifdef PF_PROF
+  if (threadIdx.x == 0 || threadIdx.x == 32 * kMmaWarp || threadIdx.x == 32 * kProducerWarp ||
+      threadIdx.x == 32 * kVProducerWarp) {
+    const int role = threadIdx.x == 0 ? 0 : threadIdx.x == 32 * kMmaWarp ? 1 : threadIdx.x == 32 * kProducerWarp ? 2 : 3;
+    atomicAdd(&g_pf_prof[role][15], (unsigned long long)(clock64() - prof_t0));
+  }
+#endif
   __syncthreads();
-  if (warp == 5) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == kMmaWarp) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -602,3 +824,13 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
 }
 
 }  // namespace rk
+
+#ifdef PF_PROF
+extern "C" int rk_pf_prof_read(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, rk::pf::g_pf_prof, sizeof(rk::pf::g_pf_prof));
+  unsigned long long z[4][16] = {};
+  cudaMemcpyToSymbol(rk::pf::g_pf_prof, z, sizeof(z));
+  return 0;
+}
+#endif
