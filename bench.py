@@ -39,9 +39,10 @@ WORKLOADS = {
     # the configs[4] batch sweep); --batch 1 --groups 1 for a single dialogue
     "c2": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512, batch=32,
                decode_steps=128, host_unique=4),
-    # Qwen2-7B-shaped, 64 rounds x 1K tokens (decode path; multi-row scoring lives in tests/kernels)
-    "c3": dict(num_layers=28, watershed=10, hq=28, hkv=4, head_dim=128, rounds=64, round_tokens=1024, batch=1,
-               decode_steps=128, host_unique=0),
+    # Qwen2-7B-shaped, 64 rounds x 1K tokens, 512-row question: tcgen05 prefill of the lower layers with the
+    # round scoring fused at layer Lw-1, then the upper layers over the kept rounds, then 128 answer tokens
+    "c3": dict(num_layers=28, watershed=10, hq=28, hkv=4, head_dim=128, rounds=64, round_tokens=1024, batch=8,
+               decode_steps=128, host_unique=2, question_rows=512),
     # Llama-3-8B-shaped 128K context, 16 dialogues, deep layers in pinned host memory
     "c4": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=128, round_tokens=1024, batch=16,
                decode_steps=64, host_unique=2),
@@ -212,8 +213,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         ms_e, _, brk_e, h2d_e, _ = timed(True, args.steps)
-        step_in = sum(e.turn_tokens * (e.q_in[0].numel() * 4 + e.kv_in[0].numel() * 2) for e in eng.groups)
-        step_out = sum((e.turn_tokens - 1) * e.out.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
+        step_in = sum(e.turn_tokens * (e.q_in[0].numel() * 4 + e.kv_in[0].numel() * 2)
+                      + (e.qq_in.numel() * 4 + e.qkv_in.numel() * 2 if e.nq > 1 else 0) for e in eng.groups)
+        step_out = sum(e.cfg.decode_steps * e.out.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
                        for e in eng.groups)
         e2e = {"value": world * tokens_per_turn * args.steps / (ms_e / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out),
@@ -235,13 +237,25 @@ def main():
         t = json.loads(tp.read_text())
         traffic = t["per_dialogue_token_bytes"] * cfg.batch
 
+    prefill = None
+    if g0.nq > 1:
+        # question prefill (tcgen05): lower layers incl. fused scoring = marks 0 -> 1 of group 0 (its own
+        # stream; the other group's decode runs beside it), algorithmic FLOPs of those layers
+        lw, nq = cfg.watershed, g0.nq
+        lower_flops = 4.0 * cfg.hq * cfg.head_dim * lw * (nq * g0.hist + nq * (nq + 1) / 2) * g0.cfg.batch
+        prefill = {"question_rows": nq, "flops_per_turn_all_layers": sum(e.prefill_flops_per_turn() for e in eng.groups),
+                   "lower_layers_ms_group0": brk["score_select"],
+                   "lower_layers_tflops_group0": lower_flops / (brk["score_select"] / 1000.0) / 1e12,
+                   "note": "lower-layer prefill + fused Lw-1 scoring + select, timed on group 0's stream while "
+                           "the other group decodes; kernel-alone figures: profiles/r01_prefill_c3.json"}
     line = {
         "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16 KV, fp32 accumulate", "data": "synthetic (random KV + activations)",
         "config": {"workload": f"{args.workload}: L={cfg.num_layers} Lw={cfg.watershed} Hq={cfg.hq} "
                                f"Hkv={cfg.hkv} d={cfg.head_dim} rounds={cfg.rounds}x{cfg.round_tokens} "
-                               f"K={g0.K} batch/GPU={cfg.batch} in {groups} groups tokens/turn={eng.turn_tokens}",
+                               f"K={g0.K} batch/GPU={cfg.batch} in {groups} groups question_rows={g0.nq} "
+                               f"decode tokens/turn={eng.turn_tokens}",
                    "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
                    "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
@@ -259,6 +273,8 @@ def main():
         "clocks": clocks,
         "kept_dialogue0": [int(x) for x in kept0[0]],
     }
+    if prefill:
+        line["prefill"] = prefill
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -39,6 +39,7 @@ import torch
 
 from . import _lib, kernels
 from .selection import SelectionPolicy, top_k_count
+from .stats import build_round_items
 
 
 @dataclass
@@ -58,6 +59,7 @@ class EngineConfig:
     input_period: int = 8         # distinct synthetic step inputs, cycled
     plant: int = 2                # rounds per dialogue with planted relevance at L_w-1 (0 = none)
     plant_beta: float = 0.25
+    question_rows: int = 1        # n_q: 1 = single-token question (decode kernel); > 1 = tensor-core prefill
 
     @property
     def group(self) -> int:
@@ -79,9 +81,13 @@ class RoundDecodeEngine:
         self.L_up = L - lw
         self.K = top_k_count(R, c.policy.fraction, c.policy.min_rounds)
         self.hist = R * T
-        self.turn_tokens = 1 + c.decode_steps                 # question token + answer tokens
-        self.s_lo = self.hist + self.turn_tokens
-        self.s_up = self.K * T + self.turn_tokens
+        self.nq = nq = max(1, c.question_rows)
+        # rows appended to the caches per turn; tokens the decode metric counts
+        # (a 1-row question runs through the decode kernel and counts as one)
+        self.turn_rows = nq + c.decode_steps
+        self.turn_tokens = 1 + c.decode_steps if nq == 1 else c.decode_steps
+        self.s_lo = self.hist + self.turn_rows
+        self.s_up = self.K * T + self.turn_rows
         self.row = c.hkv * c.head_dim                         # elements per key (all heads)
         g = torch.Generator(device="cpu").manual_seed(seed)
         gd = torch.Generator(device=self.dev).manual_seed(seed + 1)
@@ -107,7 +113,7 @@ class RoundDecodeEngine:
                     flat[s0:s0 + n].copy_(pool[o:o + n])
                 blocks.append(blk)
             self.host_blocks.append(blocks)
-        self.writeback = torch.empty((B, self.L_up, 2, self.turn_tokens, c.hkv, c.head_dim), dtype=self.dtype,
+        self.writeback = torch.empty((B, self.L_up, 2, self.turn_rows, c.hkv, c.head_dim), dtype=self.dtype,
                                      pin_memory=True)
 
         # ---- lengths (device) and their per-turn reset values
@@ -117,9 +123,10 @@ class RoundDecodeEngine:
         self.upper_len0 = torch.full((B,), self.K * T, dtype=torch.int32, device=self.dev)
 
         # ---- round-aligned scoring items at layer L_w-1 (prior rounds + the question token)
-        bounds = [[(r * T, (r + 1) * T, r) for r in range(R)] + [(self.hist, self.hist + 1, R)]
+        bounds = [[(r * T, (r + 1) * T, r) for r in range(R)] + [(self.hist, self.hist + self.nq, R)]
                   for _ in range(B)]
         self.items, self.n_items = kernels.items_tensor(bounds, c.item_chunk, self.dev)
+        self.n_items_host = [len(build_round_items(b_, c.item_chunk)) for b_ in bounds]
         if self.items.shape[1] > 512:
             raise ValueError("too many scoring items; raise item_chunk")
 
@@ -129,6 +136,18 @@ class RoundDecodeEngine:
         self.q_in = torch.randn((P, L, B, c.hq, c.head_dim), generator=gd, device=self.dev)
         self.kv_in = torch.randn((P, L, 2, B, c.hkv, c.head_dim), generator=gd, device=self.dev).to(self.dtype)
         self.out = torch.empty((L, B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+        if nq > 1:
+            # multi-row question: per-layer query rows and new K/V rows (positions hist ..)
+            self.qq_in = torch.randn((L, B, nq, c.hq, c.head_dim), generator=gd, device=self.dev)
+            self.qkv_in = torch.randn((L, 2, B, nq, c.hkv, c.head_dim), generator=gd, device=self.dev).to(self.dtype)
+            self.qout = torch.empty((B, nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+            self.q_pos = torch.arange(self.hist, self.hist + nq, dtype=torch.int64, device=self.dev)
+            self.k_pos_lo = torch.arange(self.hist + nq, dtype=torch.int64, device=self.dev)
+            self.k_pos_up = torch.zeros((B, self.K * T + nq), dtype=torch.int64, device=self.dev)
+            self.k_pos_up_host = torch.zeros((B, self.K * T + nq), dtype=torch.int64, pin_memory=True)
+            self.bad_row = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self.lower_len_q = torch.full((B,), self.hist + nq, dtype=torch.int32, device=self.dev)
+            self.upper_len_q = torch.full((B,), self.K * T + nq, dtype=torch.int32, device=self.dev)
         if c.plant:
             self._plant(gd)
 
@@ -164,7 +183,10 @@ class RoundDecodeEngine:
         K-boundary gap is wide (SURVEY.md §8d planted relevance)."""
         c = self.cfg
         lw1 = c.watershed - 1
-        q = self.q_in[0, lw1].view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)   # (B, Hkv, d)
+        if self.nq > 1:       # mean direction of the question rows
+            q = self.qq_in[lw1].mean(dim=1).view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)
+        else:
+            q = self.q_in[0, lw1].view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)   # (B, Hkv, d)
         u = q / q.norm(dim=-1, keepdim=True)
         rng = np.random.default_rng(1234)
         self.planted = []
@@ -196,7 +218,9 @@ class RoundDecodeEngine:
         return 2                                            # decode + merge
 
     def _phase_a(self):
-        """Question token through the lower layers, fused scoring, selection."""
+        """Question through the lower layers, fused scoring, selection."""
+        if self.nq > 1:
+            return self._phase_a_prefill()
         c = self.cfg
         self.lower_len.copy_(self.lower_len0)
         self.upper_len.copy_(self.upper_len0)
@@ -206,6 +230,65 @@ class RoundDecodeEngine:
                                        self.ws, raw=self.raw, kv_dtype=self.dtype)
         self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(
             self.raw, "top_percent", k_top=self.K)
+
+    # ---- multi-row question: tensor-core prefill (rk_prefill_attention) ------
+    def _phase_a_prefill(self):
+        """n_q question rows through the lower layers (causal over the full
+        history + the question, pipeline.py:225-230); at layer L_w-1 the same
+        pass leaves the Eq. 1 round masses (fused scoring), then selection."""
+        c = self.cfg
+        nq, hist = self.nq, self.hist
+        for l in range(c.watershed):
+            last = l == c.watershed - 1
+            for b in range(c.batch):
+                self.lower[b, l, :, hist:hist + nq].copy_(self.qkv_in[l, :, b])     # append the question's K/V
+                kernels.prefill_attention(
+                    self.qq_in[l, b], self.lower[b, l, 0, :hist + nq], self.lower[b, l, 1, :hist + nq],
+                    self.q_pos, self.k_pos_lo, out=self.qout[b], bad_row=self.bad_row,
+                    items=self.items[b, :self.n_items_host[b]] if last else None,
+                    n_bins=c.rounds if last else 0, raw=self.raw[b] if last else None)
+        self.lower_len.copy_(self.lower_len_q)
+        self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(self.raw, "top_percent", k_top=self.K)
+
+    def _phase_b1_prefill(self, kept, layer_wait: bool):
+        """n_q question rows through the upper layers over the kept rounds +
+        the question (pipeline.py:292-296); positions keep their original
+        values, so the splice equals the masked attention (engine.py:94-112)."""
+        c = self.cfg
+        nq, T, KT = self.nq, c.round_tokens, self.K * c.round_tokens
+        for b in range(c.batch):       # key positions of the spliced cache: kept rounds ascending, question
+            pos = self.k_pos_up_host[b]
+            for i, r in enumerate(kept[b]):
+                pos[i * T:(i + 1) * T] = torch.arange(int(r) * T, (int(r) + 1) * T)
+            pos[KT:KT + nq] = torch.arange(self.hist, self.hist + nq)
+        self.k_pos_up.copy_(self.k_pos_up_host, non_blocking=True)
+        for l in range(c.watershed, c.num_layers):
+            u = l - c.watershed
+            if layer_wait:
+                torch.cuda.current_stream().wait_event(self.layer_events[u])
+            for b in range(c.batch):
+                self.upper[b, u, :, KT:KT + nq].copy_(self.qkv_in[l, :, b])
+                kernels.prefill_attention(
+                    self.qq_in[l, b], self.upper[b, u, 0, :KT + nq], self.upper[b, u, 1, :KT + nq],
+                    self.q_pos, self.k_pos_up[b], out=self.qout[b], bad_row=self.bad_row)
+        self.upper_len.copy_(self.upper_len_q)
+
+    def _phase_b1_any(self, kept, layer_wait: bool):
+        if self.nq > 1:
+            self._phase_b1_prefill(kept, layer_wait)
+        else:
+            self._phase_b1(layer_wait)
+
+    def prefill_flops_per_turn(self) -> float:
+        """Algorithmic FLOPs of the question prefill (QK^T + PV once, causal
+        visible pairs only): 4 * Hq * d per visible (row, key) pair."""
+        if self.nq == 1:
+            return 0.0
+        c = self.cfg
+        nq = self.nq
+        causal = nq * (nq + 1) / 2
+        pairs = c.watershed * (nq * self.hist + causal) + self.L_up * (nq * self.K * c.round_tokens + causal)
+        return 4.0 * c.hq * c.head_dim * pairs * c.batch
 
     def _phase_b1(self, layer_wait: bool):
         """Question token through the upper layers (each waits for its rows)."""
@@ -218,7 +301,7 @@ class RoundDecodeEngine:
     def _phase_b2(self, e2e: bool = False):
         """Answer tokens: all L layers per token."""
         c = self.cfg
-        for t in range(1, self.turn_tokens):
+        for t in range(1, c.decode_steps + 1):
             if e2e:
                 p = t % self.period
                 self.q_in[p].copy_(self.host_q[p], non_blocking=True)
@@ -281,7 +364,12 @@ class RoundDecodeEngine:
             self.host_q.copy_(self.q_in)
             self.host_kv = torch.empty(self.kv_in.shape, dtype=self.kv_in.dtype, pin_memory=True)
             self.host_kv.copy_(self.kv_in)
-            self.host_out = torch.empty((self.turn_tokens,) + tuple(self.out.shape), dtype=torch.float32,
+            if self.nq > 1:
+                self.host_qq = torch.empty(self.qq_in.shape, dtype=self.qq_in.dtype, pin_memory=True)
+                self.host_qq.copy_(self.qq_in)
+                self.host_qkv = torch.empty(self.qkv_in.shape, dtype=self.qkv_in.dtype, pin_memory=True)
+                self.host_qkv.copy_(self.qkv_in)
+            self.host_out = torch.empty((c.decode_steps + 1,) + tuple(self.out.shape), dtype=torch.float32,
                                         pin_memory=True)
         with torch.cuda.stream(self.compute_stream):
             self.run_turn_eager()                     # warm-up, sets kernel attributes
@@ -317,7 +405,7 @@ class RoundDecodeEngine:
         kept = self._select_to_host()
         self.copy_stream.wait_stream(torch.cuda.current_stream())
         self.issue_gather(self.gather_plan(kept))
-        self._phase_b1(layer_wait=True)
+        self._phase_b1_any(kept, layer_wait=True)
         self._phase_b2()
         self.decode_done.record()
         self.copy_stream.wait_event(self.decode_done)
@@ -337,9 +425,13 @@ class RoundDecodeEngine:
         with torch.cuda.stream(self.compute_stream):
             m[0].record()
             if e2e:
-                # the question token's inputs come from pinned host memory too
-                self.q_in[0].copy_(self.host_q[0], non_blocking=True)
-                self.kv_in[0].copy_(self.host_kv[0], non_blocking=True)
+                # the question's inputs come from pinned host memory too
+                if self.nq > 1:
+                    self.qq_in.copy_(self.host_qq, non_blocking=True)
+                    self.qkv_in.copy_(self.host_qkv, non_blocking=True)
+                else:
+                    self.q_in[0].copy_(self.host_q[0], non_blocking=True)
+                    self.kv_in[0].copy_(self.host_kv[0], non_blocking=True)
             self.graph_a.replay()
             m[1].record()
             kept = self._select_to_host()
@@ -349,7 +441,7 @@ class RoundDecodeEngine:
             nbytes = self.issue_gather(plans)
             self.copy_marks[1].record(self.copy_stream)
             self.last_h2d_bytes = nbytes
-            self._phase_b1(layer_wait=True)
+            self._phase_b1_any(kept, layer_wait=True)
             m[2].record()
             if self.window_log is not None:          # per-turn decode window (bench roofline)
                 a = torch.cuda.Event(enable_timing=True)
@@ -380,6 +472,8 @@ class RoundDecodeEngine:
     def kernel_launches_per_turn(self) -> int:
         c = self.cfg
         per_layer = 2                                   # bulk decode + merge
+        if self.nq > 1:   # prefill per (layer, dialogue): bad-row fill, q prep, tcgen05 pass, merge (+2 scoring)
+            return (c.num_layers * c.batch * 4 + 2 * c.batch + c.num_layers * per_layer * c.decode_steps + 1)
         return (c.num_layers * per_layer * self.turn_tokens   # question token + answer tokens
                 + 2)                                    # score finalize + batched select
 
@@ -389,7 +483,7 @@ class RoundDecodeEngine:
         layers): K and V of every visible key, SURVEY.md §8d."""
         c = self.cfg
         es = 2
-        mid = self.turn_tokens // 2
+        mid = self.nq + c.decode_steps // 2           # mean rows of the turn visible to a decode token
         lower = c.watershed * (self.hist + mid) * self.row * 2 * es
         upper = self.L_up * (self.K * c.round_tokens + mid) * self.row * 2 * es
         return c.batch * (lower + upper)
@@ -398,9 +492,9 @@ class RoundDecodeEngine:
         """(resident KV bytes of the round engine, full-cache bytes) at turn end."""
         c = self.cfg
         es = 2
-        full = c.batch * c.num_layers * 2 * (self.hist + self.turn_tokens) * self.row * es
-        resident = c.batch * 2 * self.row * es * (c.watershed * (self.hist + self.turn_tokens)
-                                                   + self.L_up * (self.K * c.round_tokens + self.turn_tokens))
+        full = c.batch * c.num_layers * 2 * (self.hist + self.turn_rows) * self.row * es
+        resident = c.batch * 2 * self.row * es * (c.watershed * (self.hist + self.turn_rows)
+                                                   + self.L_up * (self.K * c.round_tokens + self.turn_rows))
         return resident, full
 
 
@@ -478,8 +572,8 @@ class GroupedDecoder:
         if cur1 is not None:
             busy += cur1 - cur0
         self.last_decode_busy_ms = busy
-        self.last_decode_bytes = turns * sum((e.turn_tokens - 1) * e.kv_bytes_per_token() for e in self.groups)
-        self.last_decode_launches = turns * sum(e.cfg.num_layers * e.launches_per_layer() * (e.turn_tokens - 1)
+        self.last_decode_bytes = turns * sum(e.cfg.decode_steps * e.kv_bytes_per_token() for e in self.groups)
+        self.last_decode_launches = turns * sum(e.cfg.num_layers * e.launches_per_layer() * e.cfg.decode_steps
                                                 for e in self.groups)
         for eng in self.groups:
             eng.window_log = None

@@ -85,3 +85,66 @@ def test_engine_accounting():
     resident, full = eng.gpu_kv_bytes()
     assert 1 - resident / full > 0.54                      # >= 54 % GPU KV saved (north star)
     assert eng.K == 4
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_engine_prefill_turn_matches_oracle(graphs):
+    """Multi-row question (tcgen05 prefill, fused scoring at Lw-1): kept rounds
+    equal the oracle's selection from the capture of ALL question rows
+    (aggregate_round_attention over rows, stats.py:59-94); the question's upper
+    layers attend kept rounds + the question with original positions
+    (pipeline.py:292-296); the decode tokens then see the history / kept
+    rounds plus every row of the turn."""
+    nq, hkv, G = 40, 2, 4
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=hkv * G, hkv=hkv, head_dim=128, rounds=7, round_tokens=128,
+                       batch=2, decode_steps=4, policy=SelectionPolicy("top_percent", fraction=0.3),
+                       item_chunk=128, input_period=3, plant=2, plant_beta=0.3, question_rows=nq)
+    eng = RoundDecodeEngine(cfg, seed=5)
+    lw, L, T, R, hist = cfg.watershed, cfg.num_layers, cfg.round_tokens, cfg.rounds, eng.hist
+    lower0 = _f(eng.lower[:, :, :, :hist])
+    if graphs:
+        eng.prepare(e2e=False)
+        kept, _ = eng.run_turn()
+        kept, _ = eng.run_turn()
+    else:
+        with torch.cuda.stream(eng.compute_stream):
+            kept = eng.run_turn_eager()
+    torch.cuda.synchronize()
+    P = eng.period
+    qpos = np.arange(hist, hist + nq)
+    for b in range(cfg.batch):
+        # ---- selection from the question rows' capture at layer Lw-1
+        qq = _f(eng.qq_in[lw - 1, b])
+        kq = np.concatenate([lower0[b, lw - 1, 0], _f(eng.qkv_in[lw - 1, 0, b])])
+        _, cap = oatt.attention_forward_gqa(qq, kq, kq, qpos, np.arange(hist + nq), capture=True)
+        rounds = [orr.Round(r, (r * T, r * T + 1), (r * T + 1, (r + 1) * T)) for r in range(R)]
+        rounds.append(orr.Round(R, (hist, hist + nq), (hist + nq, hist + nq)))
+        raw = orr.aggregate_round_attention(cap, rounds, "question", R, active_rounds=list(range(R)),
+                                            row_offset=hist)
+        want = orr.select(orr.normalize(raw), orr.SelectionPolicy("top_percent", fraction=0.3))
+        assert tuple(int(x) for x in kept[b]) == want
+        # ---- last decode token at a lower and an upper layer
+        for l in (0, lw - 1, lw, L - 1):
+            qk, qv = _f(eng.qkv_in[l, 0, b]), _f(eng.qkv_in[l, 1, b])
+            rows_k = np.stack([_f(eng.kv_in[t % P, l, 0, b]) for t in range(1, cfg.decode_steps + 1)])
+            rows_v = np.stack([_f(eng.kv_in[t % P, l, 1, b]) for t in range(1, cfg.decode_steps + 1)])
+            if l < lw:
+                K = np.concatenate([lower0[b, l, 0], qk, rows_k])
+                V = np.concatenate([lower0[b, l, 1], qv, rows_v])
+            else:
+                hs = b % eng.host_sets
+                blocks = [eng.host_blocks[hs][int(r)][l - lw] for r in kept[b]]
+                K = np.concatenate([_f(bk[0]) for bk in blocks] + [qk, rows_k])
+                V = np.concatenate([_f(bk[1]) for bk in blocks] + [qv, rows_v])
+            q = _f(eng.q_in[cfg.decode_steps % P, l, b])[None]
+            ref, _ = oatt.attention_forward_gqa(q, K, V, [len(K) - 1], np.arange(len(K)))
+            err = np.abs(_f(eng.out[l, b]).reshape(1, -1) - ref).max() / np.abs(ref).max()
+            assert err < 1e-4, (l, err)
+        # ---- the question's last upper layer: kept rounds + causal question, original positions
+        blocks = [eng.host_blocks[b % eng.host_sets][int(r)][L - 1 - lw] for r in kept[b]]
+        K = np.concatenate([_f(bk[0]) for bk in blocks] + [_f(eng.qkv_in[L - 1, 0, b])])
+        V = np.concatenate([_f(bk[1]) for bk in blocks] + [_f(eng.qkv_in[L - 1, 1, b])])
+        kpos = np.concatenate([np.arange(int(r) * T, (int(r) + 1) * T) for r in kept[b]] + [qpos])
+        ref, _ = oatt.attention_forward_gqa(_f(eng.qq_in[L - 1, b]), K, V, qpos, kpos)
+        got = _f(eng.qout[b]).reshape(nq, -1)
+        assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-4
