@@ -9,13 +9,6 @@
 #include "prefill_tc.cuh"
 #include <cstdlib>
 
-namespace rk {
-bool score_tc_supported(int kv_dtype, int d, int n_q, int G);
-size_t score_tc_scratch_bytes(int n_q, int hkv, int G);
-int launch_score_tc(const float* q, int n_q, int hq, const void* k, int s, int hkv, const int64_t* q_pos,
-                    const int64_t* k_pos, const int32_t* items, int n_items, float* part_m, float* part_l,
-                    void* qs_scratch, cudaStream_t st);
-}  // namespace rk
 
 
 namespace rk {
@@ -386,22 +379,24 @@ int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream) {
   return RK_OK;
 }
 
-// the tcgen05 path (score_tc.cu) serves bf16 K, d = 128, >= 64 stacked rows;
-// RK_SCORE_TC=0 forces the CUDA-core split kernel (tests compare both)
+// the tcgen05 path (prefill_tc.cu, scores-only kernel) serves bf16 K, d = 128,
+// >= 64 stacked rows; RK_SCORE_TC=0 forces the CUDA-core split kernel (tests compare both)
 static bool use_tc(int kv_dtype, int d, int n_q, int G) {
   static int env = -1;
   if (env < 0) {
     const char* e = std::getenv("RK_SCORE_TC");
     env = (e && e[0] == '0') ? 0 : 1;
   }
-  return env && score_tc_supported(kv_dtype, d, n_q, G);
+  return env && prefill_tc_supported(kv_dtype, d, n_q, G);
 }
 
 size_t rk_round_scores_workspace_bytes(int n_q, int hq, int hkv, int n_items, int d, int n_bins) {
-  if (n_q <= 0 || n_items <= 0 || hkv <= 0) return 256;
+  if (n_q <= 0 || n_items <= 0 || hkv <= 0 || hq % hkv) return 256;
   size_t a = carve(nullptr, n_q, hq, hkv, n_items, d).bytes;
   a = align_up(a + sizeof(double) * (size_t)n_q * (n_bins > 0 ? n_bins : 1), 256);
-  return align_up(a + score_tc_scratch_bytes(n_q, hkv, hq / hkv), 256);
+  if (prefill_tc_supported(RK_BF16, d, n_q, hq / hkv))
+    a = align_up(a + prefill_plan(n_q, hq, hkv, 0, n_items, true, false).total, 256);
+  return a;
 }
 
 int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int kv_dtype, int s, int hkv,
@@ -417,13 +412,18 @@ int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int k
   size_t need = align_up(w.bytes + sizeof(double) * (size_t)n_q * n_bins, 256);
   if (need > workspace_bytes) return fail(RK_ERR_CAPACITY, "score workspace %zu < %zu", workspace_bytes, need);
   double* rows_mass = reinterpret_cast<double*>(static_cast<char*>(workspace) + w.bytes);
-  const size_t tc_off = align_up(w.bytes + sizeof(double) * (size_t)n_q * n_bins, 256);
+  const float* part_m = w.part_m;
+  const float* part_l = w.part_l;
   if (use_tc(kv_dtype, d, n_q, hq / hkv)) {
-    if (tc_off + score_tc_scratch_bytes(n_q, hkv, hq / hkv) > workspace_bytes)
+    const size_t tc_bytes = prefill_plan(n_q, hq, hkv, s, n_items, true, false).total;
+    if (need + tc_bytes > workspace_bytes)
       return fail(RK_ERR_CAPACITY, "score workspace too small for the tensor-core path");
-    st = launch_score_tc(q, n_q, hq, k, s, hkv, q_pos, k_pos, items, n_items, w.part_m, w.part_l,
-                         static_cast<char*>(workspace) + tc_off, cs);
+    float *im = nullptr, *il = nullptr;
+    st = launch_prefill_tc(q, n_q, hq, k, nullptr, s, hkv, q_pos, k_pos, nullptr, items, n_items, true, nullptr,
+                           nullptr, static_cast<char*>(workspace) + need, tc_bytes, &im, &il, nullptr, nullptr, cs);
     if (st) return st;
+    part_m = im;
+    part_l = il;
   } else {
   SplitParams p{};
   p.q = q; p.k = k; p.v = k;
@@ -440,7 +440,7 @@ int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int k
   if (st) return st;
   }
   score_rows_kernel<<<n_q, 128, score_rows_smem(n_bins, hq), cs>>>(
-      w.part_m, w.part_l, n_items, 1, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
+      part_m, part_l, n_items, 1, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
   RK_CHECK_LAUNCH("score_rows_kernel");
   score_sum_rows_kernel<<<(n_bins + 127) / 128, 128, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
   RK_CHECK_LAUNCH("score_sum_rows_kernel");

@@ -231,6 +231,9 @@ __device__ __forceinline__ void tmem_st32u(uint32_t addr, const uint32_t (&v)[32
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// SCORE_ONLY: the watershed scorer (rk_round_scores) — QK^T and the per-item
+// softmax statistics only: no V, no PV, no O, no row-max exchange.
+template <bool SCORE_ONLY>
 __global__ void __launch_bounds__(THREADS, 1)
 prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                   const __grid_constant__ CUtensorMap vmap, const __grid_constant__ Params p) {
@@ -366,20 +369,22 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
       __syncwarp();
     }
   } else if (warp == kVProducerWarp) {
-    // ================= V producer: V of tile t once PV_{t-STAGES} freed its slot
-    // (a separate warp so the K loads, needed a tile earlier, never queue behind it)
-    TileIter ti;
-    ti.init(p, u0, u1);
-    const uint32_t vs_a = sa(vs);
-    for (int t = 0; ti.valid; ++t, ti.advance()) {
-      const int kvh = ti.mtile / p.mtiles, s = t % STAGES;
-      if (t >= STAGES) PWAIT(&v_empty[s], ((t / STAGES) - 1) & 1, 3, 0);
-      if (elect_one()) {
-        bar_expect(&v_full[s], KV_STAGE);
-        tma_2d_s(vs_a + s * KV_STAGE, &vmap, kvh * D, ti.j0, &v_full[s]);
-        tma_2d_s(vs_a + s * KV_STAGE + KBOX, &vmap, kvh * D + 64, ti.j0, &v_full[s]);
+    if (!SCORE_ONLY) {
+      // ================= V producer: V of tile t once PV_{t-STAGES} freed its slot
+      // (a separate warp so the K loads, needed a tile earlier, never queue behind it)
+      TileIter ti;
+      ti.init(p, u0, u1);
+      const uint32_t vs_a = sa(vs);
+      for (int t = 0; ti.valid; ++t, ti.advance()) {
+        const int kvh = ti.mtile / p.mtiles, s = t % STAGES;
+        if (t >= STAGES) PWAIT(&v_empty[s], ((t / STAGES) - 1) & 1, 3, 0);
+        if (elect_one()) {
+          bar_expect(&v_full[s], KV_STAGE);
+          tma_2d_s(vs_a + s * KV_STAGE, &vmap, kvh * D, ti.j0, &v_full[s]);
+          tma_2d_s(vs_a + s * KV_STAGE + KBOX, &vmap, kvh * D + 64, ti.j0, &v_full[s]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer.  The whole warp runs the (uniform) control
@@ -429,6 +434,14 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
     while (pi.valid) {
       const int b = tp % NB, s = tp % STAGES;
       PWAIT(&p_full[b], (tp / NB) & 1, 1, 3);
+      if (SCORE_ONLY) {               // S_tp consumed: its buffer is free (nothing async to wait for)
+        if (elect_one()) bar_arrive(&buf_free[b]);
+        __syncwarp();
+        ++tp;
+        pi.advance();
+        if (qi.valid) issue_qk();
+        continue;
+      }
       PWAIT(&v_full[s], (tp / STAGES) & 1, 1, 4);
       fence_after();
       if (elect_one()) {
@@ -496,6 +509,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
               sc[32 + i] = v1[i];
             }
           }
+          if (SCORE_ONLY) {                             // S is in registers: release the buffer now
+            fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&p_full[b]);
+          }
 
           if (!__all_sync(0xffffffffu, all_vis)) {     // diagonal / masked tile: per-key check
             const int nv = min(BN, hi - j0);
@@ -512,6 +530,29 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           float hmax = -INFINITY;
 #pragma unroll
           for (int i = 0; i < HK; ++i) hmax = fmaxf(hmax, sc[i]);
+          if (SCORE_ONLY) {
+            // this half's (max, sum) of the tile, folded into the item statistics
+            if (hmax != -INFINITY) {
+              float2 acc2 = make_float2(0.f, 0.f);
+              const float2 nm = make_float2(-hmax, -hmax), one = make_float2(1.f, 1.f);
+#pragma unroll
+              for (int i = 0; i < HK; i += 2) {
+                const float2 dlt = ffma2(make_float2(sc[i], sc[i + 1]), one, nm);
+                acc2 = ffma2(make_float2(fast_exp2(dlt.x), fast_exp2(dlt.y)), one, acc2);
+              }
+              const float tl = acc2.x + acc2.y;
+              if (m_it == -INFINITY) {
+                m_it = hmax;
+                l_it = tl;
+              } else {
+                const float M = fmaxf(m_it, hmax);
+                l_it = l_it * fast_exp2(m_it - M) + tl * fast_exp2(hmax - M);
+                m_it = M;
+              }
+            }
+            any_tile = true;
+            continue;
+          }
           xmax[(t & 1) * 256 + half * 128 + r] = hmax;
           fence_before();                                // our S reads precede the partner's P writes
 #ifdef PF_PROF
@@ -616,6 +657,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           named_sync(bar_id, 64);
         }
       }
+      if (SCORE_ONLY) continue;
       // ---- unit end: O after the last PV, partial (m, l, O) for the merge
       const int64_t po = ((int64_t)qi * p.hq + h) * p.n_chunks + c;
       if (any_tile) {
@@ -725,7 +767,7 @@ bool prefill_tc_supported(int kv_dtype, int d, int n_q, int G) {
 }
 
 // item table: `items` (n_items given) or uniform items of item_keys keys over s
-PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool stats) {
+PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool stats, bool with_output) {
   PrefillPlan pl{};
   const int G = hq / hkv;
   pl.mpad = (G * n_q + pf::BM - 1) / pf::BM * pf::BM;
@@ -747,7 +789,8 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
   pl.n_units = mt_total * pl.n_chunks;
   pl.qs_bytes = align_up((size_t)hkv * 2 * pl.mpad * pf::D * 2, 256);
   const size_t rh = (size_t)n_q * hq;
-  pl.part_bytes = align_up(rh * pl.n_chunks * 4, 256) * 2 + align_up(rh * pl.n_chunks * pf::D * 4, 256);
+  pl.part_bytes = with_output ? align_up(rh * pl.n_chunks * 4, 256) * 2 + align_up(rh * pl.n_chunks * pf::D * 4, 256)
+                              : 0;
   pl.item_bytes = stats ? align_up(rh * pl.n_items * 4, 256) * 2 : 0;
   pl.total = pl.qs_bytes + pl.part_bytes + pl.item_bytes + align_up(rh * 4, 256) * 2;
   return pl;
@@ -762,18 +805,23 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
                       float** item_m_out, float** item_l_out, float** stat_m_out, float** stat_l_out,
                       cudaStream_t st) {
   const int G = hq / hkv;
-  PrefillPlan pl = prefill_plan(n_q, hq, hkv, s, items ? n_items_in : 0, stats);
+  const bool score_only = out == nullptr;          // the watershed scorer: statistics only
+  if (score_only && !stats) return fail(RK_ERR_DOMAIN, "prefill without output needs the scoring statistics");
+  PrefillPlan pl = prefill_plan(n_q, hq, hkv, s, items ? n_items_in : 0, stats, !score_only);
   if (pl.total > ws_bytes) return fail(RK_ERR_CAPACITY, "prefill workspace %zu < %zu", ws_bytes, pl.total);
   char* b = static_cast<char*>(ws);
   const size_t rh = (size_t)n_q * hq;
   __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(b);
   b += pl.qs_bytes;
-  float* part_m = reinterpret_cast<float*>(b);
-  b += align_up(rh * pl.n_chunks * 4, 256);
-  float* part_l = reinterpret_cast<float*>(b);
-  b += align_up(rh * pl.n_chunks * 4, 256);
-  float* part_o = reinterpret_cast<float*>(b);
-  b += align_up(rh * pl.n_chunks * pf::D * 4, 256);
+  float *part_m = nullptr, *part_l = nullptr, *part_o = nullptr;
+  if (!score_only) {
+    part_m = reinterpret_cast<float*>(b);
+    b += align_up(rh * pl.n_chunks * 4, 256);
+    part_l = reinterpret_cast<float*>(b);
+    b += align_up(rh * pl.n_chunks * 4, 256);
+    part_o = reinterpret_cast<float*>(b);
+    b += align_up(rh * pl.n_chunks * pf::D * 4, 256);
+  }
   float* item_m = nullptr;
   float* item_l = nullptr;
   if (stats) {
@@ -798,7 +846,7 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
   if (r) return r;
   r = tc::make_map(&kmap, k, (uint64_t)hkv * pf::D, (uint64_t)s, (uint64_t)hkv * pf::D * 2, pf::BN);
   if (r) return r;
-  r = tc::make_map(&vmap, v, (uint64_t)hkv * pf::D, (uint64_t)s, (uint64_t)hkv * pf::D * 2, pf::BN);
+  r = tc::make_map(&vmap, score_only ? k : v, (uint64_t)hkv * pf::D, (uint64_t)s, (uint64_t)hkv * pf::D * 2, pf::BN);
   if (r) return r;
   pf::Params p{};
   p.n_q = n_q; p.hq = hq; p.hkv = hkv; p.G = G; p.mpad = pl.mpad; p.mtiles = pl.mtiles;
@@ -809,12 +857,19 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
   p.part_m = part_m; p.part_l = part_l; p.part_o = part_o;
   static bool configured = false;
   if (!configured) {
-    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pf::SMEM),
-            "prefill_tc smem attribute");
+    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pf::SMEM), "prefill_tc smem attribute");
+    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pf::SMEM), "prefill_tc smem attribute");
     configured = true;
   }
   const int grid = std::min(sm_count(), pl.n_units);
-  pf::prefill_tc_kernel<<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
+  if (score_only) {
+    pf::prefill_tc_kernel<true><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
+    RK_CHECK_LAUNCH("prefill_tc_kernel<score>");
+    return RK_OK;
+  }
+  pf::prefill_tc_kernel<false><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
   RK_CHECK_LAUNCH("prefill_tc_kernel");
   const int nrh = (int)rh;
   pf::prefill_merge_kernel<<<(nrh * 32 + 255) / 256, 256, 0, st>>>(part_m, part_l, part_o, nrh, hq, pl.n_chunks,

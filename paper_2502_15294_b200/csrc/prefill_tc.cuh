@@ -13,9 +13,12 @@ struct PrefillPlan {
 };
 
 // work decomposition and workspace size; n_items_in > 0: caller's item table,
-// else uniform 512-key items over s.  stats: per-item scoring statistics.
-PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool stats);
+// else uniform 512-key items over s.  stats: per-item scoring statistics;
+// with_output = false: the scores-only pass (no O partials).
+PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool stats, bool with_output = true);
 
+// out == nullptr runs the scores-only kernel (the multi-row watershed scorer):
+// item_m/item_l [n_q][hq][n_items] only, stats must be true.
 int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void* v, int s, int hkv,
                       const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed, const int32_t* items,
                       int n_items_in, bool stats, float* out, int32_t* bad_row, void* ws, size_t ws_bytes,

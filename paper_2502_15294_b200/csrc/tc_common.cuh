@@ -1,6 +1,6 @@
 // tcgen05 / TMA / mbarrier helpers shared by the tensor-core kernels
-// (score_tc.cu: multi-row watershed scoring; prefill_tc.cu: question prefill
-// attention).  Raw PTX for sm_100a; descriptor encodings follow the sm100 UMMA
+// (prefill_tc.cu: question prefill attention and, in its scores-only form, the
+// multi-row watershed scorer).  Raw PTX for sm_100a; descriptor encodings follow the sm100 UMMA
 // shared-memory descriptor (start >> 4, LBO >> 4, SBO >> 4, version 1,
 // layout type) and the kind::f16 instruction descriptor.
 #pragma once
