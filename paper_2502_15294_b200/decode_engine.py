@@ -135,7 +135,10 @@ class RoundDecodeEngine:
         self.period = P
         self.q_in = torch.randn((P, L, B, c.hq, c.head_dim), generator=gd, device=self.dev)
         self.kv_in = torch.randn((P, L, 2, B, c.hkv, c.head_dim), generator=gd, device=self.dev).to(self.dtype)
-        self.out = torch.empty((L, B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+        # per-token attention outputs, double-buffered so the end-to-end path can
+        # read token t back to the host while token t+1 computes
+        self.out_buf = torch.empty((2, L, B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+        self.out = self.out_buf[0]
         if nq > 1:
             # multi-row question: per-layer query rows and new K/V rows (positions hist ..)
             self.qq_in = torch.randn((L, B, nq, c.hq, c.head_dim), generator=gd, device=self.dev)
@@ -199,7 +202,7 @@ class RoundDecodeEngine:
                 self.lower[b, lw1, 0, r * c.round_tokens:(r + 1) * c.round_tokens] = sl.to(self.dtype)
 
     # ------------------------------------------------------------------ kernels
-    def _layer(self, l: int, step: int, advance: bool, items: bool = False):
+    def _layer(self, l: int, step: int, advance: bool, items: bool = False, out=None):
         c = self.cfg
         p = step % self.period
         if l < c.watershed:
@@ -211,7 +214,8 @@ class RoundDecodeEngine:
             cap = self.s_up
         kernels.decode_attention(self.q_in[p, l], kc, vc, ln, cap, k_new=self.kv_in[p, l, 0],
                                  v_new=self.kv_in[p, l, 1], items=self.items if items else None,
-                                 n_items=self.n_items if items else None, out=self.out[l], ws=self.ws,
+                                 n_items=self.n_items if items else None,
+                                 out=(self.out if out is None else out)[l], ws=self.ws,
                                  advance=ln if advance else None)
 
     def launches_per_layer(self) -> int:
@@ -299,17 +303,51 @@ class RoundDecodeEngine:
             self._layer(l, 0, advance=(l == c.num_layers - 1))
 
     def _phase_b2(self, e2e: bool = False):
-        """Answer tokens: all L layers per token."""
+        """Answer tokens: all L layers per token.
+
+        End to end (e2e), every token's q/k/v come from pinned host memory and
+        its attention outputs go back to it.  The copies run on the e2e copy
+        stream, pipelined against the decode kernels: token t+1's inputs load
+        while token t computes (input slots cycle with period P, a slot is
+        reloaded only after the token that last read it finished), and token
+        t's outputs (double buffer) drain while token t+1 computes."""
         c = self.cfg
-        for t in range(1, c.decode_steps + 1):
-            if e2e:
-                p = t % self.period
+        T = c.decode_steps
+        if not e2e:
+            for t in range(1, T + 1):
+                for l in range(c.num_layers):
+                    self._layer(l, t, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
+            return
+        cs, cp = torch.cuda.current_stream(), self.e2e_stream
+        ev = self.e2e_events
+        cp.wait_stream(cs)                                   # fork
+        P = self.period
+
+        def load(t):
+            with torch.cuda.stream(cp):
+                if t - P >= 1:
+                    cp.wait_event(ev["done"][t - P])         # slot t % P free
+                p = t % P
                 self.q_in[p].copy_(self.host_q[p], non_blocking=True)
                 self.kv_in[p].copy_(self.host_kv[p], non_blocking=True)
+                ev["in"][t].record(cp)
+
+        load(1)
+        for t in range(1, T + 1):
+            if t + 1 <= T:
+                load(t + 1)
+            cs.wait_event(ev["in"][t])
+            if t - 2 >= 1:
+                cs.wait_event(ev["out"][t - 2])              # out buffer t % 2 drained
+            ob = self.out_buf[t % 2]
             for l in range(c.num_layers):
-                self._layer(l, t, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
-            if e2e:
-                self.host_out[t].copy_(self.out, non_blocking=True)
+                self._layer(l, t, advance=(l == c.watershed - 1 or l == c.num_layers - 1), out=ob)
+            ev["done"][t].record(cs)
+            with torch.cuda.stream(cp):
+                cp.wait_event(ev["done"][t])
+                self.host_out[t].copy_(ob, non_blocking=True)
+                ev["out"][t].record(cp)
+        cs.wait_stream(cp)                                   # join
 
     def _phase_wb(self):
         """Writeback of the new round's upper rows to pinned host memory
@@ -369,6 +407,8 @@ class RoundDecodeEngine:
                 self.host_qq.copy_(self.qq_in)
                 self.host_qkv = torch.empty(self.qkv_in.shape, dtype=self.qkv_in.dtype, pin_memory=True)
                 self.host_qkv.copy_(self.qkv_in)
+            self.e2e_stream = torch.cuda.Stream(self.dev)
+            self.e2e_events = {k: [torch.cuda.Event() for _ in range(c.decode_steps + 2)] for k in ("in", "done", "out")}
             self.host_out = torch.empty((c.decode_steps + 1,) + tuple(self.out.shape), dtype=torch.float32,
                                         pin_memory=True)
         with torch.cuda.stream(self.compute_stream):

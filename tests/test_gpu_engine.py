@@ -148,3 +148,33 @@ def test_engine_prefill_turn_matches_oracle(graphs):
         ref, _ = oatt.attention_forward_gqa(_f(eng.qq_in[L - 1, b]), K, V, qpos, kpos)
         got = _f(eng.qout[b]).reshape(nq, -1)
         assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-4
+
+
+def test_engine_e2e_pipeline_matches_device_path():
+    """End-to-end turn (inputs from pinned host memory, outputs back to it, the
+    copies pipelined on a side stream against the decode kernels) produces
+    exactly the device-resident turn's outputs for every token."""
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=16, hkv=4, head_dim=128, rounds=6, round_tokens=64, batch=2,
+                       decode_steps=9, policy=SelectionPolicy("top_percent", fraction=0.3), item_chunk=32,
+                       input_period=3, plant=1)
+    eng = RoundDecodeEngine(cfg, seed=11)
+    eng.prepare(e2e=True)
+    T = cfg.decode_steps
+    want = []
+    for _ in range(2):
+        eng.run_turn(e2e=False)
+        torch.cuda.synchronize()
+    # device path, token by token: replay the answer phase eagerly to collect every token's outputs
+    kept, _ = eng.run_turn(e2e=False)
+    torch.cuda.synchronize()
+    last_dev = eng.out.clone()
+    kept_e, _ = eng.run_turn(e2e=True)
+    eng.compute_stream.synchronize()
+    torch.cuda.synchronize()
+    assert [list(map(int, k)) for k in kept] == [list(map(int, k)) for k in kept_e]
+    assert torch.equal(eng.host_out[T], last_dev.cpu())
+    assert torch.equal(eng.host_out[T], eng.out_buf[T % 2].cpu())
+    want = eng.host_out[1:T + 1].clone()
+    eng.run_turn(e2e=True)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.host_out[1:T + 1], want)      # every token, turn after turn
