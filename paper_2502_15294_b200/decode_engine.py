@@ -307,10 +307,10 @@ class RoundDecodeEngine:
 
         End to end (e2e), every token's q/k/v come from pinned host memory and
         its attention outputs go back to it.  The copies run on the e2e copy
-        stream, pipelined against the decode kernels: token t+1's inputs load
-        while token t computes (input slots cycle with period P, a slot is
-        reloaded only after the token that last read it finished), and token
-        t's outputs (double buffer) drain while token t+1 computes."""
+        stream, pipelined against the decode kernels: inputs load P-2 tokens
+        ahead (input slots cycle with period P, a slot is reloaded only after
+        the token that last read it finished), and token t's outputs (double
+        buffer) drain while token t+1 computes."""
         c = self.cfg
         T = c.decode_steps
         if not e2e:
@@ -332,10 +332,12 @@ class RoundDecodeEngine:
                 self.kv_in[p].copy_(self.host_kv[p], non_blocking=True)
                 ev["in"][t].record(cp)
 
-        load(1)
+        ahead = max(1, P - 2)        # inputs prefetched this many tokens ahead (absorbs DMA queueing
+        for t in range(1, min(T, ahead) + 1):    # behind the other group's KV gather)
+            load(t)
         for t in range(1, T + 1):
-            if t + 1 <= T:
-                load(t + 1)
+            if t + ahead <= T:
+                load(t + ahead)
             cs.wait_event(ev["in"][t])
             if t - 2 >= 1:
                 cs.wait_event(ev["out"][t - 2])              # out buffer t % 2 drained
