@@ -274,7 +274,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_bulk_kernel(const __gr
 // contiguous.  Item mode uses n_items[b].  8 warps split the slots, lanes own
 // 4 consecutive dims, 4 slots' loads are issued together.
 // advance (nullable): advance[b] += 1 (lengths of the next step).
-__global__ void __launch_bounds__(128) decode_merge_kernel(const float* __restrict__ part_m,
+// NW warps per (dialogue, head): 4 when the grid is large (fits beside a
+// resident decode CTA); 16 for small batches, where only B*hq blocks exist and
+// each must fetch its ~150 partials in one round of loads, not ten.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) decode_merge_kernel(const float* __restrict__ part_m,
                                                            const float* __restrict__ part_l,
                                                            const float* __restrict__ part_acc,
                                                            const int32_t* __restrict__ seq_len, int append,
@@ -288,7 +292,6 @@ __global__ void __launch_bounds__(128) decode_merge_kernel(const float* __restri
   pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NW = 4;      // 128 threads: fits beside a resident decode CTA (registers)
   __shared__ int s_c0, s_c1, s_sparse;
   __shared__ int64_t s_W, s_P0, s_P1;
   __shared__ float s_red[NW];
@@ -461,16 +464,18 @@ int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const Bu
                 : bulk_by_hkv<float, 128>(hkv, G, grid, st, p, pdl, &e);
   if (r) return fail(RK_ERR_UNSUPPORTED, "bulk decode: hkv %d / group %d unsupported", hkv, G);
   if (e != cudaSuccess) return cuda_status(e, "decode_bulk_kernel launch");
+  const bool wide = p.B * p.hq <= sm_count();   // at most one (dialogue, head) block per SM: 16 warps each
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.B, p.hq);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(wide ? 512 : 128);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, decode_merge_kernel, (const float*)p.part_m, (const float*)p.part_l,
+  e = cudaLaunchKernelEx(&cfg, wide ? decode_merge_kernel<16> : decode_merge_kernel<4>, (const float*)p.part_m,
+                         (const float*)p.part_l,
                          (const float*)p.part_acc, p.seq_len, p.k_new ? 1 : 0,
                          p.items ? p.n_items : (const int32_t*)nullptr, p.B, p.nsplit, slices,
                          (int)(p.items ? p.items_stride : nsplit / slices), p.hq, d, out, advance);
