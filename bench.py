@@ -206,6 +206,8 @@ def main():
         return ms, clk.summary(), brk, h2d, kept
 
     ms, clocks, brk, h2d_bytes, kept0 = timed(False, args.steps)
+    # decode-kernel statistics of THIS (device-resident) timed run, before the e2e run overwrites them
+    dec_busy_ms, dec_bytes, dec_launches = eng.last_decode_busy_ms, eng.last_decode_bytes, eng.last_decode_launches
     tokens_per_turn = cfg.batch * eng.turn_tokens
     value = world * tokens_per_turn * args.steps / (ms / 1000.0)
     g0 = eng.groups[0]
@@ -228,7 +230,7 @@ def main():
     # every timed decode token / the union of the decode-loop intervals on the
     # device timeline (CUDA events on each group's compute stream)
     bytes_tok = eng.kv_bytes_per_token()
-    achieved = eng.last_decode_bytes / (eng.last_decode_busy_ms / 1000.0) / 1e9
+    achieved = dec_bytes / (dec_busy_ms / 1000.0) / 1e9
     step_bw = bytes_tok * eng.turn_tokens * args.steps / (ms / 1000.0) / 1e9
     resident, full = eng.gpu_kv_bytes()
     traffic = None      # DRAM bytes per token-step from the committed ncu capture of this kernel (same shapes)
@@ -262,7 +264,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "rk decode attention (decode_mma + merge): KV bytes of every timed decode token / "
                                                 "union of the groups' decode-loop intervals (CUDA events)",
-                     "decode_busy_ms": eng.last_decode_busy_ms, "launches": eng.last_decode_launches,
+                     "decode_busy_ms": dec_busy_ms, "launches": dec_launches,
                      "whole_step_GBps": step_bw, "whole_step_frac": step_bw / peak,
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},
         "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],

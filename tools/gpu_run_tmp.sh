@@ -1,2 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -x -q 2>&1 | tail -2
-for B in 4 8; do timeout 300 python bench.py --batch $B --groups 1 --steps 3 --warmup 3 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(json.dumps({'batch': $B, 'tok_s': d['value'], 'ms_step': d['ms_per_step'], 'frac': d['roofline']['frac'], 'whole': d['roofline']['whole_step_frac']}))"; done | tee gpurun_out/sweep_small.jsonl
+timeout 900 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; tail -2 gpurun_out/bench_c2.err; cat gpurun_out/bench_c2.json
