@@ -53,25 +53,31 @@ namespace pf {
 using namespace tc;
 
 constexpr int BM = 128, BN = 128, D = 128;   // rows, keys per tile, head dim
-constexpr int STAGES = 2;                // K ring and V ring depth
+constexpr int STAGES = 4;                // K ring and V ring depth
 constexpr int MR = 8;                    // tile-visibility metadata ring
 constexpr int NB = 3;                    // S/P buffers in TMEM (3 x 128 columns + O = 512)
 constexpr int LA = NB - 1;               // QK runs LA tiles ahead (its buffer is freed by the PV queued before)
 constexpr int QBOX = BM * 64 * 2;        // 128 rows x 64 bf16, swizzled: 16 KB
 constexpr int Q_BYTES = 4 * QBOX;        // q_hi, q_lo x two 64-dim halves
-constexpr int KBOX = BN * 64 * 2;        // 128 keys x 64 bf16: 16 KB
-constexpr int KV_STAGE = 2 * KBOX;       // one K or V tile (2 boxes): 32 KB
+// CTA pair (cta_group::2): an M tile is 256 stacked rows, CTA rank r owns rows
+// [128r, 128r+128) (its Q, S, P, O); the B operands are split by N: CTA r holds
+// keys [64r, 64r+64) of a K tile and head dims [64r, 64r+64) of a V tile.
+constexpr int PM = 2 * BM;               // rows per pair M tile
+constexpr int KBOX = (BN / 2) * 64 * 2;  // 64 keys x 64 bf16: 8 KB
+constexpr int K_STAGE = 2 * KBOX;        // this CTA's K half-tile (64 keys x 128 dims): 16 KB
+constexpr int VBOX = BN * 64 * 2;        // 128 keys x 64 dims: 16 KB
+constexpr int V_STAGE = VBOX;            // this CTA's V half-tile (128 keys x 64 dims): 16 KB
 constexpr int kSoftmaxWarps = 8, kMmaWarp = 8, kProducerWarp = 9, kVProducerWarp = 10;
 constexpr int THREADS = 352;
 constexpr int BAR_BYTES = 512;           // mbarriers, TMEM slot, per-stage tile maxima
 constexpr int XCH_BYTES = (2 * 256 + 3 * 128) * 4;  // row-max exchange (2 tiles x 2 halves) + item / unit sums
-constexpr size_t SMEM = 1024 + Q_BYTES + 2 * STAGES * KV_STAGE + BAR_BYTES + XCH_BYTES;
+constexpr size_t SMEM = 1024 + Q_BYTES + STAGES * (K_STAGE + V_STAGE) + BAR_BYTES + XCH_BYTES;
 constexpr uint32_t TMEM_COLS = 512;      // S/P buffers NB x 128 at 0.., O (128) at NB * 128 (= 384)
 constexpr float TAU = 8.f;               // lazy rescale threshold (log2 units)
 constexpr float FALLBACK = 100.f;        // item statistics recomputed when keys sit this far below m
 
-constexpr uint32_t kIdescQK = idesc_f16(BM, BN);             // S[128 x 128] = Q K^T (both K-major, smem)
-constexpr uint32_t kIdescPV = idesc_f16(BM, D, true);        // O[128 x 128] += P V (P from TMEM, V MN-major)
+constexpr uint32_t kIdescQK = idesc_f16(PM, BN);             // S[256 x 128] = Q K^T (both K-major, smem)
+constexpr uint32_t kIdescPV = idesc_f16(PM, D, true);        // O[256 x 128] += P V (P from TMEM, V MN-major)
 
 struct Params {
   int n_q, hq, hkv, G, mpad, mtiles;
@@ -169,10 +175,53 @@ __device__ unsigned long long g_pf_prof[4][16];
 #define PWAIT(bar, par, role, slot) bar_wait(bar, par)
 #endif
 
-__device__ __forceinline__ void tma_2d_s(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// TMA into this CTA's smem, completion bytes counted on the pair leader's
+// barrier (bar_cluster: shared::cluster address from mapa(.., 0))
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(sa(bar))
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of a shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sa(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void bar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+// pair MMAs (issued by the leader; A rows and B columns split across the pair)
+__device__ __forceinline__ void umma2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// completion of the leader's MMAs issued so far -> the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma2_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      ::"r"(sa(bar)), "h"((unsigned short)3)
       : "memory");
 }
 
@@ -234,24 +283,24 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 // SCORE_ONLY: the watershed scorer (rk_round_scores) — QK^T and the per-item
 // softmax statistics only: no V, no PV, no O, no row-max exchange.
 template <bool SCORE_ONLY>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                   const __grid_constant__ CUtensorMap vmap, const __grid_constant__ Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* qs = smem;                               // [hi d0-63 | hi d64-127 | lo d0-63 | lo d64-127]
-  uint8_t* ks = qs + Q_BYTES;                       // STAGES x [K d0-63 | K d64-127]
-  uint8_t* vs = ks + STAGES * KV_STAGE;             // STAGES x [V d0-63 | V d64-127]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vs + STAGES * KV_STAGE);
-  uint64_t* k_full = bars;                          // [STAGES] TMA -> MMA
-  uint64_t* k_empty = k_full + STAGES;              // [STAGES] QK done -> producer
-  uint64_t* v_full = k_empty + STAGES;              // [STAGES] TMA -> MMA
-  uint64_t* v_empty = v_full + STAGES;              // [STAGES] PV done -> producer
+  uint8_t* ks = qs + Q_BYTES;                       // STAGES x [K d0-63 | K d64-127] of this CTA's 64 keys
+  uint8_t* vs = ks + STAGES * K_STAGE;              // STAGES x [V, this CTA's 64 dims] of 128 keys
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vs + STAGES * V_STAGE);
+  uint64_t* k_full = bars;                          // [STAGES] both CTAs' TMA -> leader's MMA (leader's copy used)
+  uint64_t* k_empty = k_full + STAGES;              // [STAGES] QK done -> producers (multicast)
+  uint64_t* v_full = k_empty + STAGES;              // [STAGES] both CTAs' TMA -> leader's MMA
+  uint64_t* v_empty = v_full + STAGES;              // [STAGES] PV done -> producers (multicast)
   uint64_t* meta_full = v_empty + STAGES;           // [MR] producer -> softmax (tile_max)
   uint64_t* q_full = meta_full + MR;
   uint64_t* q_empty = q_full + 1;
   uint64_t* s_full = q_full + 2;                    // [NB] QK done -> softmax
-  uint64_t* p_full = s_full + NB;                   // [NB] P written (8 softmax warps) -> MMA
+  uint64_t* p_full = s_full + NB;                   // [NB] P written (8 + 8 softmax warps of the pair) -> leader
   uint64_t* buf_free = p_full + NB;                 // [NB] PV done: S/P buffer reusable, O stable
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(buf_free + NB);
   // per tile (ring of MR): the largest effective key position of the tile
@@ -263,8 +312,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
   float* xl_u = xl_it + 128;                        // [128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
-  const int u1 = (int)((int64_t)(blockIdx.x + 1) * p.n_units / gridDim.x);
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int u0 = (int)((int64_t)pair * p.n_units / npairs);
+  const int u1 = (int)((int64_t)(pair + 1) * p.n_units / npairs);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -278,18 +330,18 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
     bar_init(q_empty, 1);
     for (int b = 0; b < NB; ++b) {
       bar_init(&s_full[b], 1);
-      bar_init(&p_full[b], kSoftmaxWarps);
+      bar_init(&p_full[b], 2 * kSoftmaxWarps);
       bar_init(&buf_free[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)),
+  if (warp == kMmaWarp) {     // same warp in both CTAs: the pair's TMEM (same columns on both SMs)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)),
                  "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   fence_before();
-  __syncthreads();
+  cluster_sync();             // both CTAs' barriers initialised before any remote arrive
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_o = tmem + NB * BN;
@@ -305,6 +357,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
       asm volatile("prefetch.tensormap [%0];" ::"l"(&vmap) : "memory");
     }
     const uint32_t qs_a = sa(qs), ks_a = sa(ks);
+    const uint32_t q_full_l = mapa(q_full, 0);     // the leader's barriers count both CTAs' bytes
     TileIter ti, ta;                                // ta runs PF tiles ahead: key-position prefetch
     ti.init(p, u0, u1);
     ta.init(p, u0, u1);
@@ -336,12 +389,12 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
       if (ti.mtile != cur_mtile) {
         if (qn > 0) PWAIT(q_empty, (qn - 1) & 1, 2, 1);
         if (elect_one()) {
-          bar_expect(q_full, Q_BYTES);
-          const int row0 = kvh * 2 * p.mpad + mt * BM;
-          tma_2d_s(qs_a + 0 * QBOX, &qmap, 0, row0, q_full);
-          tma_2d_s(qs_a + 1 * QBOX, &qmap, 64, row0, q_full);
-          tma_2d_s(qs_a + 2 * QBOX, &qmap, 0, row0 + p.mpad, q_full);
-          tma_2d_s(qs_a + 3 * QBOX, &qmap, 64, row0 + p.mpad, q_full);
+          if (leader) bar_expect(q_full, 2 * Q_BYTES);
+          const int row0 = kvh * 2 * p.mpad + mt * PM + BM * (int)rank;   // this CTA's 128 rows
+          tma_2d_pair(qs_a + 0 * QBOX, &qmap, 0, row0, q_full_l);
+          tma_2d_pair(qs_a + 1 * QBOX, &qmap, 64, row0, q_full_l);
+          tma_2d_pair(qs_a + 2 * QBOX, &qmap, 0, row0 + p.mpad, q_full_l);
+          tma_2d_pair(qs_a + 3 * QBOX, &qmap, 64, row0 + p.mpad, q_full_l);
         }
         __syncwarp();
         cur_mtile = ti.mtile;
@@ -362,9 +415,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
       if (elect_one()) {
         tile_max[t % MR] = kmax;
         bar_arrive(&meta_full[t % MR]);               // release: tile_max visible with the phase
-        bar_expect(&k_full[s], KV_STAGE);
-        tma_2d_s(ks_a + s * KV_STAGE, &kmap, kvh * D, j0, &k_full[s]);
-        tma_2d_s(ks_a + s * KV_STAGE + KBOX, &kmap, kvh * D + 64, j0, &k_full[s]);
+        if (leader) bar_expect(&k_full[s], 2 * K_STAGE);
+        const uint32_t kb = mapa(&k_full[s], 0);
+        const int jr = j0 + (BN / 2) * (int)rank;      // this CTA's 64 keys of the tile
+        tma_2d_pair(ks_a + s * K_STAGE, &kmap, kvh * D, jr, kb);
+        tma_2d_pair(ks_a + s * K_STAGE + KBOX, &kmap, kvh * D + 64, jr, kb);
       }
       __syncwarp();
     }
@@ -378,90 +433,93 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
       for (int t = 0; ti.valid; ++t, ti.advance()) {
         const int kvh = ti.mtile / p.mtiles, s = t % STAGES;
         if (t >= STAGES) PWAIT(&v_empty[s], ((t / STAGES) - 1) & 1, 3, 0);
-        if (elect_one()) {
-          bar_expect(&v_full[s], KV_STAGE);
-          tma_2d_s(vs_a + s * KV_STAGE, &vmap, kvh * D, ti.j0, &v_full[s]);
-          tma_2d_s(vs_a + s * KV_STAGE + KBOX, &vmap, kvh * D + 64, ti.j0, &v_full[s]);
+        if (elect_one()) {                           // this CTA's 64 head dims of all 128 keys
+          if (leader) bar_expect(&v_full[s], 2 * V_STAGE);
+          tma_2d_pair(vs_a + s * V_STAGE, &vmap, kvh * D + 64 * (int)rank, ti.j0, mapa(&v_full[s], 0));
         }
         __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
-    // ================= MMA issuer.  The whole warp runs the (uniform) control
-    // flow and one elected lane issues, so descriptors live in uniform
-    // registers; each tile's descriptors are built once and advanced by
-    // compile-time offsets.  Order: QK of the LA tiles ahead, then per tile t:
-    // PV_t (after its P), QK_{t+LA} into the buffer PV_{t-1} frees — the
-    // issuer never waits on the PV it just issued, and the tensor pipe always
-    // holds queued work.  (LA = NB - 1: QK_{t+LA} reuses the buffer of PV_{t-1},
-    // which sits ahead of PV_t in the tensor queue and is normally done.)
-    TileIter qi, pi;
-    qi.init(p, u0, u1);
-    pi.init(p, u0, u1);
-    const uint32_t qs_a = sa(qs), ks_a = sa(ks), vs_a = sa(vs);
-    int tq = 0, tp = 0, cur_mtile = -1, qn = 0;
-    auto issue_qk = [&]() {
-      if (qi.mtile != cur_mtile) {
-        if (qn > 0 && elect_one()) umma_commit(q_empty);   // Q slot free once the QKs issued so far finish
+    if (leader) {
+      // ================= MMA issuer.  The whole warp runs the (uniform) control
+      // flow and one elected lane issues, so descriptors live in uniform
+      // registers; each tile's descriptors are built once and advanced by
+      // compile-time offsets.  Order: QK of the LA tiles ahead, then per tile t:
+      // PV_t (after its P), QK_{t+LA} into the buffer PV_{t-1} frees — the
+      // issuer never waits on the PV it just issued, and the tensor pipe always
+      // holds queued work.  (LA = NB - 1: QK_{t+LA} reuses the buffer of PV_{t-1},
+      // which sits ahead of PV_t in the tensor queue and is normally done.)
+      // Only the pair leader issues (cta_group::2 MMAs over both SMs' operands);
+      // every commit arrives on the barrier at the same offset in both CTAs.
+      TileIter qi, pi;
+      qi.init(p, u0, u1);
+      pi.init(p, u0, u1);
+      const uint32_t qs_a = sa(qs), ks_a = sa(ks), vs_a = sa(vs);
+      int tq = 0, tp = 0, cur_mtile = -1, qn = 0;
+      auto issue_qk = [&]() {
+        if (qi.mtile != cur_mtile) {
+          if (qn > 0 && elect_one()) umma2_commit(q_empty);   // Q slot free once the QKs issued so far finish
+          __syncwarp();
+          PWAIT(q_full, qn & 1, 1, 0);
+          cur_mtile = qi.mtile;
+          ++qn;
+        }
+        const int b = tq % NB, s = tq % STAGES;
+        if (tq >= NB) PWAIT(&buf_free[b], ((tq / NB) - 1) & 1, 1, 1);
+        PWAIT(&k_full[s], (tq / STAGES) & 1, 1, 2);
+        fence_after();
+        if (elect_one()) {
+          const uint32_t dS = tmem + b * BN;
+          const uint64_t a0 = desc_sw128(qs_a, 16);
+          const uint64_t b0 = desc_sw128(ks_a + s * K_STAGE, 16);     // this CTA's 64 keys (peer: same offset)
+  #pragma unroll
+          for (int hl = 0; hl < 2; ++hl)          // q_hi, q_lo
+  #pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              umma2(dS, a0 + (uint64_t)((((2 * hl + k / 4) * QBOX) + 32 * (k % 4)) >> 4),
+                   b0 + (uint64_t)((((k / 4) * KBOX) + 32 * (k % 4)) >> 4), kIdescQK, (hl | k) ? 1u : 0u);
+            }
+          umma2_commit(&k_empty[s]);                   // K slots free once this QK completes
+          umma2_commit(&s_full[b]);
+        }
         __syncwarp();
-        PWAIT(q_full, qn & 1, 1, 0);
-        cur_mtile = qi.mtile;
-        ++qn;
-      }
-      const int b = tq % NB, s = tq % STAGES;
-      if (tq >= NB) PWAIT(&buf_free[b], ((tq / NB) - 1) & 1, 1, 1);
-      PWAIT(&k_full[s], (tq / STAGES) & 1, 1, 2);
-      fence_after();
-      if (elect_one()) {
-        const uint32_t dS = tmem + b * BN;
-        const uint64_t a0 = desc_sw128(qs_a, 16);
-        const uint64_t b0 = desc_sw128(ks_a + s * KV_STAGE, 16);
-#pragma unroll
-        for (int hl = 0; hl < 2; ++hl)          // q_hi, q_lo
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            umma(dS, a0 + (uint64_t)((((2 * hl + k / 4) * QBOX) + 32 * (k % 4)) >> 4),
-                 b0 + (uint64_t)((((k / 4) * KBOX) + 32 * (k % 4)) >> 4), kIdescQK, (hl | k) ? 1u : 0u);
-          }
-        umma_commit(&k_empty[s]);                    // K slot free once this QK completes
-        umma_commit(&s_full[b]);
-      }
-      __syncwarp();
-      ++tq;
-      qi.advance();
-    };
-    for (int i = 0; i < LA && qi.valid; ++i) issue_qk();
-    while (pi.valid) {
-      const int b = tp % NB, s = tp % STAGES;
-      PWAIT(&p_full[b], (tp / NB) & 1, 1, 3);
-      if (SCORE_ONLY) {               // S_tp consumed: its buffer is free (nothing async to wait for)
-        if (elect_one()) bar_arrive(&buf_free[b]);
+        ++tq;
+        qi.advance();
+      };
+      for (int i = 0; i < LA && qi.valid; ++i) issue_qk();
+      while (pi.valid) {
+        const int b = tp % NB, s = tp % STAGES;
+        PWAIT(&p_full[b], (tp / NB) & 1, 1, 3);
+        if (SCORE_ONLY) {               // S_tp consumed: its buffer is free (nothing async to wait for)
+          if (elect_one()) bar_arrive(&buf_free[b]);
+          __syncwarp();
+          ++tp;
+          pi.advance();
+          if (qi.valid) issue_qk();
+          continue;
+        }
+        PWAIT(&v_full[s], (tp / STAGES) & 1, 1, 4);
+        fence_after();
+        if (elect_one()) {
+          const uint64_t b0 = desc_sw128(vs_a + s * V_STAGE, VBOX);    // V MN-major, one 64-dim atom per CTA
+          const uint32_t a0 = tmem + b * BN;                             // P_hi | P_lo (16 keys = 8 columns)
+          const bool first = pi.first;
+  #pragma unroll
+          for (int hl = 0; hl < 2; ++hl)          // P_hi, P_lo
+  #pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              umma2_ts(tmem_o, a0 + hl * (BN / 2) + kk * 8, b0 + (uint64_t)((kk * 16 * 128) >> 4), kIdescPV,
+                      (first && hl == 0 && kk == 0) ? 0u : 1u);
+            }
+          umma2_commit(&v_empty[s]);
+          umma2_commit(&buf_free[b]);
+        }
         __syncwarp();
         ++tp;
         pi.advance();
         if (qi.valid) issue_qk();
-        continue;
       }
-      PWAIT(&v_full[s], (tp / STAGES) & 1, 1, 4);
-      fence_after();
-      if (elect_one()) {
-        const uint64_t b0 = desc_sw128(vs_a + s * KV_STAGE, KBOX);   // V MN-major: d-halves LBO apart
-        const uint32_t a0 = tmem + b * BN;                             // P_hi | P_lo (16 keys = 8 columns)
-        const bool first = pi.first;
-#pragma unroll
-        for (int hl = 0; hl < 2; ++hl)          // P_hi, P_lo
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            umma_ts(tmem_o, a0 + hl * (BN / 2) + kk * 8, b0 + (uint64_t)((kk * 16 * 128) >> 4), kIdescPV,
-                    (first && hl == 0 && kk == 0) ? 0u : 1u);
-          }
-        umma_commit(&v_empty[s]);
-        umma_commit(&buf_free[b]);
-      }
-      __syncwarp();
-      ++tp;
-      pi.advance();
-      if (qi.valid) issue_qk();
     }
   } else {
     // ================= softmax / epilogue: warps 0-7.  TMEM lane quarter q4 =
@@ -478,7 +536,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
       unit_of(p, u, mtile, it0, it1);
       const int kvh = mtile / p.mtiles, mt = mtile - kvh * p.mtiles;
       const int c = unit_chunk(p, u);
-      const int R = mt * BM + r;
+      const int R = mt * PM + BM * (int)rank + r;   // stacked row of this CTA's half of the pair tile
       const bool real = R < p.G * p.n_q;
       const int g = real ? R / p.n_q : 0, qi = real ? R - g * p.n_q : 0;
       const int h = kvh * p.G + g;
@@ -512,7 +570,10 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           if (SCORE_ONLY) {                             // S is in registers: release the buffer now
             fence_before();
             __syncwarp();
-            if (lane == 0) bar_arrive(&p_full[b]);
+            if (lane == 0) {
+              if (leader) bar_arrive(&p_full[b]);
+              else bar_arrive_cluster(mapa(&p_full[b], 0));
+            }
           }
 
           if (!__all_sync(0xffffffffu, all_vis)) {     // diagonal / masked tile: per-key check
@@ -636,7 +697,10 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           fence_before();
           __syncwarp();
-          if (lane == 0) bar_arrive(&p_full[b]);
+          if (lane == 0) {                               // the leader issues this tile's PV
+            if (leader) bar_arrive(&p_full[b]);
+            else bar_arrive_cluster(mapa(&p_full[b], 0));
+          }
         }
         if (p.item_m) {                        // combine the halves' item statistics
           if (half == 1) {
@@ -695,10 +759,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
     atomicAdd(&g_pf_prof[role][15], (unsigned long long)(clock64() - prof_t0));
   }
 #endif
-  __syncthreads();
+  fence_before();
+  cluster_sync();             // the leader's last MMAs touched both SMs' TMEM; both CTAs are done
   if (warp == kMmaWarp) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -770,8 +835,8 @@ bool prefill_tc_supported(int kv_dtype, int d, int n_q, int G) {
 PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool stats, bool with_output) {
   PrefillPlan pl{};
   const int G = hq / hkv;
-  pl.mpad = (G * n_q + pf::BM - 1) / pf::BM * pf::BM;
-  pl.mtiles = pl.mpad / pf::BM;
+  pl.mpad = (G * n_q + pf::PM - 1) / pf::PM * pf::PM;      // pair M tiles of 256 stacked rows
+  pl.mtiles = pl.mpad / pf::PM;
   const int mt_total = hkv * pl.mtiles;
   if (n_items_in > 0) {
     pl.n_items = n_items_in;
@@ -781,7 +846,7 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
     pl.n_items = s > 0 ? (s + pl.item_keys - 1) / pl.item_keys : 1;
   }
   // ~8 units per SM: balance over the persistent CTAs, >= 1 item per chunk
-  const int target = 8 * sm_count();
+  const int target = 8 * (sm_count() / 2);                  // ~8 units per CTA pair
   int nc = (target + mt_total - 1) / mt_total;
   nc = std::max(1, std::min(nc, pl.n_items));
   pl.items_per_chunk = (pl.n_items + nc - 1) / nc;
@@ -844,7 +909,7 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
   CUtensorMap qmap, kmap, vmap;
   int r = tc::make_map(&qmap, qs, pf::D, (uint64_t)hkv * 2 * pl.mpad, pf::D * 2, pf::BM);
   if (r) return r;
-  r = tc::make_map(&kmap, k, (uint64_t)hkv * pf::D, (uint64_t)s, (uint64_t)hkv * pf::D * 2, pf::BN);
+  r = tc::make_map(&kmap, k, (uint64_t)hkv * pf::D, (uint64_t)s, (uint64_t)hkv * pf::D * 2, pf::BN / 2);
   if (r) return r;
   r = tc::make_map(&vmap, score_only ? k : v, (uint64_t)hkv * pf::D, (uint64_t)s, (uint64_t)hkv * pf::D * 2, pf::BN);
   if (r) return r;
@@ -863,7 +928,7 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
                                  (int)pf::SMEM), "prefill_tc smem attribute");
     configured = true;
   }
-  const int grid = std::min(sm_count(), pl.n_units);
+  const int grid = 2 * std::min(sm_count() / 2, pl.n_units);   // CTA pairs (__cluster_dims__(2,1,1))
   if (score_only) {
     pf::prefill_tc_kernel<true><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
     RK_CHECK_LAUNCH("prefill_tc_kernel<score>");
