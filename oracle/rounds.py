@@ -441,3 +441,59 @@ def footprint_report(batch, seq_len, hidden, num_layers, watershed, kept_rounds,
                + 4.0 * batch * (kept_rounds / total_rounds) * seq_len * hidden * (num_layers - watershed))
     return {"m_orig_bytes": m_orig, "m_round_bytes": m_round, "ratio": m_round / m_orig,
             "closed_form_ratio": ratio, "save_percent_at_k0": save_percent(num_layers, watershed)}
+
+
+# ---------------------------------------------------------------- calibration
+# stats.py:118-181 (KL curve, watershed detection) and the conversation token
+# layout of conversation.py:164-186 — restated for the calibration fixtures.
+
+KL_EPSILON = 1e-10          # stats.py:22
+
+
+def make_conversation_layout(q_lens, a_lens, rng):
+    """Token ids and (q_span, a_span) per round: SEP (256) before every later
+    question and before every answer (conversation.py:164-186); a_len 0 = the
+    in-flight question."""
+    ids, spans = [], []
+    for m, (ql, al) in enumerate(zip(q_lens, a_lens)):
+        qs = len(ids)
+        if m > 0:
+            ids.append(256)
+        ids.extend(int(x) for x in rng.integers(0, 256, size=ql))
+        qe = len(ids)
+        ae = qe
+        if al > 0:
+            ids.append(256)
+            ids.extend(int(x) for x in rng.integers(0, 256, size=al))
+            ae = len(ids)
+        spans.append(((qs, qe), (qe, ae)))
+    return ids, spans
+
+
+def kl_divergence(p, q, epsilon=KL_EPSILON):
+    """stats.py:118-128."""
+    p = np.asarray(p, dtype=np.float64)
+    q = np.asarray(q, dtype=np.float64)
+    if np.array_equal(p, q):
+        return 0.0
+    ps = (p + epsilon) / (p + epsilon).sum()
+    qs = (q + epsilon) / (q + epsilon).sum()
+    return float(np.sum(ps * np.log(ps / qs)))
+
+
+def kl_curve(per_layer_masses):
+    """stats.py:131-144: D(l) = mean KL from layer l to every later layer."""
+    d = [np.asarray(x, dtype=np.float64) for x in per_layer_masses]
+    L = len(d)
+    return np.array([np.mean([kl_divergence(d[l], d[lp]) for lp in range(l + 1, L)]) for l in range(L - 1)])
+
+
+def detect_watershed(curves, criterion="max_drop", tau=0.1):
+    """stats.py:157-181 over the corpus mean curve (stats.py:147-154)."""
+    d = np.stack(curves).mean(axis=0)
+    L = d.shape[0] + 1
+    cand = np.arange(1, L - 1)
+    if criterion == "max_drop":
+        return int(cand[np.argmax(d[cand - 1] - d[cand])])
+    below = cand[d[cand] <= tau]
+    return int(below[0]) if below.size else int(cand[np.argmin(d[cand])])

@@ -1,0 +1,51 @@
+"""GPU watershed calibration (calibration.py) against the
+reference's own calibration outputs (tests/golden/calib_cases.npz, generated
+by tools/make_golden.py from pipeline.capture_all_layers + layer_distributions
++ stats.kl_curve + detect_watershed, pipeline.py:439-494): the per-layer round
+distributions come from one device prefill with fused scoring (no capture
+matrices) and must match the reference's, and the detected layers must be
+identical."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2502_15294_b200 import calibration as cal  # noqa: E402
+from paper_2502_15294_b200.engine import Model, ModelConfig  # noqa: E402
+from paper_2502_15294_b200.stats import Round  # noqa: E402
+
+
+def _corpus(z):
+    convs = []
+    for i in range(int(z["n_conv"])):
+        spans = z[f"c{i}_spans"]
+        rounds = [Round(m, (int(s[0][0]), int(s[0][1])), (int(s[1][0]), int(s[1][1]))) for m, s in enumerate(spans)]
+        convs.append(cal.Conversation(rounds=rounds, token_ids=[int(t) for t in z[f"c{i}_ids"]]))
+    return convs
+
+
+def test_calibration_matches_reference():
+    z = np.load(GOLDEN / "calib_cases.npz")
+    model = Model(ModelConfig(num_layers=int(z["num_layers"]), num_heads=int(z["num_heads"]),
+                              d_model=int(z["d_model"]), rng_seed=int(z["seed"])))
+    convs = _corpus(z)
+    curves = []
+    for i, conv in enumerate(convs):
+        n = cal.analysis_round_index(conv)
+        assert n == int(z[f"c{i}_n"])
+        masses = cal.layer_round_masses(model, conv, n)
+        np.testing.assert_allclose(masses, z[f"c{i}_masses"], rtol=1e-4, atol=1e-7)
+        curve = cal.kl_curve(masses)
+        np.testing.assert_allclose(curve.values, z[f"c{i}_curve"], rtol=1e-3, atol=1e-7)
+        curves.append(curve)
+    assert cal.detect_watershed(curves).layer == int(z["ws_max_drop_0.1"])
+    res = cal.calibrate_watershed(model, convs, criterion="threshold", tau=1e-3)
+    assert res.layer == int(z["ws_threshold_0.001"]) and res.corpus_size == len(convs)

@@ -170,3 +170,33 @@ def test_c1_pipeline_oracle_matches_reference():
         led = z[f"t{t}_ledger"]
         assert rec.h2d_bytes == led[1] + led[3]
         assert rec.d2h_bytes == led[5]
+
+
+# ----------------------------------------------------------------- calibration (stats.py:118-181)
+def _calib():
+    return np.load(GOLDEN / "calib_cases.npz")
+
+
+def test_oracle_kl_curve_and_watershed_match_reference():
+    z = _calib()
+    curves = []
+    for i in range(int(z["n_conv"])):
+        c = orr.kl_curve(z[f"c{i}_masses"])
+        np.testing.assert_allclose(c, z[f"c{i}_curve"], rtol=1e-12, atol=1e-15)
+        curves.append(c)
+    assert orr.detect_watershed(curves, "max_drop") == int(z["ws_max_drop_0.1"])
+    assert orr.detect_watershed(curves, "threshold", 0.1) == int(z["ws_threshold_0.1"])
+    assert orr.detect_watershed(curves, "threshold", 1e-3) == int(z["ws_threshold_0.001"])
+
+
+def test_package_calibration_host_math_matches_reference():
+    from paper_2502_15294_b200 import calibration as cal
+    z = _calib()
+    curves = [cal.kl_curve(z[f"c{i}_masses"]) for i in range(int(z["n_conv"]))]
+    for i, c in enumerate(curves):
+        np.testing.assert_allclose(c.values, z[f"c{i}_curve"], rtol=1e-12, atol=1e-15)
+    assert cal.detect_watershed(curves).layer == int(z["ws_max_drop_0.1"])
+    assert cal.detect_watershed(curves, "threshold", 1e-3).layer == int(z["ws_threshold_0.001"])
+    assert cal.kl_divergence([0.5, 0.5], [0.5, 0.5]) == 0.0
+    with pytest.raises(cal.DomainError):
+        cal.detect_watershed(curves, "nope")

@@ -299,6 +299,46 @@ def pipeline_c1(ref, rng_unused, turns=9, steps=63):
     np.savez_compressed(GOLDEN / "c1_pipeline.npz", **out)
 
 
+def calibration_cases(ref, rng, n_conv=4):
+    """Watershed calibration (pipeline.py:439-494, stats.py:118-181) on a
+    6-layer model over synthetic conversations: per-conversation layer
+    distributions and KL curves, and the corpus watershed for both criteria."""
+    sys.path.insert(0, str(REPO))
+    from oracle.rounds import make_conversation_layout
+    from roundkv_ref.conversation import Conversation, Round, Token
+    from roundkv_ref.engine import Model, ModelConfig
+    from roundkv_ref.pipeline import analysis_round_index, capture_all_layers, layer_distributions
+    from roundkv_ref.stats import detect_watershed, kl_curve
+    model = Model(ModelConfig(num_layers=6, num_heads=4, d_model=128, rng_seed=7))
+    out = {"n_conv": np.array(n_conv), "num_layers": np.array(6), "num_heads": np.array(4),
+           "d_model": np.array(128), "seed": np.array(7)}
+    curves = []
+    for i in range(n_conv):
+        n_rounds = int(rng.integers(3, 7))
+        q_lens = [int(x) for x in rng.integers(8, 40, size=n_rounds)]
+        a_lens = [int(x) for x in rng.integers(10, 60, size=n_rounds)]
+        if i % 2:                                  # odd conversations end with an in-flight question
+            a_lens[-1] = 0
+        ids, spans = make_conversation_layout(q_lens, a_lens, rng)
+        conv = Conversation(rounds=[Round(m, tuple(q), tuple(a)) for m, (q, a) in enumerate(spans)],
+                            tokens=[Token(t, p) for p, t in enumerate(ids)])
+        n = analysis_round_index(conv)
+        caps = capture_all_layers(model, conv)
+        dists = layer_distributions([caps[l] for l in range(6)], conv.rounds, n)
+        curve = kl_curve([d.masses for d in dists])
+        curves.append(curve)
+        out[f"c{i}_ids"] = np.array(ids, dtype=np.int64)
+        out[f"c{i}_spans"] = np.array(spans, dtype=np.int64)
+        out[f"c{i}_n"] = np.array(n)
+        out[f"c{i}_masses"] = np.stack([d.masses for d in dists])
+        out[f"c{i}_curve"] = curve.values
+    for crit, tau in (("max_drop", 0.1), ("threshold", 0.1), ("threshold", 1e-3)):
+        w = detect_watershed(curves, criterion=crit, tau=tau)
+        out[f"ws_{crit}_{tau}"] = np.array(w.layer)
+        out["mean_curve"] = w.curve.values
+    np.savez_compressed(GOLDEN / "calib_cases.npz", **out)
+
+
 def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
     ref = load_reference()
@@ -308,6 +348,7 @@ def main():
     select_cases(ref, rng)
     store_memory_cases(ref, rng)
     pipeline_c1(ref, rng)
+    calibration_cases(ref, np.random.default_rng(777))
     for p in sorted(GOLDEN.iterdir()):
         print(f"{p.name:28s} {p.stat().st_size:>10d} B")
 
