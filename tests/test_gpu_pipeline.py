@@ -122,3 +122,26 @@ def test_fetch_upper_moves_bytes():
     assert blocks[0].payload.is_cuda
     torch.testing.assert_close(blocks[0].payload.cpu(), up)
     assert s.ledger.per_turn[-1].h2d_events == 1
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("drop2", dict(policy=SelectionPolicy("top_percent", fraction=0.25), drop_window=2, drop_protect=1)),
+    ("fixed", dict(policy=SelectionPolicy("fixed", v=0.12))),
+    ("adaptive", dict(policy=SelectionPolicy("adaptive", kappa=0.5))),
+])
+def test_c1_policy_and_drop_variants_match_reference(name, kw):
+    """Inactivity drop policy (ActivityLedger.update_and_drop + store.drop_upper,
+    selection.py:168-204, store.py:280-285) and the fixed / adaptive strategies
+    through whole turns: kept rounds, dropped set, answers and transfer ledger
+    equal the reference's (tests/golden/c1_variants.npz)."""
+    z = np.load(GOLDEN / "c1_variants.npz")
+    model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42))
+    pipe = RoundPipeline(model, 2, **kw)
+    for t in range(6):
+        res = pipe.run_turn(list(z[f"{name}_t{t}_q"]), max_decode_steps=15)
+        m = res.metrics
+        assert m.kept == tuple(z[f"{name}_t{t}_kept"]), (name, t)
+        assert sorted(pipe.activity.dropped) == list(z[f"{name}_t{t}_dropped"]), (name, t)
+        assert list(res.answer_ids) == list(z[f"{name}_t{t}_answer"]), (name, t)
+        assert [m.upper_h2d_events, m.upper_h2d_bytes, m.d2h_events, m.d2h_bytes, m.device_used_peak,
+                m.hist_tokens_attended] == z[f"{name}_t{t}_ledger"].tolist(), (name, t)

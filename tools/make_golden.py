@@ -339,6 +339,36 @@ def calibration_cases(ref, rng, n_conv=4):
     np.savez_compressed(GOLDEN / "calib_cases.npz", **out)
 
 
+def pipeline_variants(ref):
+    """C1-shaped pipeline runs with the inactivity drop policy active
+    (drop_window=2, selection.py:168-204 + store.drop_upper) and with the
+    fixed / adaptive strategies (selection.py:76-108): 6 turns, 15 decode steps."""
+    from roundkv_ref.engine import Model, ModelConfig
+    from roundkv_ref.pipeline import RoundPipeline
+    from roundkv_ref.selection import SelectionPolicy
+    model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42))
+    variants = {
+        "drop2": dict(policy=SelectionPolicy("top_percent", fraction=0.25), drop_window=2, drop_protect=1),
+        "fixed": dict(policy=SelectionPolicy("fixed", v=0.12)),
+        "adaptive": dict(policy=SelectionPolicy("adaptive", kappa=0.5)),
+    }
+    out = {}
+    for name, kw in variants.items():
+        pipe = RoundPipeline(model, 2, **kw)
+        qrng = np.random.default_rng(5)
+        for t in range(6):
+            q = [int(x) for x in qrng.integers(0, 256, size=31)]
+            res = pipe.run_turn(q, max_decode_steps=15)
+            m = res.metrics
+            out[f"{name}_t{t}_q"] = np.array(q, dtype=np.int64)
+            out[f"{name}_t{t}_answer"] = np.array(res.answer_ids, dtype=np.int64)
+            out[f"{name}_t{t}_kept"] = np.array(m.kept, dtype=np.int64)
+            out[f"{name}_t{t}_dropped"] = np.array(sorted(pipe.activity.dropped), dtype=np.int64)
+            out[f"{name}_t{t}_ledger"] = np.array([m.upper_h2d_events, m.upper_h2d_bytes, m.d2h_events, m.d2h_bytes,
+                                                   m.device_used_peak, m.hist_tokens_attended], dtype=np.int64)
+    np.savez_compressed(GOLDEN / "c1_variants.npz", **out)
+
+
 def main():
     GOLDEN.mkdir(parents=True, exist_ok=True)
     ref = load_reference()
@@ -349,6 +379,7 @@ def main():
     store_memory_cases(ref, rng)
     pipeline_c1(ref, rng)
     calibration_cases(ref, np.random.default_rng(777))
+    pipeline_variants(ref)
     for p in sorted(GOLDEN.iterdir()):
         print(f"{p.name:28s} {p.stat().st_size:>10d} B")
 
