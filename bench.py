@@ -60,6 +60,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--question-noise", type=float, default=None,
+                    help="per-turn question variation (EngineConfig.question_noise)")
+    ap.add_argument("--no-round-cache", action="store_true",
+                    help="fetch every kept round every turn (the reference's transfer pattern)")
     ap.add_argument("--groups", type=int, default=None,
                     help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
@@ -184,6 +188,10 @@ def main():
         w["batch"] = args.batch
     if args.decode_steps:
         w["decode_steps"] = args.decode_steps
+    if args.no_round_cache:
+        w["round_cache"] = False
+    if args.question_noise is not None:
+        w["question_noise"] = args.question_noise
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
@@ -216,7 +224,8 @@ def main():
     if not args.no_e2e:
         ms_e, _, brk_e, h2d_e, _ = timed(True, args.steps)
         step_in = sum(e.turn_tokens * (e.q_in[0].numel() * 4 + e.kv_in[0].numel() * 2)
-                      + (e.qq_in.numel() * 4 + e.qkv_in.numel() * 2 if e.nq > 1 else 0) for e in eng.groups)
+                      + (e.qq_in.numel() * 4 + e.qkv_in.numel() * 2 + e.q_var[0].numel() * 4 if e.nq > 1 else 0)
+                      for e in eng.groups)
         step_out = sum(e.cfg.decode_steps * e.out.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
                        for e in eng.groups)
         e2e = {"value": world * tokens_per_turn * args.steps / (ms_e / 1000.0), "unit": "tokens/s",
@@ -268,6 +277,9 @@ def main():
                      "whole_step_GBps": step_bw, "whole_step_frac": step_bw / peak,
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},
         "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],
+                "round_cache": {"enabled": cfg.round_cache, "question_variants": cfg.question_variants,
+                                "rounds_fetched_group0_last_turn": g0.last_copied_rounds,
+                                "rounds_kept_group0": g0.cfg.batch * g0.K},
                 "GBps": g0.last_h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None,
                 "link": "PCIe Gen5 x16 (~63 GB/s/dir theoretical)"},
         "gpu_kv_saved": {"resident_bytes": resident, "full_cache_bytes": full, "saved_frac": 1 - resident / full},

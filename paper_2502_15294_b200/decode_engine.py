@@ -60,6 +60,9 @@ class EngineConfig:
     plant: int = 2                # rounds per dialogue with planted relevance at L_w-1 (0 = none)
     plant_beta: float = 0.25
     question_rows: int = 1        # n_q: 1 = single-token question (decode kernel); > 1 = tensor-core prefill
+    round_cache: bool = True      # keep rounds kept again in their working-cache slots (no re-fetch)
+    question_variants: int = 4    # distinct questions cycled over turns (noisy copies of question 0)
+    question_noise: float = 1.0   # variants about as far from question 0 as it is long
 
     @property
     def group(self) -> int:
@@ -153,6 +156,21 @@ class RoundDecodeEngine:
             self.upper_len_q = torch.full((B,), self.K * T + nq, dtype=torch.int32, device=self.dev)
         if c.plant:
             self._plant(gd)
+        # per-turn question variants (layer inputs of the question at L_w-1 and above vary, so
+        # consecutive turns keep overlapping but different round sets)
+        V = max(1, c.question_variants)
+        self.turn = 0
+        if self.nq > 1:
+            base = self.qq_in[c.watershed - 1]
+            self.q_var = torch.stack([base + (c.question_noise * torch.randn(base.shape, generator=gd, device=self.dev)
+                                              if v else 0.0) for v in range(V)])
+        else:
+            base = self.q_in[0]
+            self.q_var = torch.stack([base + (c.question_noise * torch.randn(base.shape, generator=gd, device=self.dev)
+                                              if v else 0.0) for v in range(V)])
+        # working-cache slot -> round id per dialogue (-1 = empty); see assign_slots
+        self.slot_round = np.full((B, self.K), -1, dtype=np.int64)
+        self.last_copied_rounds = 0
 
         # ---- scratch
         self.raw = torch.empty((B, R), dtype=torch.float64, device=self.dev)
@@ -260,9 +278,9 @@ class RoundDecodeEngine:
         values, so the splice equals the masked attention (engine.py:94-112)."""
         c = self.cfg
         nq, T, KT = self.nq, c.round_tokens, self.K * c.round_tokens
-        for b in range(c.batch):       # key positions of the spliced cache: kept rounds ascending, question
+        for b in range(c.batch):       # key positions of the working cache: its round slots, then the question
             pos = self.k_pos_up_host[b]
-            for i, r in enumerate(kept[b]):
+            for i, r in enumerate(self.slot_round[b]):
                 pos[i * T:(i + 1) * T] = torch.arange(int(r) * T, (int(r) + 1) * T)
             pos[KT:KT + nq] = torch.arange(self.hist, self.hist + nq)
         self.k_pos_up.copy_(self.k_pos_up_host, non_blocking=True)
@@ -357,24 +375,49 @@ class RoundDecodeEngine:
         self.writeback.copy_(self.upper[:, :, :, self.K * self.cfg.round_tokens:], non_blocking=True)
 
     # ------------------------------------------------------------------ gather
+    def assign_slots(self, kept):
+        """Cross-turn round cache: the working cache's K
+        round slots keep the rounds that stay kept; only newly kept rounds are
+        fetched, into the slots of the rounds that left.  Decode attention is
+        invariant to the order of the cached keys (every cached key is visible
+        to a decode token), so the splice need not be ascending; the question
+        prefill reads the slots' original positions (k_pos_up).  Without the
+        cache every kept round is fetched, ascending (pipeline._assemble).
+        Returns [(dialogue, slot, round)] copies."""
+        copies = []
+        for b in range(self.cfg.batch):
+            new = [int(r) for r in kept[b]]
+            cur = self.slot_round[b]
+            if not self.cfg.round_cache:
+                cur[:] = -1
+            stay = set(new) & set(int(x) for x in cur if x >= 0)
+            for i in range(self.K):
+                if cur[i] not in stay:
+                    cur[i] = -1
+            free = [i for i in range(self.K) if cur[i] < 0]
+            for i, r in zip(free, [r for r in new if r not in stay]):
+                cur[i] = r
+                copies.append((b, i, r))
+        self.last_copied_rounds = len(copies)
+        return copies
+
     def gather_plan(self, kept: np.ndarray):
         """Per upper layer: (src, spitch, dst, dpitch, width, height) arrays, one
-        2-row (K, V) strided copy per (dialogue, kept round)."""
+        2-row (K, V) strided copy per (dialogue, newly kept round)."""
         c = self.cfg
         es = 2
         T = c.round_tokens
         width = T * self.row * es
         spitch = width
         dpitch = self.s_up * self.row * es
+        copies = self.assign_slots(kept)
         plans = []
         for u in range(self.L_up):
             srcs, dsts = [], []
-            for b in range(c.batch):
-                hs = b % self.host_sets
-                for i, r in enumerate(kept[b]):
-                    blk = self.host_blocks[hs][int(r)]
-                    srcs.append(blk.data_ptr() + u * 2 * T * self.row * es)
-                    dsts.append(self.upper[b, u, 0, i * T].data_ptr())
+            for b, i, r in copies:
+                blk = self.host_blocks[b % self.host_sets][r]
+                srcs.append(blk.data_ptr() + u * 2 * T * self.row * es)
+                dsts.append(self.upper[b, u, 0, i * T].data_ptr())
             n = len(srcs)
             plans.append(dict(n=n, src=_ptr_array(srcs), dst=_ptr_array(dsts),
                               spitch=np.full(n, spitch, np.uint64), dpitch=np.full(n, dpitch, np.uint64),
@@ -409,6 +452,8 @@ class RoundDecodeEngine:
                 self.host_qq.copy_(self.qq_in)
                 self.host_qkv = torch.empty(self.qkv_in.shape, dtype=self.qkv_in.dtype, pin_memory=True)
                 self.host_qkv.copy_(self.qkv_in)
+            self.host_q_var = torch.empty(self.q_var.shape, dtype=self.q_var.dtype, pin_memory=True)
+            self.host_q_var.copy_(self.q_var)
             self.e2e_stream = torch.cuda.Stream(self.dev)
             self.e2e_events = {k: [torch.cuda.Event() for _ in range(c.decode_steps + 2)] for k in ("in", "done", "out")}
             self.host_out = torch.empty((c.decode_steps + 1,) + tuple(self.out.shape), dtype=torch.float32,
@@ -441,8 +486,17 @@ class RoundDecodeEngine:
             kept.append(self.kept_host[b, :n].numpy().copy())
         return kept
 
+    def _set_question(self, e2e: bool = False):
+        """This turn's question (variant turn % V) into the question inputs."""
+        v = self.turn % self.q_var.shape[0]
+        dst = self.qq_in[self.cfg.watershed - 1] if self.nq > 1 else self.q_in[0]
+        src = self.host_q_var[v] if e2e else self.q_var[v]
+        dst.copy_(src, non_blocking=True)
+        self.turn += 1
+
     def run_turn_eager(self):
         """Whole turn without graphs (first call / debugging)."""
+        self._set_question()
         self._phase_a()
         kept = self._select_to_host()
         self.copy_stream.wait_stream(torch.cuda.current_stream())
@@ -472,8 +526,8 @@ class RoundDecodeEngine:
                     self.qq_in.copy_(self.host_qq, non_blocking=True)
                     self.qkv_in.copy_(self.host_qkv, non_blocking=True)
                 else:
-                    self.q_in[0].copy_(self.host_q[0], non_blocking=True)
                     self.kv_in[0].copy_(self.host_kv[0], non_blocking=True)
+            self._set_question(e2e)
             self.graph_a.replay()
             m[1].record()
             kept = self._select_to_host()

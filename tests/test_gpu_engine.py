@@ -156,7 +156,7 @@ def test_engine_e2e_pipeline_matches_device_path():
     exactly the device-resident turn's outputs for every token."""
     cfg = EngineConfig(num_layers=4, watershed=2, hq=16, hkv=4, head_dim=128, rounds=6, round_tokens=64, batch=2,
                        decode_steps=9, policy=SelectionPolicy("top_percent", fraction=0.3), item_chunk=32,
-                       input_period=3, plant=1)
+                       input_period=3, plant=1, question_variants=1)     # identical turns
     eng = RoundDecodeEngine(cfg, seed=11)
     eng.prepare(e2e=True)
     T = cfg.decode_steps
@@ -178,3 +178,37 @@ def test_engine_e2e_pipeline_matches_device_path():
     eng.run_turn(e2e=True)
     torch.cuda.synchronize()
     assert torch.equal(eng.host_out[1:T + 1], want)      # every token, turn after turn
+
+
+def test_engine_round_cache_reuses_slots():
+    """Cross-turn round cache: a round kept again stays in its working-cache
+    slot (no H2D); with the same question every turn nothing is re-fetched and
+    the outputs are bit-identical to the first turn's; with varying questions
+    only the newly kept rounds are fetched and outputs still match the oracle
+    (checked by test_engine_turn_matches_oracle)."""
+    base = dict(num_layers=4, watershed=2, hq=16, hkv=4, head_dim=128, rounds=8, round_tokens=64, batch=2,
+                decode_steps=3, policy=SelectionPolicy("top_percent", fraction=0.3), item_chunk=32, plant=2)
+    eng = RoundDecodeEngine(EngineConfig(**base, question_variants=1), seed=21)
+    eng.prepare()                              # (its warm-up turn already fills the slots)
+    eng.slot_round[:] = -1                     # cold cache
+    _, b0 = eng.run_turn()
+    torch.cuda.synchronize()
+    out0 = eng.out.clone()
+    assert eng.last_copied_rounds == 2 * eng.K and b0 > 0
+    kept, b1 = eng.run_turn()
+    torch.cuda.synchronize()
+    assert eng.last_copied_rounds == 0 and b1 == 0
+    assert torch.equal(eng.out, out0)
+    # varying questions: only rounds not already resident are fetched
+    eng2 = RoundDecodeEngine(EngineConfig(**base, question_variants=3, question_noise=1.0), seed=21)
+    eng2.prepare()
+    prev = None
+    for _ in range(4):
+        kept, _ = eng2.run_turn()
+        torch.cuda.synchronize()
+        now = [set(int(x) for x in k) for k in kept]
+        if prev is not None:
+            assert eng2.last_copied_rounds == sum(len(n - p) for n, p in zip(now, prev))
+        for b in range(2):
+            assert set(int(x) for x in eng2.slot_round[b]) == now[b]
+        prev = now

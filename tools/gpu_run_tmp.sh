@@ -1,4 +1,5 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python tools/bench_prefill.py --json gpurun_out/prefill_c3.json 2>&1 | cut -c1-250
-timeout 900 python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; tail -1 gpurun_out/bench_c3.err; python -c "import json; d=json.load(open('gpurun_out/bench_c3.json')); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['prefill'])"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_tc_kernel -s 2 -c 1 -o gpurun_out/prefill_tc python tools/bench_prefill.py --nq 512 --reps 1 > gpurun_out/prefill_ncu.log 2>&1; tail -1 gpurun_out/prefill_ncu.log
+for a in "--question-noise 0.3" "--question-noise 1.0" "--question-noise 1.0 --no-round-cache"; do
+timeout 600 python bench.py --no-cpu $a 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); h=d['h2d']
+print(json.dumps({'args': '$a', 'value': round(d['value']), 'e2e': round(d['e2e']['value']), 'frac': round(d['roofline']['frac'],3), 'whole': round(d['roofline']['whole_step_frac'],3), 'h2d_GB_turn': round(h['bytes_per_turn_all_groups']/1e9,2), 'fetched': h['round_cache']['rounds_fetched_group0_last_turn'], 'kept': h['round_cache']['rounds_kept_group0']}))"
+done | tee gpurun_out/round_cache_sweep.jsonl
