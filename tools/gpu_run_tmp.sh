@@ -1,8 +1,4 @@
-timeout 300 python -m pytest tests/test_gpu_prefill.py tests/test_gpu_kernels.py -x -q -k "prefill or round_scores" 2>&1 | tail -2
-for v in poly0 poly1 base poly3 poly4; do
-  if [ $v = base ]; then lib=paper_2502_15294_b200/librk.so; else lib=variants_tmp/librk_$v.so; fi
-  echo "== $v"; ROUNDKV_B200_LIB=$PWD/$lib timeout 120 python tools/bench_prefill.py --nq 512,1024 --reps 10 2>&1 | python -c "
-import sys,json
-for l in sys.stdin:
-    if l.startswith('{'): d=json.loads(l); print(d['n_q'], round(d['ms_prefill'],4), round(d['ms_prefill_fused_scoring'],4), round(d['ms_separate_scorer'],4), round(d['algo_tflops']))"
-done
+timeout 1200 python bench.py --workload c4 --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; tail -1 gpurun_out/bench_c4.err
+timeout 900 python bench.py --workload c3 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; tail -1 gpurun_out/bench_c3.err
+for f in c4 c3; do python -c "
+import json; d=json.load(open('gpurun_out/bench_$f.json')); print('$f', round(d['value']), round(d['roofline']['frac'],3), round(d['roofline']['whole_step_frac'],3), round(d['e2e']['value']), d['gpu_kv_saved']['saved_frac'], d['h2d']['GBps'], d.get('prefill',{}).get('lower_layers_tflops_group0'))"; done
