@@ -16,6 +16,8 @@
 // start prefetching K/V tiles while the previous merge is still running, and
 // wait (griddepcontrol.wait) only before touching q / the workspace.
 #include <cmath>
+#include <cstdlib>
+#include <algorithm>
 #include <type_traits>
 
 #include "decode_common.cuh"
@@ -444,8 +446,13 @@ bool bulk_supported(int kv_dtype, int d, int hkv, int G) {
 // partial slots of the uniform mode: one persistent CTA per SM (capped so each
 // CTA streams >= 32 keys), times the warps-per-head slices
 int bulk_splits(int batch, int max_seq_len, int hkv) {
+  static int min_keys = -1;        // keys per CTA floor; RK_DECODE_MIN_KEYS overrides (experiments)
+  if (min_keys < 0) {
+    const char* e = std::getenv("RK_DECODE_MIN_KEYS");
+    min_keys = e ? std::max(1, std::atoi(e)) : 32;
+  }
   int64_t total = (int64_t)batch * max_seq_len;
-  int64_t ctas = total / 32;
+  int64_t ctas = total / min_keys;
   int n = (int)(ctas < sm_count() ? (ctas < 1 ? 1 : ctas) : sm_count());
   return n * (8 / hkv);
 }
