@@ -193,13 +193,17 @@ int rk_d2h_scatter(int n, const void* const* src, const size_t* src_pitch,
  *    NULL (uniform split).  bad_row: INT32_MAX or the first row with no
  *    visible key (-> InvariantError).
  * ---------------------------------------------------------------------- */
+/* flags: RK_PREFILL_SINGLE_PASS = the bf16 path (q and softmax P rounded to
+ * bf16, one MMA pass each; outputs ~1e-2 relative instead of ~1e-6; not with
+ * raw_out).  0 = the default two-pass fp32-class path. */
+#define RK_PREFILL_SINGLE_PASS 1
 size_t rk_prefill_workspace_bytes(int n_q, int hq, int hkv, int s, int d, int n_items, int n_bins);
 int rk_prefill_attention(const float* q, int n_q, int hq, int d,
                          const void* k, const void* v, int kv_dtype, int s, int hkv,
                          const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed,
                          const int32_t* items, int n_items, int n_bins, const uint8_t* active,
                          float* out, double* raw_out, int32_t* bad_row,
-                         void* workspace, size_t workspace_bytes, rk_stream_t stream);
+                         void* workspace, size_t workspace_bytes, int flags, rk_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -46,7 +46,7 @@ _SIGS = {
     "rk_d2h_scatter": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "rk_prefill_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
     "rk_prefill_attention": (_i, [_p, _i, _i, _i, _p, _p, _i, _i, _i, _p, _p, _p, _p, _i, _i, _p, _p, _p, _p, _p,
-                                  _sz, _p]),
+                                  _sz, _i, _p]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -57,6 +57,7 @@ for _name, (_res, _args) in _SIGS.items():
 ABI_VERSION = lib.rk_abi_version()
 
 RK_F32, RK_BF16 = 0, 1
+RK_PREFILL_SINGLE_PASS = 1
 SEL_KINDS = {"fixed": 0, "top_percent": 1, "adaptive": 2, "all": 3}
 
 

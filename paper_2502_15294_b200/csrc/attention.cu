@@ -474,7 +474,7 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d, const void* k, 
                          int s, int hkv, const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed,
                          const int32_t* items, int n_items, int n_bins, const uint8_t* active, float* out,
                          double* raw_out, int32_t* bad_row, void* workspace, size_t workspace_bytes,
-                         rk_stream_t stream) {
+                         int flags, rk_stream_t stream) {
   Shape sh;
   int st = check_heads(hq, hkv, d, &sh);
   if (st) return st;
@@ -484,6 +484,9 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d, const void* k, 
   const bool stats = raw_out != nullptr;
   if (stats && (items == nullptr || n_items <= 0 || n_bins <= 0))
     return fail(RK_ERR_DOMAIN, "round scoring needs the round-aligned item table and n_bins");
+  const bool single_pass = (flags & RK_PREFILL_SINGLE_PASS) != 0;
+  if (stats && single_pass)
+    return fail(RK_ERR_DOMAIN, "round scoring needs the two-pass (fp32-class) path: selection is bit-exact");
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (bad_row) {
     fill_i32<<<1, 1, 0, cs>>>(bad_row, INT_MAX);
@@ -494,7 +497,7 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d, const void* k, 
   if (need > workspace_bytes) return fail(RK_ERR_CAPACITY, "prefill workspace %zu < %zu", workspace_bytes, need);
   float *item_m = nullptr, *item_l = nullptr;
   st = launch_prefill_tc(q, n_q, hq, k, v, s, hkv, q_pos, k_pos, allowed, items, items ? n_items : 0, stats, out,
-                         bad_row, workspace, pl.total, &item_m, &item_l, nullptr, nullptr, cs);
+                         bad_row, workspace, pl.total, &item_m, &item_l, nullptr, nullptr, cs, single_pass);
   if (st) return st;
   if (stats) {
     double* rows_mass = reinterpret_cast<double*>(static_cast<char*>(workspace) + pl.total);

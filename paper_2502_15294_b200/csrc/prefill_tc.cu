@@ -318,7 +318,10 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 
 // SCORE_ONLY: the watershed scorer (rk_round_scores) — QK^T and the per-item
 // softmax statistics only: no V, no PV, no O, no row-max exchange.
-template <bool SCORE_ONLY>
+// SPLIT (default): q and P as bf16 hi + lo, two MMA passes each (fp32-class
+// outputs).  !SPLIT: the single-pass bf16 path (bf16 q and P, one pass each,
+// bf16-class outputs; rk_prefill_attention flag RK_PREFILL_SINGLE_PASS).
+template <bool SCORE_ONLY, bool SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                   const __grid_constant__ CUtensorMap vmap, const __grid_constant__ Params p) {
@@ -510,7 +513,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           const uint64_t a0 = desc_sw128(qs_a, 16);
           const uint64_t b0 = desc_sw128(ks_a + s * K_STAGE, 16);     // this CTA's 64 keys (peer: same offset)
   #pragma unroll
-          for (int hl = 0; hl < 2; ++hl)          // q_hi, q_lo
+          for (int hl = 0; hl < (SPLIT ? 2 : 1); ++hl)          // q_hi, q_lo
   #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
               umma2(dS, a0 + (uint64_t)((((2 * hl + k / 4) * QBOX) + 32 * (k % 4)) >> 4),
@@ -542,7 +545,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           const uint32_t a0 = tmem + b * BN;                             // P_hi | P_lo (16 keys = 8 columns)
           const bool first = pi.first;
   #pragma unroll
-          for (int hl = 0; hl < 2; ++hl)          // P_hi, P_lo
+          for (int hl = 0; hl < (SPLIT ? 2 : 1); ++hl)          // P_hi, P_lo
   #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
               umma2_ts(tmem_o, a0 + hl * (BN / 2) + kk * 8, b0 + (uint64_t)((kk * 16 * 128) >> 4), kIdescPV,
@@ -681,11 +684,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
             acc2 = ffma2(e, one, acc2);
             __nv_bfloat162 hb = __floats2bfloat162_rn(e.x, e.y);
             const uint32_t hu = *reinterpret_cast<uint32_t*>(&hb);
-            const float2 lo2 = ffma2(make_float2(__uint_as_float(hu << 16), __uint_as_float(hu & 0xffff0000u)),
-                                     mone, e);
-            __nv_bfloat162 lb = __floats2bfloat162_rn(lo2.x, lo2.y);
             hw[i / 2] = hu;
-            lw[i / 2] = *reinterpret_cast<uint32_t*>(&lb);
+            if constexpr (SPLIT) {
+              const float2 lo2 = ffma2(make_float2(__uint_as_float(hu << 16), __uint_as_float(hu & 0xffff0000u)),
+                                       mone, e);
+              __nv_bfloat162 lb = __floats2bfloat162_rn(lo2.x, lo2.y);
+              lw[i / 2] = *reinterpret_cast<uint32_t*>(&lb);
+            }
           }
           const float rs = acc2.x + acc2.y;
           l_half = (rescale ? l_half * fac : l_half) + rs;
@@ -732,7 +737,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           any_tile = true;
           // ---- P over its own S columns: [P_hi keys 0-63 | P_lo keys 0-63], bf16x2 per column
           tmem_st32u(tmem + lane_base + b * BN + (HK / 2) * half, hw);            // P_hi columns
-          tmem_st32u(tmem + lane_base + b * BN + BN / 2 + (HK / 2) * half, lw);   // P_lo columns
+          if constexpr (SPLIT) tmem_st32u(tmem + lane_base + b * BN + BN / 2 + (HK / 2) * half, lw);   // P_lo
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           fence_before();
           __syncwarp();
@@ -907,7 +912,7 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
                       const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed, const int32_t* items,
                       int n_items_in, bool stats, float* out, int32_t* bad_row, void* ws, size_t ws_bytes,
                       float** item_m_out, float** item_l_out, float** stat_m_out, float** stat_l_out,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool single_pass) {
   const int G = hq / hkv;
   const bool score_only = out == nullptr;          // the watershed scorer: statistics only
   if (score_only && !stats) return fail(RK_ERR_DOMAIN, "prefill without output needs the scoring statistics");
@@ -961,19 +966,24 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
   p.part_m = part_m; p.part_l = part_l; p.part_o = part_o;
   static bool configured = false;
   if (!configured) {
-    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pf::SMEM), "prefill_tc smem attribute");
-    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pf::SMEM), "prefill_tc smem attribute");
+    RK_CUDA(cudaFuncSetAttribute(pf::prefill_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pf::SMEM), "prefill_tc smem attribute");
     configured = true;
   }
   const int grid = 2 * std::min(sm_count() / 2, pl.n_units);   // CTA pairs (__cluster_dims__(2,1,1))
   if (score_only) {
-    pf::prefill_tc_kernel<true><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
+    pf::prefill_tc_kernel<true, true><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
     RK_CHECK_LAUNCH("prefill_tc_kernel<score>");
     return RK_OK;
   }
-  pf::prefill_tc_kernel<false><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
+  if (single_pass)
+    pf::prefill_tc_kernel<false, false><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
+  else
+    pf::prefill_tc_kernel<false, true><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
   RK_CHECK_LAUNCH("prefill_tc_kernel");
   const int nrh = (int)rh;
   pf::prefill_merge_kernel<<<(nrh * 32 + 255) / 256, 256, 0, st>>>(part_m, part_l, part_o, nrh, hq, pl.n_chunks,

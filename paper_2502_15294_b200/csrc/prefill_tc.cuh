@@ -23,6 +23,6 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
                       const int64_t* q_pos, const int64_t* k_pos, const uint8_t* allowed, const int32_t* items,
                       int n_items_in, bool stats, float* out, int32_t* bad_row, void* ws, size_t ws_bytes,
                       float** item_m_out, float** item_l_out, float** stat_m_out, float** stat_l_out,
-                      cudaStream_t st);
+                      cudaStream_t st, bool single_pass = false);
 
 }  // namespace rk

@@ -116,11 +116,13 @@ def items_tensor(per_dialogue_bounds, chunk: int, device) -> tuple[torch.Tensor,
 def prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: torch.Tensor, k_pos: torch.Tensor,
                       *, allowed: torch.Tensor | None = None, items: torch.Tensor | None = None, n_bins: int = 0,
                       active: torch.Tensor | None = None, out: torch.Tensor | None = None,
-                      raw: torch.Tensor | None = None, bad_row: torch.Tensor | None = None, stream=None):
+                      raw: torch.Tensor | None = None, bad_row: torch.Tensor | None = None,
+                      single_pass: bool = False, stream=None):
     """Question-prefill attention on the tensor cores (rk_prefill_attention).
 
     q (n_q, Hq, 128) f32; k/v (S, Hkv, 128) bf16; q_pos (n_q,) / k_pos (S,)
-    int64 device; allowed (S,) uint8 or None.  With `items` ((n_items, 3)
+    int64 device; allowed (S,) uint8 or None.  single_pass: the bf16 path (q and
+    P rounded to bf16, one MMA pass each; ~1e-2 relative).  With `items` ((n_items, 3)
     int32 round-aligned (lo, hi, bin)) and n_bins > 0 the Eq. 1 masses of the
     active bins come back in `raw` (float64) from the same pass.  Returns
     (out (n_q, Hq, 128) f32, raw or None, bad_row (1,) int32 device).
@@ -141,5 +143,5 @@ def prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: 
     _lib.call("rk_prefill_attention", _lib.ptr(q), n_q, hq, d, _lib.ptr(k), _lib.ptr(v), kv_code(k), s, hkv,
               _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(allowed), _lib.ptr(items), n_items,
               n_bins if raw is not None else 0, _lib.ptr(active), _lib.ptr(out), _lib.ptr(raw), _lib.ptr(bad_row),
-              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
+              _lib.ptr(ws), ws.numel(), _lib.RK_PREFILL_SINGLE_PASS if single_pass else 0, _lib.stream_ptr(stream))
     return out, raw, bad_row

@@ -20,7 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 from paper_2502_15294_b200 import backend, kernels  # noqa: E402
-from paper_2502_15294_b200.errors import InvariantError  # noqa: E402
+from paper_2502_15294_b200.errors import DomainError, InvariantError  # noqa: E402
 from paper_2502_15294_b200.stats import build_round_items  # noqa: E402
 
 D = 128
@@ -136,3 +136,20 @@ def test_kernel_contract_routes_multirow_bf16_to_tensor_cores(rng, monkeypatch):
     np.testing.assert_allclose(sc.cpu().numpy(), ref_sc, rtol=1e-4, atol=1e-8)
     with pytest.raises(InvariantError):
         backend.attention_forward_gqa(tq, tk, tv, tqp - 10**6, tkp)
+
+
+def test_prefill_single_pass_bf16_path(rng):
+    """RK_PREFILL_SINGLE_PASS: q and P rounded to bf16, one MMA pass each (the
+    bf16 path, stated separately from the fp32-class default): max error within
+    3e-2 of the output range, mean within 3e-3; scoring is refused on it."""
+    n_q, hist, hkv, G = 200, 3000, 2, 7
+    q, k, v, qp, kp = _inputs(rng, n_q, hist, hkv, G, scale=1.0)
+    ref, _ = oatt.attention_forward_gqa(q, k, v, qp, kp)
+    args = _dev(q, k, v, qp, kp)[:5]
+    out, _, _ = kernels.prefill_attention(*args, single_pass=True)
+    got = out.reshape(n_q, -1).cpu().numpy()
+    assert _rel(got, ref) < 3e-2
+    assert float(np.abs(got - ref).mean() / np.abs(ref).max()) < 3e-3
+    items = torch.from_numpy(build_round_items([(0, hist, 0), (hist, hist + n_q, 1)], 1024)).cuda()
+    with pytest.raises(DomainError):
+        kernels.prefill_attention(*args, items=items, n_bins=1, single_pass=True)

@@ -66,8 +66,10 @@ for nq in [int(x) for x in a.nq.split(",")]:
     ms_fused = timed(lambda: kernels.prefill_attention(q, k, v, qp, kp, items=items, n_bins=a.rounds, out=out),
                      a.reps)
     ms_score = timed(lambda: stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024), a.reps)
+    ms_single = timed(lambda: kernels.prefill_attention(q, k, v, qp, kp, out=out, single_pass=True), a.reps)
     r = dict(n_q=nq, keys=s, hq=hq, hkv=hkv, ms_prefill=ms_plain, ms_prefill_fused_scoring=ms_fused,
-             ms_separate_scorer=ms_score, algo_tflops=flop / ms_plain / 1e9,
+             ms_separate_scorer=ms_score, ms_single_pass_bf16=ms_single,
+             algo_tflops_single_pass=flop / ms_single / 1e9, algo_tflops=flop / ms_plain / 1e9,
              frac_bf16_peak=flop / ms_plain / 1e9 / PEAK_TF, issued_tflops=2 * flop / ms_plain / 1e9,
              fused_scoring_overhead=ms_fused / ms_plain - 1.0, peak_tflops=PEAK_TF)
     rows.append(r)
