@@ -130,6 +130,43 @@ def test_decode_append_vs_oracle(rng, G, d, dtype):
     assert torch.equal(sl.cpu(), torch.from_numpy(lens.astype(np.int32)))
 
 
+@pytest.mark.parametrize("lens", [
+    [2999, 17, 1024, 1, 700, 2048, 5, 333, 1500, 64, 2999, 900],     # ragged, a dialogue spans 1..many CTAs
+    [3, 1, 2, 5, 4, 1, 2, 3, 1],                                       # fewer keys than CTAs (sparse ranges)
+    [2999] * 16,                                                       # the bench's 16-dialogue group shape
+])
+def test_decode_larger_batches_vs_oracle(rng, lens):
+    """B >= 8 ragged / sparse / bench-shaped batches: persistent split over the
+    concatenated key ranges + merge; repeated calls and a different shape on
+    the same workspace arena give identical results."""
+    B, hkv, G, d, cap = len(lens), 8, 4, 128, 3000
+    lens = np.array(lens)
+    kc = torch.randn(B, cap + 1, hkv, d, device="cuda").bfloat16()
+    vc = torch.randn(B, cap + 1, hkv, d, device="cuda").bfloat16()
+    q = torch.randn(B, hkv * G, d, device="cuda")
+    kn = torch.randn(B, hkv, d, device="cuda").bfloat16()
+    vn = torch.randn(B, hkv, d, device="cuda").bfloat16()
+    sl = torch.from_numpy(lens.astype(np.int32)).cuda()
+    ws = kernels.decode_workspace(B, hkv * G, hkv, d, 592, "cuda", tag="batch_test")
+    outs = []
+    for rep in range(3):
+        outs.append(kernels.decode_attention(q, kc, vc, sl, int(lens.max()) + 1, k_new=kn, v_new=vn, ws=ws).clone())
+        # a different (smaller) batch on the same arena between calls
+        kernels.decode_attention(q[:9], kc[:9], vc[:9], sl[:9], int(lens[:9].max()) + 1, k_new=kn[:9],
+                                 v_new=vn[:9], ws=ws)
+    torch.cuda.synchronize()
+    for rep in range(1, 3):
+        assert torch.equal(outs[rep], outs[0])
+    out = outs[0]
+    for b in range(B):
+        L = lens[b]
+        kk = kc[b, : L + 1].float().cpu().numpy()
+        vv = vc[b, : L + 1].float().cpu().numpy()
+        ref, _ = oatt.attention_forward_gqa(q[b:b + 1].cpu().numpy(), kk, vv, [L], np.arange(L + 1))
+        err = np.abs(out[b].reshape(1, -1).cpu().numpy() - ref).max() / np.abs(ref).max()
+        assert err < 1e-5, (b, err)
+
+
 def test_decode_advance_lengths():
     sl = torch.tensor([3, 5], dtype=torch.int32, device="cuda")
     kernels.advance_lengths(sl, 2)
