@@ -35,6 +35,7 @@ for S in [int(x) for x in a.keys.split(",")]:
         out = torch.empty(B, a.hq, d, device="cuda")
         ws = kernels.decode_workspace(B, a.hq, a.hkv, d, 592, "cuda", tag=f"l{B}_{S}")
         st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())      # inputs were written on the default stream
         with torch.cuda.stream(st):
             for _ in range(3):
                 kernels.decode_attention(q, kc, vc, sl, S + 1, k_new=kn, v_new=vn, out=out, ws=ws)

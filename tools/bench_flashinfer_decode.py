@@ -33,6 +33,7 @@ for S in [int(x) for x in a.keys.split(",")]:
         w.plan(indptr, indices, last, a.hq, a.hkv, d, page, q_data_type=torch.bfloat16,
                kv_data_type=torch.bfloat16)
         st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())      # inputs were written on the default stream
         with torch.cuda.stream(st):
             for _ in range(3):
                 o = w.run(q, kv)
