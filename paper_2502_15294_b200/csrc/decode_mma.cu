@@ -14,11 +14,11 @@
 // reductions and bf16 unpacking that made the CUDA-core consumer
 // instruction-bound (profiles/r01_decode_bulk_ncu.txt).
 //
-// Shared-memory tiles keep each key's row of all heads ([HKV][D] bf16) padded
-// by 16 bytes, so the 8 row addresses of every ldmatrix hit distinct banks; the
-// producer fills them with one cp.async.bulk per key row (32 lanes in
+// Shared-memory tiles hold key rows ([HKV][D] bf16, token-major as in the
+// cache) in runs of GK consecutive keys, ~2 KB per run, each run padded by 16
+// bytes; the producer fills a run with one cp.async.bulk (32 lanes in
 // parallel).  The appended token's row is copied from k_new straight into its
-// slot of the last tile.
+// slot of the last run.
 #include <cmath>
 
 #include "decode_common.cuh"
@@ -30,17 +30,26 @@ constexpr float kRescaleLog2 = 8.f;   // lazy softmax rescale threshold (log2 un
 template <int D, int HKV>
 struct MmaTile {
   static constexpr int ROW = HKV * D;               // bf16 elements per key
-  static constexpr int RS = ROW * 2 + 16;           // padded row stride, bytes
+  static constexpr int ROWB = ROW * 2;              // bytes per key row (all kv-heads)
+  // keys are copied in runs of GK consecutive rows (contiguous in the token-major
+  // cache), so every bulk copy moves ~2 KB whatever the head count: per-copy
+  // issue, not bandwidth, limited 1 KB rows to ~4.5 TB/s and 512 B rows to
+  // ~2.4 TB/s; each run is padded by 16 B (GK-way ldmatrix bank conflicts,
+  // cheap beside the memory stream)
+  static constexpr int GK = ROWB >= 2048 ? 1 : 2048 / ROWB;
+  static constexpr int GS = GK * ROWB + 16;         // run stride, bytes
   static constexpr int P = kConsumerWarps / HKV;    // warps per kv-head
   static constexpr int TK = 16 * P;                 // keys per stage: one 16-key group per warp
-  static constexpr int SB = TK * RS;                // bytes per operand per stage
+  static_assert(TK % GK == 0, "a stage holds whole runs");
+  static constexpr int SB = (TK / GK) * GS;         // bytes per operand per stage
+  __host__ __device__ static constexpr int row_off(int r) { return (r / GK) * GS + (r % GK) * ROWB; }
   static constexpr size_t smem = 2 * kStages * (size_t)SB + 2 * kStages * sizeof(uint64_t);
 };
 
 template <int D, int G, int HKV>
 __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __grid_constant__ BulkParams p) {
   using Tl = MmaTile<D, HKV>;
-  constexpr int ROW = Tl::ROW, RS = Tl::RS, P = Tl::P, TK = Tl::TK, SB = Tl::SB;
+  constexpr int ROW = Tl::ROW, P = Tl::P, TK = Tl::TK, SB = Tl::SB, GK = Tl::GK;
   constexpr int KC = D / 16;                        // k-chunks of the QK product
   constexpr int NT = D / 8;                         // n-tiles of the PV product
   static_assert(G <= 8 && D % 32 == 0, "group <= 8 rows per half, D multiple of 32");
@@ -89,14 +98,24 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
           mbar_expect_tx(&full[s], (unsigned)(2 * nk * ROW * 2));
         }
         __syncwarp();
-        for (int i = lane; i < nk; i += 32) {
+        for (int i = lane * GK; i < nk; i += 32 * GK) {      // one run of <= GK rows per lane
           const int j = j0 + i;
-          const __nv_bfloat16* ks = (j == new_j) ? reinterpret_cast<const __nv_bfloat16*>(p.k_new) + (int64_t)sgm.b * ROW
-                                                 : kb + (int64_t)j * ROW;
-          const __nv_bfloat16* vs = (j == new_j) ? reinterpret_cast<const __nv_bfloat16*>(p.v_new) + (int64_t)sgm.b * ROW
-                                                 : vb + (int64_t)j * ROW;
-          bulk_g2s(kst + (size_t)s * SB + (size_t)i * RS, ks, ROW * 2, &full[s], pol);
-          bulk_g2s(vst + (size_t)s * SB + (size_t)i * RS, vs, ROW * 2, &full[s], pol);
+          int cnt = min(GK, nk - i);
+          // the appended key (the dialogue's last, new_j) comes from k_new / v_new
+          const bool has_new = new_j >= j && new_j < j + cnt;
+          const int from_cache = has_new ? new_j - j : cnt;
+          uint8_t* kd = kst + (size_t)s * SB + Tl::row_off(i);
+          uint8_t* vd = vst + (size_t)s * SB + Tl::row_off(i);
+          if (from_cache > 0) {
+            bulk_g2s(kd, kb + (int64_t)j * ROW, (unsigned)(from_cache * ROW * 2), &full[s], pol);
+            bulk_g2s(vd, vb + (int64_t)j * ROW, (unsigned)(from_cache * ROW * 2), &full[s], pol);
+          }
+          if (has_new) {
+            bulk_g2s(kd + from_cache * ROW * 2, reinterpret_cast<const __nv_bfloat16*>(p.k_new) + (int64_t)sgm.b * ROW,
+                     ROW * 2, &full[s], pol);
+            bulk_g2s(vd + from_cache * ROW * 2, reinterpret_cast<const __nv_bfloat16*>(p.v_new) + (int64_t)sgm.b * ROW,
+                     ROW * 2, &full[s], pol);
+          }
         }
       }
     }
@@ -156,12 +175,12 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
       const int nkw = min(16, max(0, nk - 16 * slice));        // valid keys of this warp's group
       mbar_wait(&full[s], (t / kStages) & 1);
       if (nkw > 0) {
-        const uint8_t* kb = kst + (size_t)s * SB + (size_t)(16 * slice) * RS + h * D * 2;
-        uint8_t* vb = vst + (size_t)s * SB + (size_t)(16 * slice) * RS + h * D * 2;
+        const uint8_t* kb = kst + (size_t)s * SB + h * D * 2;    // + Tl::row_off(key row)
+        uint8_t* vb = vst + (size_t)s * SB + h * D * 2;
         if (nkw < 16) {   // rows past the valid keys hold stale bytes: zero this head's V columns
           for (int e = lane; e < (16 - nkw) * (D / 8); e += 32) {
             const int r = nkw + e / (D / 8), q16 = e % (D / 8);
-            reinterpret_cast<uint4*>(vb + (size_t)r * RS)[q16] = make_uint4(0, 0, 0, 0);
+            reinterpret_cast<uint4*>(vb + Tl::row_off(16 * slice + r))[q16] = make_uint4(0, 0, 0, 0);
           }
           // generic-proxy writes to a buffer the bulk copies refill later
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -172,10 +191,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
 #pragma unroll
         for (int kk = 0; kk < KC / 2; ++kk) {
           uint32_t r[4];
-          ldmatrix_x4(r, kb + (size_t)(lane & 7) * RS + (32 * kk + 8 * (lane >> 3)) * 2);
+          ldmatrix_x4(r, kb + Tl::row_off(16 * slice + (lane & 7)) + (32 * kk + 8 * (lane >> 3)) * 2);
           mma_bf16_16816(s0, qa[2 * kk], r[0], r[1]);
           mma_bf16_16816(s0, qa[2 * kk + 1], r[2], r[3]);
-          ldmatrix_x4(r, kb + (size_t)(8 + (lane & 7)) * RS + (32 * kk + 8 * (lane >> 3)) * 2);
+          ldmatrix_x4(r, kb + Tl::row_off(16 * slice + 8 + (lane & 7)) + (32 * kk + 8 * (lane >> 3)) * 2);
           mma_bf16_16816(s1, qa[2 * kk], r[0], r[1]);
           mma_bf16_16816(s1, qa[2 * kk + 1], r[2], r[3]);
         }
@@ -217,7 +236,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
 #pragma unroll
         for (int jj = 0; jj < NT / 2; ++jj) {
           uint32_t r[4];
-          ldmatrix_x4_trans(r, vb + (size_t)((lane & 7) + 8 * ((lane >> 3) & 1)) * RS + (16 * jj + 8 * (lane >> 4)) * 2);
+          ldmatrix_x4_trans(r, vb + Tl::row_off(16 * slice + (lane & 7) + 8 * ((lane >> 3) & 1)) +
+                                   (16 * jj + 8 * (lane >> 4)) * 2);
           mma_bf16_16816(o[2 * jj], pa, r[0], r[1]);
           mma_bf16_16816(o[2 * jj + 1], pa, r[2], r[3]);
         }
