@@ -15,7 +15,7 @@
 // instruction-bound (profiles/r01_decode_bulk_ncu.txt).
 //
 // Shared-memory tiles hold key rows ([HKV][D] bf16, token-major as in the
-// cache) in runs of GK consecutive keys, ~2 KB per run, each run padded by 16
+// cache) in runs of GK consecutive keys, ~4 KB per run, each run padded by 16
 // bytes; the producer fills a run with one cp.async.bulk (32 lanes in
 // parallel).  The appended token's row is copied from k_new straight into its
 // slot of the last run.
@@ -32,11 +32,14 @@ struct MmaTile {
   static constexpr int ROW = HKV * D;               // bf16 elements per key
   static constexpr int ROWB = ROW * 2;              // bytes per key row (all kv-heads)
   // keys are copied in runs of GK consecutive rows (contiguous in the token-major
-  // cache), so every bulk copy moves ~2 KB whatever the head count: per-copy
+  // cache), so every bulk copy moves >= ~4 KB whatever the head count: per-copy
   // issue, not bandwidth, limited 1 KB rows to ~4.5 TB/s and 512 B rows to
   // ~2.4 TB/s; each run is padded by 16 B (GK-way ldmatrix bank conflicts,
   // cheap beside the memory stream)
-  static constexpr int GK = ROWB >= 2048 ? 1 : 2048 / ROWB;
+#ifndef RK_RUN_BYTES
+#define RK_RUN_BYTES 4096
+#endif
+  static constexpr int GK = ROWB >= RK_RUN_BYTES ? 1 : RK_RUN_BYTES / ROWB;
   static constexpr int GS = GK * ROWB + 16;         // run stride, bytes
   static constexpr int P = kConsumerWarps / HKV;    // warps per kv-head
   static constexpr int TK = 16 * P;                 // keys per stage: one 16-key group per warp
