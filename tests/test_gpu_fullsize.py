@@ -1,0 +1,83 @@
+"""Parity at the BASELINE configurations' full sizes, where the
+fp64 oracle is still affordable on a subset: decode attention over a C4-sized
+128 K-token cache (Llama-3-8B-shaped GQA), and the C3 question prefill
+(Qwen2-7B-shaped, 512 question rows over 64 x 1024 history keys) checked row
+by row on sampled rows, with its fused Eq. 1 masses checked against the
+oracle's capture + aggregate on a 16-row question subset (all 66K keys) and the
+selection from the 512-row masses against the planted relevant rounds."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import attention as oatt
+from oracle import rounds as orr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2502_15294_b200 import kernels, stats  # noqa: E402
+from paper_2502_15294_b200.stats import build_round_items  # noqa: E402
+
+
+def test_decode_c4_128k_context_vs_oracle():
+    hkv, G, d, S = 8, 4, 128, 128 * 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    kc = torch.randn(1, S + 1, hkv, d, device="cuda", generator=g).bfloat16()
+    vc = torch.randn(1, S + 1, hkv, d, device="cuda", generator=g).bfloat16()
+    q = 2.0 * torch.randn(1, hkv * G, d, device="cuda", generator=g)
+    kn = torch.randn(1, hkv, d, device="cuda", generator=g).bfloat16()
+    vn = torch.randn(1, hkv, d, device="cuda", generator=g).bfloat16()
+    sl = torch.full((1,), S, dtype=torch.int32, device="cuda")
+    out = kernels.decode_attention(q, kc, vc, sl, S + 1, k_new=kn, v_new=vn)
+    torch.cuda.synchronize()
+    K = kc[0].float().cpu().numpy()
+    V = vc[0].float().cpu().numpy()
+    ref, _ = oatt.attention_forward_gqa(q.cpu().numpy(), K, V, [S], np.arange(S + 1))
+    err = np.abs(out.reshape(1, -1).cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err < 1e-5, err
+
+
+def test_prefill_c3_full_size_rows_and_masses():
+    hq, hkv, d, nq, R, T = 28, 4, 128, 512, 64, 1024
+    hist = R * T
+    s = hist + nq
+    rng = np.random.default_rng(11)
+    q = rng.standard_normal((nq, hq, d)).astype(np.float32)
+    k = oatt.round_to_bf16(rng.standard_normal((s, hkv, d)).astype(np.float32))
+    v = oatt.round_to_bf16(rng.standard_normal((s, hkv, d)).astype(np.float32))
+    # planted relevance on rounds 5 and 40 so the K-boundary gap is wide
+    u = q.reshape(nq, hkv, G := hq // hkv, d).mean(axis=(0, 2))
+    u /= np.linalg.norm(u, axis=-1, keepdims=True)
+    for r in (5, 40):
+        k[r * T:(r + 1) * T] = oatt.round_to_bf16(k[r * T:(r + 1) * T] + 0.4 * np.sqrt(d) * u[None])
+    qp, kp = np.arange(hist, s), np.arange(s)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    tq, tk, tv = t(q), t(k).bfloat16(), t(v).bfloat16()
+    tqp, tkp = t(qp.astype(np.int64)), t(kp.astype(np.int64))
+    bounds = [(r * T, (r + 1) * T, r) for r in range(R)] + [(hist, s, R)]
+    items = torch.from_numpy(build_round_items(bounds, 1024)).cuda()
+    out, raw, bad = kernels.prefill_attention(tq, tk, tv, tqp, tkp, items=items, n_bins=R)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 2**31 - 1
+    got = out.reshape(nq, -1).cpu().numpy()
+    rows = [0, 1, 255, 511]                  # first rows, middle, the last (most causal keys)
+    ref, _ = oatt.attention_forward_gqa(q[rows], k, v, qp[rows], kp)
+    err = np.abs(got[rows] - ref).max() / np.abs(ref).max()
+    assert err < 2e-5, err
+    # fused Eq. 1 masses vs the oracle's capture + aggregate, on the last 16 question
+    # rows (every history key + the causal question prefix; row_offset maps the rows)
+    sub = np.arange(nq - 16, nq)
+    _, raw_sub, _ = kernels.prefill_attention(tq[sub], tk, tv, tqp[sub], tkp, items=items, n_bins=R)
+    _, cap = oatt.attention_forward_gqa(q[sub], k, k, qp[sub], kp, capture=True)
+    rounds = [orr.Round(r, (r * T, r * T + 1), (r * T + 1, (r + 1) * T)) for r in range(R)]
+    rounds.append(orr.Round(R, (hist + nq - 16, s), (s, s)))   # the question span = the 16 rows
+    ref_raw = orr.aggregate_round_attention(cap, rounds, "question", R, row_offset=hist + nq - 16)
+    np.testing.assert_allclose(raw_sub.cpu().numpy(), ref_raw, rtol=2e-5, atol=1e-9)
+    raw_tc = raw.cpu().numpy()
+    pol = orr.SelectionPolicy("top_percent", fraction=0.10)
+    kept = orr.select(orr.normalize(raw_tc), pol)
+    assert {5, 40} <= set(kept) and len(kept) == orr.top_k_count(R, 0.10, 1)
