@@ -106,6 +106,15 @@ int rk_decode_attention(const float* q, int batch, int hq, int d,
 /* seq_len[i] += delta for i < n (advance one decode step) */
 int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream);
 
+/* Which decode kernel rk_decode_attention runs for this shape (no launch):
+ * C > 0  one thread-block cluster of C CTAs per (dialogue, kv-head), split-K
+ *        merged in distributed shared memory (small batches: batch*hkv <= SMs,
+ *        bf16, d 64/128, no item table);
+ * 0      persistent split-K over the concatenated key ranges + merge kernel;
+ * -1     the generic split kernel (other dtypes / head shapes). */
+int rk_decode_plan(int batch, int hq, int hkv, int d, int kv_dtype, int max_seq_len, int64_t cache_stride,
+                   int has_items);
+
 /* ------------------------------------------------------------------------
  * 3. Watershed round scoring: the fused equivalent of
  *      capture = attention_forward(q, K_{Lw-1}, ..., capture=True)[1]

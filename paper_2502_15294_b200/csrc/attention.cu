@@ -332,6 +332,16 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
     return fail(RK_ERR_DOMAIN, "item table needs 0 < items_stride <= 512 and n_items");
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   const int G = hq / hkv;
+  if (!items) {   // small batches: one cluster per (dialogue, kv-head), merge in DSMEM (decode_cluster.cu)
+    const int C = cluster_decode_size(kv_dtype, d, hkv, G, batch, max_seq_len, cache_stride);
+    if (C) {
+      st = launch_decode_cluster(C, q, batch, hq, d, k_cache, v_cache, hkv, cache_stride, seq_len, max_seq_len,
+                                 k_new, v_new, out, cs);
+      if (st) return st;
+      if (advance_len) return rk_advance_lengths(advance_len, batch, 1, stream);
+      return RK_OK;
+    }
+  }
   if (bulk_supported(kv_dtype, d, hkv, G)) {
     int sp = items ? items_stride * (8 / hkv) : bulk_splits(batch, max_seq_len, hkv);
     SplitWs w = carve(workspace, batch, hq, hkv, sp, d);
@@ -370,6 +380,17 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
   if (st) return st;
   if (advance_len) return rk_advance_lengths(advance_len, batch, 1, stream);
   return RK_OK;
+}
+
+int rk_decode_plan(int batch, int hq, int hkv, int d, int kv_dtype, int max_seq_len, int64_t cache_stride,
+                   int has_items) {
+  if (batch <= 0 || hkv <= 0 || hq <= 0 || hq % hkv) return -1;
+  const int G = hq / hkv;
+  if (!has_items) {
+    const int C = cluster_decode_size(kv_dtype, d, hkv, G, batch, max_seq_len, cache_stride);
+    if (C) return C;
+  }
+  return bulk_supported(kv_dtype, d, hkv, G) ? 0 : -1;
 }
 
 int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream) {

@@ -30,4 +30,10 @@ int launch_decode_mma(int d, int hkv, int G, dim3 grid, const BulkParams& p, cud
 int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const BulkParams& p, float* out,
                        int32_t* advance, cudaStream_t st, bool pdl);
 
+// small-batch cluster decode (decode_cluster.cu): cluster size, 0 = not applicable
+int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride);
+int launch_decode_cluster(int C, const float* q, int batch, int hq, int d, void* k_cache, void* v_cache, int hkv,
+                          int64_t batch_stride, const int32_t* seq_len, int max_len, const void* k_new,
+                          const void* v_new, float* out, cudaStream_t st);
+
 }  // namespace rk

@@ -1,0 +1,489 @@
+// Small-batch decode attention: one thread-block cluster per (dialogue,
+// kv-head), the split-K merge done in distributed shared memory.
+//
+// At a few dialogues the persistent split-K decode (decode_mma.cu) spends more
+// time on its fixed per-layer chain (decode grid -> partials in global memory
+// -> merge kernel) than on streaming the ~9 MB of a kept-rounds layer.  Here
+// the C CTAs of a cluster split one (dialogue b, kv-head h) key range
+// [0, len) into C contiguous slices and combine their (m, l, acc) partials
+// over DSMEM, so a layer is ONE kernel with no workspace:
+//   warp 8      producer: one lane issues 2-D TMA boxes {64 dims, 128 keys}
+//               (128-byte swizzle) of head h's K and V columns — 256-byte
+//               pieces of the token-major [S][HKV][D] rows, gathered by the
+//               tensor unit instead of one bulk copy per key — into a 3-stage
+//               ring (full/empty mbarriers); the box, not the byte count, is
+//               the TMA's unit of work (tools/tma_probe.cu: {64,16} boxes
+//               stream 18 B/clk/SM, {64,128} 36 B/clk/SM);
+//   warps 0..7  consumers: warp w owns the 16-key group w of each stage; the
+//               math is decode_mma's (mma.sync m16n8k16, q and P split into
+//               bf16 hi/lo rows so the products carry ~16 mantissa bits, lazy
+//               rescale), with swizzled ldmatrix addresses;
+//   epilogue    warps -> CTA partial in smem -> barrier.cluster -> CTA rank r
+//               merges its share of the (query head, dim) outputs from all C
+//               CTAs' partials (ld.shared::cluster) and writes them.
+// The appended token (k_new/v_new) is written into the cache row len-1 by the
+// producer of the slice that owns it, before its TMA reads that row
+// (fence.proxy.async orders the generic stores before the async-proxy loads).
+// Semantics = rk_decode_attention's uniform mode (pipeline.py:298-313 ->
+// engine.py:244-267 with one question row; kernel contract _attn_ext.pyx:20-81).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "decode_common.cuh"
+#include "tc_common.cuh"
+
+namespace rk {
+namespace {
+
+// 8 consumer warps + 1 producer, 3 stages of 128 keys (~197 KB): one CTA per
+// SM.  (A 4-warp, 64-key-stage variant with two CTAs per SM, meant to let the
+// next layer's CTAs prefetch under PDL, measured slower at every batch.)
+constexpr int kCW = 8;                       // consumer warps
+constexpr int kThreads = (kCW + 1) * 32;
+constexpr int kStg = 3;
+constexpr int kBoxRows = 16;                 // keys per box (one consumer warp's group)
+constexpr int kTK = kBoxRows * kCW;          // keys per stage
+constexpr int kBoxBytes = kBoxRows * 128;    // 16 keys x 64 bf16 dims
+
+template <int D>
+struct CTile {
+  static constexpr int NH = D / 64;                      // 64-dim halves (boxes per key group)
+  static constexpr int HALF = kTK * 128;                 // one 64-dim half of a stage: [kTK rows][128 B]
+  static constexpr int OP = NH * HALF;                   // bytes of K (or V) per stage
+  static constexpr size_t smem = 1024 + 2 * (size_t)kStg * OP + 2 * kStg * sizeof(uint64_t);
+  // byte offset of (key row r of group w, dims [8*c8, 8*c8+8)) in one operand
+  // stage; rows of a half are contiguous, so a full stage is one {64, kTK} box
+  // per half and a partial one is {64, 16} boxes per group (same layout)
+  __device__ static __forceinline__ uint32_t off(int w, int r, int c8) {
+    const int hf = c8 >> 3, c = c8 & 7;
+    return (uint32_t)(hf * HALF + (16 * w + r) * 128 + ((c ^ (r & 7)) << 4));
+  }
+};
+
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32)); }
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_cluster(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                        uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+struct ClusterParams {
+  const float* q;          // [B][Hq][D]
+  __nv_bfloat16* k;        // cache base (k_map / v_map describe the same memory)
+  __nv_bfloat16* v;
+  int64_t rows_per_b;      // cache rows (keys) per dialogue = batch_stride / (HKV*D)
+  const int32_t* seq_len;  // [B]
+  const __nv_bfloat16* k_new;   // [B][HKV][D] or null
+  const __nv_bfloat16* v_new;
+  int hq, hkv;
+  float scale_log2;
+  float* out;              // [B][Hq][D]
+};
+
+// kmap/vmap: {64, kTK}-key boxes (whole stages); kmap16/vmap16: {64, 16} (the
+// last, partial stage of a slice, so a slice reads at most 15 keys past its end)
+template <int D, int G>
+__global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                                     const __grid_constant__ CUtensorMap vmap,
+                                                                     const __grid_constant__ CUtensorMap kmap16,
+                                                                     const __grid_constant__ CUtensorMap vmap16,
+                                                                     const __grid_constant__ ClusterParams p) {
+  using T = CTile<D>;
+  constexpr int NH = T::NH, OP = T::OP;
+  constexpr int KC = D / 16, NT = D / 8;
+  static_assert(G <= 8, "at most 8 query heads per kv-head");
+  extern __shared__ uint8_t smem_raw[];
+  // 128-byte swizzled TMA boxes need 1024-byte aligned destinations
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* kst = smem;
+  uint8_t* vst = smem + kStg * OP;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStg * OP);
+  uint64_t* empty = full + kStg;
+  __shared__ float c_m[8], c_l[8];
+  __shared__ __align__(16) float c_acc[8][D];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.z, h = blockIdx.y;
+  const uint32_t C = cl_size(), rank = cl_rank();
+  const bool append = p.k_new != nullptr;
+  const int len = p.seq_len[b] + (append ? 1 : 0);
+  const int lo = (int)((int64_t)rank * len / C), hi = (int)((int64_t)(rank + 1) * len / C);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStg; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();          // the next layer's CTAs may start their prologue (no workspace is shared)
+  const int64_t row0 = (int64_t)b * p.rows_per_b;
+
+  if (warp == kCW) {
+    // ================= producer
+    if (append && hi == len && hi > lo) {
+      // appended key -> cache row len-1 (head h's 256 bytes of K and V), then TMA may read it
+      const int64_t dst = (row0 + len - 1) * p.hkv * D + (int64_t)h * D;
+      const int64_t src = ((int64_t)b * p.hkv + h) * D;
+      for (int e = lane; e < D / 8; e += 32) {
+        reinterpret_cast<uint4*>(p.k + dst)[e] = reinterpret_cast<const uint4*>(p.k_new + src)[e];
+        reinterpret_cast<uint4*>(p.v + dst)[e] = reinterpret_cast<const uint4*>(p.v_new + src)[e];
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int t = 0;
+      for (int j0 = lo; j0 < hi; j0 += kTK, ++t) {
+        const int s = t % kStg;
+        const int nk = min(kTK, hi - j0);
+        const int ng = (nk + kBoxRows - 1) / kBoxRows;
+        if (t >= kStg) mbar_wait(&empty[s], ((t / kStg) - 1) & 1);
+        mbar_expect_tx(&full[s], (unsigned)(2 * ng * NH * kBoxBytes));
+        const int r = (int)(row0 + j0);
+        for (int hf = 0; hf < NH; ++hf) {
+          const uint32_t kd = smem_u32(kst + s * OP) + hf * T::HALF, vd = smem_u32(vst + s * OP) + hf * T::HALF;
+          if (nk == kTK) {
+            tma_box(kd, &kmap, h * D + hf * 64, r, &full[s], pol);
+            tma_box(vd, &vmap, h * D + hf * 64, r, &full[s], pol);
+          } else {
+            for (int w = 0; w < ng; ++w) {
+              tma_box(kd + w * kBoxBytes, &kmap16, h * D + hf * 64, r + w * kBoxRows, &full[s], pol);
+              tma_box(vd + w * kBoxBytes, &vmap16, h * D + hf * 64, r + w * kBoxRows, &full[s], pol);
+            }
+          }
+        }
+      }
+    }
+    pdl_wait();   // this warp also writes outputs in the cluster merge
+  } else {
+    // ================= consumers
+    pdl_wait();   // q and out belong to the previous kernels until here
+    const int g = lane >> 2, c = lane & 3;
+    uint32_t qa[KC][4];
+    {
+      const bool real = g < G;
+      const float* qp = p.q + ((int64_t)b * p.hq + h * G + (real ? g : 0)) * D;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        const float2 lo2 = *reinterpret_cast<const float2*>(qp + 16 * kc + 2 * c);
+        const float2 hi2 = *reinterpret_cast<const float2*>(qp + 16 * kc + 2 * c + 8);
+        float x[4];
+        x[0] = real ? lo2.x * p.scale_log2 : 0.f;
+        x[1] = real ? lo2.y * p.scale_log2 : 0.f;
+        x[2] = real ? hi2.x * p.scale_log2 : 0.f;
+        x[3] = real ? hi2.y * p.scale_log2 : 0.f;
+        const float h0 = bf16_round(x[0]), h1 = bf16_round(x[1]), h2 = bf16_round(x[2]), h3 = bf16_round(x[3]);
+        qa[kc][0] = pack_bf16(h0, h1);
+        qa[kc][1] = pack_bf16(x[0] - h0, x[1] - h1);
+        qa[kc][2] = pack_bf16(h2, h3);
+        qa[kc][3] = pack_bf16(x[2] - h2, x[3] - h3);
+      }
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    float m = -INFINITY, lsum = 0.f;
+    int t = 0;
+    for (int j0 = lo; j0 < hi; j0 += kTK, ++t) {
+      const int s = t % kStg;
+      const int nkw = min(kBoxRows, max(0, min(kTK, hi - j0) - kBoxRows * warp));
+      mbar_wait(&full[s], (t / kStg) & 1);
+      if (nkw > 0) {
+        const uint8_t* kb = kst + s * OP;
+        uint8_t* vb = vst + s * OP;
+        if (nkw < kBoxRows) {   // rows past the slice are other keys (or unwritten rows): zero their V
+          for (int e = lane; e < (kBoxRows - nkw) * (D / 8); e += 32) {
+            const int r = nkw + e / (D / 8), c8 = e % (D / 8);
+            *reinterpret_cast<uint4*>(vb + T::off(warp, r, c8)) = make_uint4(0, 0, 0, 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+        }
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < KC / 2; ++kk) {
+          uint32_t r[4];
+          const int c8 = 4 * kk + (lane >> 3);
+          ldmatrix_x4(r, kb + T::off(warp, lane & 7, c8));
+          mma_bf16_16816(s0, qa[2 * kk], r[0], r[1]);
+          mma_bf16_16816(s0, qa[2 * kk + 1], r[2], r[3]);
+          ldmatrix_x4(r, kb + T::off(warp, 8 + (lane & 7), c8));
+          mma_bf16_16816(s1, qa[2 * kk], r[0], r[1]);
+          mma_bf16_16816(s1, qa[2 * kk + 1], r[2], r[3]);
+        }
+        float sc[4];
+        sc[0] = (2 * c < nkw) ? s0[0] + s0[2] : -INFINITY;
+        sc[1] = (2 * c + 1 < nkw) ? s0[1] + s0[3] : -INFINITY;
+        sc[2] = (2 * c + 8 < nkw) ? s1[0] + s1[2] : -INFINITY;
+        sc[3] = (2 * c + 9 < nkw) ? s1[1] + s1[3] : -INFINITY;
+        float tmax = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        const bool grow = tmax > m + 8.f || (m == -INFINITY && tmax != -INFINITY);
+        if (__any_sync(0xffffffffu, grow)) {
+          const float m_new = grow ? tmax : m;
+          const float corr = (m == -INFINITY) ? 0.f : fast_exp2(m - m_new);
+          m = m_new;
+          lsum *= corr;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            o[nt][0] *= corr; o[nt][1] *= corr; o[nt][2] *= corr; o[nt][3] *= corr;
+          }
+        }
+        const float mu = (m == -INFINITY) ? 0.f : m;
+        float pr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pr[i] = fast_exp2(sc[i] - mu);
+        lsum += (pr[0] + pr[1]) + (pr[2] + pr[3]);
+        uint32_t pa[4];
+        {
+          const float h0 = bf16_round(pr[0]), h1 = bf16_round(pr[1]), h2 = bf16_round(pr[2]), h3 = bf16_round(pr[3]);
+          pa[0] = pack_bf16(h0, h1);
+          pa[1] = pack_bf16(pr[0] - h0, pr[1] - h1);
+          pa[2] = pack_bf16(h2, h3);
+          pa[3] = pack_bf16(pr[2] - h2, pr[3] - h3);
+        }
+#pragma unroll
+        for (int jj = 0; jj < NT / 2; ++jj) {
+          uint32_t r[4];
+          ldmatrix_x4_trans(r, vb + T::off(warp, (lane & 7) + 8 * ((lane >> 3) & 1), 2 * jj + (lane >> 4)));
+          mma_bf16_16816(o[2 * jj], pa, r[0], r[1]);
+          mma_bf16_16816(o[2 * jj + 1], pa, r[2], r[3]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    // ---- warps -> CTA partial; every TMA has landed (all tiles were waited), so
+    // the K ring is free for the per-warp partials after the consumer barrier
+    csync();
+    float* wm = reinterpret_cast<float*>(kst);            // [kCW][8]
+    float* wl = wm + kCW * 8;                              // [kCW][8]
+    float* wacc = wl + kCW * 8;                            // [kCW][8][D]
+    if (g < G) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        *reinterpret_cast<float2*>(wacc + (warp * 8 + g) * D + 8 * nt + 2 * c) =
+            make_float2(o[nt][0] + o[nt][2], o[nt][1] + o[nt][3]);
+      if (c == 0) {
+        wm[warp * 8 + g] = m;
+        wl[warp * 8 + g] = lsum;
+      }
+    }
+    csync();
+    for (int e = threadIdx.x; e < G * D; e += kCW * 32) {
+      const int gg = e / D, dd = e % D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kCW; ++w) M = fmaxf(M, wm[w * 8 + gg]);
+      const float mu = (M == -INFINITY) ? 0.f : M;
+      float L = 0.f, A = 0.f;
+#pragma unroll
+      for (int w = 0; w < kCW; ++w) {
+        const float sc = fast_exp2(wm[w * 8 + gg] - mu);
+        L += wl[w * 8 + gg] * sc;
+        A += wacc[(w * 8 + gg) * D + dd] * sc;
+      }
+      c_acc[gg][dd] = A;
+      if (dd == 0) {
+        c_m[gg] = M;
+        c_l[gg] = L;
+      }
+    }
+  }
+  // ---- cluster merge: CTA rank r finalises outputs e = r, r + C, ... of the G*D
+  __syncwarp();
+  cl_sync();
+  for (int e = rank * kThreads + threadIdx.x; e < G * D; e += C * kThreads) {
+    const int gg = e / D, dd = e % D;
+    float M = -INFINITY;
+    for (uint32_t q = 0; q < C; ++q) M = fmaxf(M, ld_cluster(cl_map(&c_m[gg], q)));
+    const float mu = (M == -INFINITY) ? 0.f : M;
+    float L = 0.f, A = 0.f;
+    for (uint32_t q = 0; q < C; ++q) {
+      const float sc = fast_exp2(ld_cluster(cl_map(&c_m[gg], q)) - mu);
+      L += ld_cluster(cl_map(&c_l[gg], q)) * sc;
+      A += ld_cluster(cl_map(&c_acc[gg][dd], q)) * sc;
+    }
+    p.out[((int64_t)b * p.hq + h * G + gg) * D + dd] = A / L;
+  }
+  __syncwarp();
+  cl_sync();      // peers may still be reading this CTA's partial
+}
+
+int g_max_clusters[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};   // by cluster size
+
+template <int D, int G>
+cudaError_t configure(int C) {
+  auto kern = decode_cluster_kernel<D, G>;
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTile<D>::smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  (void)C;
+  return cudaSuccess;
+}
+
+template <int D, int G>
+cudaError_t launch(int C, int B, int hkv, const CUtensorMap* m, const ClusterParams& p, cudaStream_t st) {
+  cudaError_t e = configure<D, G>(C);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(C, hkv, B);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = CTile<D>::smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, decode_cluster_kernel<D, G>, m[0], m[1], m[2], m[3], p);
+}
+
+template <int D>
+cudaError_t launch_by_g(int G, int C, int B, int hkv, const CUtensorMap* m, const ClusterParams& p,
+                        cudaStream_t st) {
+  switch (G) {
+    case 1: return launch<D, 1>(C, B, hkv, m, p, st);
+    case 2: return launch<D, 2>(C, B, hkv, m, p, st);
+    case 4: return launch<D, 4>(C, B, hkv, m, p, st);
+    case 7: return launch<D, 7>(C, B, hkv, m, p, st);
+    case 8: return launch<D, 8>(C, B, hkv, m, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int max_clusters(int C) {
+  const int i = C;
+  if (g_max_clusters[i] < 0) {
+    if (configure<128, 4>(C) != cudaSuccess) return g_max_clusters[i] = 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(C, 1, 1);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = CTile<128>::smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel<128, 4>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    g_max_clusters[i] = n;
+    if (std::getenv("RK_DECODE_CLUSTER_VERBOSE")) std::fprintf(stderr, "[rk] cluster %d: %d co-resident\n", C, n);
+  }
+  return g_max_clusters[i];
+}
+
+}  // namespace
+
+// cluster size for (batch, kv-heads, longest dialogue); 0 = use the persistent
+// split-K kernel.  Applies when every (dialogue, kv-head) pair gets >= 1 CTA
+// in one wave; C = the largest of 16/12/8/6/4/3/2/1 that fits the SMs with
+// >= 64 keys per CTA and whose clusters are all co-resident (B200, 1 CTA/SM:
+// 7 clusters of 16 or 12, 15 of 8, 22 of 6, 33 of 4 — so one dialogue with 8
+// kv-heads runs 8 x 8 CTAs).  Slices follow each dialogue's own length, so a batch whose lengths
+// differ widely runs at the pace of its longest dialogue (the persistent
+// kernel balances keys across SMs instead).  RK_DECODE_CLUSTER=0 disables
+// (A/B runs, tests of the persistent kernel).
+int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = std::getenv("RK_DECODE_CLUSTER");
+    mode = e ? std::atoi(e) : 1;
+  }
+  if (mode == 0 || kv_dtype != RK_BF16 || (d != 128 && d != 64)) return 0;
+  if (!(G == 1 || G == 2 || G == 4 || G == 7 || G == 8)) return 0;
+  const int64_t row = (int64_t)hkv * d;
+  if (batch > 1 && (batch_stride % row != 0 || batch_stride <= 0)) return 0;
+  static int cmax = -1;        // RK_DECODE_CLUSTER_CMAX caps the cluster size (experiments)
+  if (cmax < 0) {
+    const char* e = std::getenv("RK_DECODE_CLUSTER_CMAX");
+    cmax = e ? std::atoi(e) : 16;
+  }
+  const int pairs = batch * hkv;
+  for (int C : {16, 12, 8, 6, 4, 3, 2, 1}) {
+    if (C > cmax) continue;
+    if ((int64_t)pairs * C > sm_count()) continue;
+    if (C > 1 && max_len / C < 64) continue;          // >= 64 keys per CTA
+    if (max_clusters(C) < pairs) continue;             // one co-resident wave
+    return C;
+  }
+  return 0;
+}
+
+int launch_decode_cluster(int C, const float* q, int batch, int hq, int d, void* k_cache, void* v_cache, int hkv,
+                          int64_t batch_stride, const int32_t* seq_len, int max_len, const void* k_new,
+                          const void* v_new, float* out, cudaStream_t st) {
+  const int64_t row = (int64_t)hkv * d;
+  const int64_t rows_per_b = batch > 1 ? batch_stride / row : (int64_t)max_len;   // max_len bounds seq_len+1
+  const uint64_t rows = (uint64_t)rows_per_b * batch;
+  CUtensorMap m[4];   // K, V whole-stage boxes; K, V 16-key boxes
+  int r = 0;
+  for (int i = 0; i < 4 && !r; ++i)
+    r = tc::make_map(&m[i], (i & 1) ? v_cache : k_cache, (uint64_t)row, rows, (uint64_t)row * 2,
+                     i < 2 ? kTK : kBoxRows);
+  if (r) return r;
+  ClusterParams p{};
+  p.q = q;
+  p.k = static_cast<__nv_bfloat16*>(k_cache);
+  p.v = static_cast<__nv_bfloat16*>(v_cache);
+  p.rows_per_b = rows_per_b;
+  p.seq_len = seq_len;
+  p.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  p.hq = hq;
+  p.hkv = hkv;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  p.out = out;
+  const int G = hq / hkv;
+  cudaError_t e = d == 128 ? launch_by_g<128>(G, C, batch, hkv, m, p, st) : launch_by_g<64>(G, C, batch, hkv, m, p, st);
+  if (e != cudaSuccess) return cuda_status(e, "decode_cluster_kernel launch");
+  return RK_OK;
+}
+
+}  // namespace rk

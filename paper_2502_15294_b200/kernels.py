@@ -57,6 +57,15 @@ def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tens
     return out
 
 
+def decode_plan(batch: int, hq: int, hkv: int, d: int, kv_dtype: torch.dtype, max_seq_len: int,
+                cache_stride: int = 0, has_items: bool = False) -> int:
+    """rk_decode_plan: C > 0 = cluster decode with C CTAs per (dialogue, kv-head),
+    0 = persistent split-K + merge, -1 = generic split kernel."""
+    code = _lib.RK_BF16 if kv_dtype == torch.bfloat16 else _lib.RK_F32
+    return int(_lib.lib.rk_decode_plan(batch, hq, hkv, d, code, int(max_seq_len), int(cache_stride),
+                                         int(has_items)))
+
+
 def decode_scores_finalize(batch: int, hq: int, hkv: int, d: int, items: torch.Tensor, n_items: torch.Tensor,
                            n_bins: int, ws: torch.Tensor, active=None, raw: torch.Tensor | None = None,
                            kv_dtype: torch.dtype = torch.bfloat16, stream=None) -> torch.Tensor:

@@ -39,20 +39,29 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       ::"r"(sa(dst)), "l"(map), "r"(c0), "r"(c1), "r"(sa(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(sa(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(sa(bar))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(bar))
                : "memory");
 }
 
-constexpr int STAGES = 8;
+constexpr int STAGES = 6;   // 192 KB in flight (the cluster decode ring: 3 stages x K+V 32 KB)
 
+// mode 2: 3-D boxes {64, box_rows, 2} (dims: 64 elems, keys, 64-elem column
+//         blocks; both halves of a kv-head in one instruction) x boxes_per_tile;
 // mode 0: tensor boxes {64, box_rows} x boxes_per_tile (column offsets 64*i);
 // mode 1: bulk copies of `span` contiguous bytes x boxes_per_tile
 __global__ void probe(const __grid_constant__ CUtensorMap map, const uint8_t* base, int mode, int box_rows,
                       int boxes_per_tile, int span, int tiles, int keys, int row_bytes) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int tile_bytes = mode == 0 ? boxes_per_tile * box_rows * 128 : boxes_per_tile * span;
+  const int tile_bytes = mode == 0 ? boxes_per_tile * box_rows * 128
+                       : mode == 2 ? boxes_per_tile * box_rows * 256 : boxes_per_tile * span;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * tile_bytes);
   uint64_t* empty = full + STAGES;
   if (threadIdx.x == 0) {
@@ -63,7 +72,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const uint8_t* ba
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int rows_per_tile = mode == 0 ? box_rows : 0;
+  const int rows_per_tile = mode != 1 ? box_rows : 0;
   if (threadIdx.x == 0) {
     for (int t = 0; t < tiles; ++t) {
       const int s = t % STAGES;
@@ -71,8 +80,18 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const uint8_t* ba
       bar_expect(&full[s], tile_bytes);
       uint8_t* dst = smem + s * tile_bytes;
       if (mode == 0) {
-        const int row0 = (int)(((int64_t)(blockIdx.x * 7919 + t) * rows_per_tile) % (keys - rows_per_tile));
-        for (int i = 0; i < boxes_per_tile; ++i) tma_2d(dst + i * box_rows * 128, &map, 64 * i, row0, &full[s]);
+        // head-slice pattern of the cluster decode: this CTA's kv-head (128 of the row's
+        // 1024 elements) as two 64-column boxes per key group, consecutive key groups
+        const int span = rows_per_tile * boxes_per_tile / 2;
+        const int row0 = (int)(((int64_t)(blockIdx.x / 8 * 7919 + t) * span) % (keys - span));
+        const int col = (blockIdx.x % 8) * 128;
+        for (int i = 0; i < boxes_per_tile; ++i)
+          tma_2d(dst + i * box_rows * 128, &map, col + 64 * (i & 1), row0 + (i >> 1) * box_rows, &full[s]);
+      } else if (mode == 2) {
+        const int span = rows_per_tile * boxes_per_tile;
+        const int row0 = (int)(((int64_t)(blockIdx.x / 8 * 7919 + t) * span) % (keys - span));
+        for (int i = 0; i < boxes_per_tile; ++i)
+          tma_3d(dst + i * box_rows * 256, &map, 0, row0 + i * box_rows, 2 * (blockIdx.x % 8), &full[s]);
       } else {
         const int64_t off = ((int64_t)(blockIdx.x * 7919 + t) * tile_bytes) % ((int64_t)keys * row_bytes - tile_bytes);
         for (int i = 0; i < boxes_per_tile; ++i) bulk_1d(dst + i * span, base + (off & ~15ll) + i * span, span, &full[s]);
@@ -89,7 +108,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const uint8_t* ba
 }
 
 int main() {
-  const int keys = 66048, row_elems = 512;   // [keys][4 heads x 128] bf16, as C3's K
+  const int keys = 66048, row_elems = 1024;  // [keys][8 heads x 128] bf16, as C2's K
   const int row_bytes = row_elems * 2;
   uint8_t* dev;
   cudaMalloc(&dev, (size_t)keys * row_bytes);
@@ -102,41 +121,60 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   struct Cfg { int mode, box_rows, boxes, span; const char* name; };
   std::vector<Cfg> cfgs = {
-      {0, 64, 2, 0, "tensor box {64,64} x2 (prefill K tile, 16 KB)"},
+      {0, 16, 16, 0, "tensor box {64,16} x16 (32 KB; cluster decode)"},
+      {0, 32, 8, 0, "tensor box {64,32} x8 (32 KB)"},
       {0, 64, 4, 0, "tensor box {64,64} x4 (32 KB)"},
-      {0, 128, 2, 0, "tensor box {64,128} x2 (score_tc K tile, 32 KB)"},
-      {0, 256, 2, 0, "tensor box {64,256} x2 (64 KB)"},
-      {1, 0, 1, 16384, "bulk 16 KB contiguous"},
-      {1, 0, 16, 1024, "bulk 16 x 1 KB rows"},
-      {1, 0, 64, 256, "bulk 64 x 256 B"},
+      {0, 128, 2, 0, "tensor box {64,128} x2 (32 KB)"},
+      {0, 256, 1, 0, "tensor box {64,256} x1 (32 KB)"},
+      {2, 64, 2, 0, "3d box {64,64,2} x2 (32 KB)"},
+      {2, 128, 1, 0, "3d box {64,128,2} x1 (32 KB; cluster decode stage)"},
+      {2, 16, 8, 0, "3d box {64,16,2} x8 (32 KB)"},
+      {1, 0, 8, 4096, "bulk 8 x 4 KB"},
+      {1, 0, 32, 1024, "bulk 32 x 1 KB rows"},
+      {1, 0, 128, 256, "bulk 128 x 256 B"},
   };
+  const int grids[2] = {sms, 128};
+  for (int gi = 0; gi < 2; ++gi)
   for (auto& c : cfgs) {
+    const int grid = grids[gi];
     CUtensorMap map;
-    cuuint64_t dims[2] = {(cuuint64_t)row_elems, (cuuint64_t)keys};
-    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
-    cuuint32_t box[2] = {64, (cuuint32_t)(c.box_rows ? c.box_rows : 64)};
-    cuuint32_t estr[2] = {1, 1};
-    enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dev, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    const int tile_bytes = c.mode == 0 ? c.boxes * c.box_rows * 128 : c.boxes * c.span;
+    CUresult er;
+    if (c.mode == 2) {   // dims {64 elems, keys, column blocks}: strides {row, 128 B} (not monotonic)
+      cuuint64_t dims[3] = {64, (cuuint64_t)keys, (cuuint64_t)(row_elems / 64)};
+      cuuint64_t strides[2] = {(cuuint64_t)row_bytes, 128};
+      cuuint32_t box[3] = {64, (cuuint32_t)c.box_rows, 2};
+      cuuint32_t estr[3] = {1, 1, 1};
+      er = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, dev, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      cuuint64_t dims[2] = {(cuuint64_t)row_elems, (cuuint64_t)keys};
+      cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+      cuuint32_t box[2] = {64, (cuuint32_t)(c.box_rows ? c.box_rows : 64)};
+      cuuint32_t estr[2] = {1, 1};
+      er = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dev, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (er != CUDA_SUCCESS) { printf("%-50s encode failed (%d)\n", c.name, (int)er); continue; }
+    const int tile_bytes = c.mode == 0 ? c.boxes * c.box_rows * 128
+                         : c.mode == 2 ? c.boxes * c.box_rows * 256 : c.boxes * c.span;
     const size_t smem = (size_t)STAGES * tile_bytes + 256;
     if (smem > 232448) { printf("%-50s skip (smem)\n", c.name); continue; }
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int tiles = (int)(((size_t)2 << 30) / sms / tile_bytes);     // ~2 GB total
+    const int tiles = (int)(((size_t)2 << 30) / grid / tile_bytes);     // ~2 GB total
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
-      probe<<<sms, 64, smem>>>(map, dev, c.mode, c.box_rows, c.boxes, c.span, tiles, keys, row_bytes);
+      probe<<<grid, 64, smem>>>(map, dev, c.mode, c.box_rows, c.boxes, c.span, tiles, keys, row_bytes);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
     }
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double bytes = (double)sms * tiles * tile_bytes;
-    printf("%-50s %8.1f GB/s  (%.1f B/clk/SM @1.9GHz)  err=%s\n", c.name, bytes / ms / 1e6,
-           bytes / ms / 1e6 / sms / 1.9, cudaGetErrorString(cudaGetLastError()));
+    const double bytes = (double)grid * tiles * tile_bytes;
+    printf("grid %3d %-46s %8.1f GB/s  (%.1f B/clk/SM @1.9GHz)  err=%s\n", grid, c.name, bytes / ms / 1e6,
+           bytes / ms / 1e6 / grid / 1.9, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
