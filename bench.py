@@ -232,10 +232,10 @@ def main():
                "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out),
                "ms_per_step": ms_e / args.steps, "breakdown_ms_group0": brk_e}
 
-    # roofline of the dominant kernel (bulk decode + merge) from the timed turns:
+    # roofline of the dominant kernel (the decode attention) from the timed turns:
     # decode-loop time per token vs algorithmic KV bytes per token
     peak, peak_kind = measured_peaks()
-    # decode kernels (bulk decode + merge) of all groups: algorithmic KV bytes of
+    # decode kernels of all groups: algorithmic KV bytes of
     # every timed decode token / the union of the decode-loop intervals on the
     # device timeline (CUDA events on each group's compute stream)
     bytes_tok = eng.kv_bytes_per_token()
@@ -271,8 +271,8 @@ def main():
                    "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "rk decode attention (decode_mma + merge): KV bytes of every timed decode token / "
-                                                "union of the groups' decode-loop intervals (CUDA events)",
+                     "traffic": traffic, "kernel": f"rk decode attention ({eng.decode_kernel_desc()}): KV bytes of every timed decode "
+                                                "token / union of the groups' decode-loop intervals (CUDA events)",
                      "decode_busy_ms": dec_busy_ms, "launches": dec_launches,
                      "whole_step_GBps": step_bw, "whole_step_frac": step_bw / peak,
                      "bytes_per_token": bytes_tok, "peak_source": peak_kind},

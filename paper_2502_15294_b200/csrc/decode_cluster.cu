@@ -460,8 +460,12 @@ int launch_decode_cluster(int C, const float* q, int batch, int hq, int d, void*
                           int64_t batch_stride, const int32_t* seq_len, int max_len, const void* k_new,
                           const void* v_new, float* out, cudaStream_t st) {
   const int64_t row = (int64_t)hkv * d;
-  const int64_t rows_per_b = batch > 1 ? batch_stride / row : (int64_t)max_len;   // max_len bounds seq_len+1
-  const uint64_t rows = (uint64_t)rows_per_b * batch;
+  const int64_t rows_per_b = batch > 1 ? batch_stride / row : (int64_t)max_len;
+  // the map ends at the last dialogue's max_len-th row (max_len bounds seq_len+1
+  // and the capacity): the 16-key tail boxes of a slice may run up to 15 rows
+  // past a dialogue's length — inside the next dialogue's rows (masked), or
+  // past the map's end, where TMA fills zeros instead of reading unowned memory
+  const uint64_t rows = (uint64_t)rows_per_b * (batch - 1) + (uint64_t)max_len;
   CUtensorMap m[4];   // K, V whole-stage boxes; K, V 16-key boxes
   int r = 0;
   for (int i = 0; i < 4 && !r; ++i)

@@ -236,8 +236,36 @@ class RoundDecodeEngine:
                                  out=(self.out if out is None else out)[l], ws=self.ws,
                                  advance=ln if advance else None)
 
-    def launches_per_layer(self) -> int:
-        return 2                                            # decode + merge
+    def _layer_launches(self, l: int, advance: bool = False, items: bool = False) -> int:
+        """Kernels one _layer call launches (rk_decode_plan): the cluster decode
+        is one kernel (+ the length advance), the persistent split-K decode is
+        decode + merge (the merge advances the lengths)."""
+        c = self.cfg
+        kc, cap = (self.lower[:, l, 0], self.s_lo) if l < c.watershed else (self.upper[:, l - c.watershed, 0], self.s_up)
+        plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0), items)
+        return (1 + int(advance)) if plan > 0 else 2
+
+    def decode_kernel_desc(self) -> str:
+        """The decode kernels the answer tokens run (lower / upper layers)."""
+        c = self.cfg
+        out = []
+        for name, kc, cap in (("lower", self.lower[:, 0, 0], self.s_lo), ("upper", self.upper[:, 0, 0], self.s_up)):
+            plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0))
+            out.append(f"{name}: " + (f"decode_cluster_kernel, {plan} CTA(s) per (dialogue, kv-head)" if plan > 0
+                                      else "decode_mma_kernel + decode_merge_kernel"))
+        return "; ".join(out)
+
+    def launches_per_token(self) -> int:
+        """Kernels of one answer token through all layers (as _phase_b2)."""
+        c = self.cfg
+        return sum(self._layer_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
+                   for l in range(c.num_layers))
+
+    def launches_question_token(self) -> int:
+        """Kernels of the 1-row question token (_phase_a + _phase_b1)."""
+        c = self.cfg
+        return sum(self._layer_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1),
+                                        items=(l == c.watershed - 1)) for l in range(c.num_layers))
 
     def _phase_a(self):
         """Question through the lower layers, fused scoring, selection."""
@@ -567,10 +595,10 @@ class RoundDecodeEngine:
 
     def kernel_launches_per_turn(self) -> int:
         c = self.cfg
-        per_layer = 2                                   # bulk decode + merge
+        answer = self.launches_per_token() * c.decode_steps
         if self.nq > 1:   # prefill per (layer, dialogue): bad-row fill, q prep, tcgen05 pass, merge (+2 scoring)
-            return (c.num_layers * c.batch * 4 + 2 * c.batch + c.num_layers * per_layer * c.decode_steps + 1)
-        return (c.num_layers * per_layer * self.turn_tokens   # question token + answer tokens
+            return c.num_layers * c.batch * 4 + 2 * c.batch + answer + 1
+        return (self.launches_question_token() + answer
                 + 2)                                    # score finalize + batched select
 
     # ------------------------------------------------------------------ accounting
@@ -669,8 +697,7 @@ class GroupedDecoder:
             busy += cur1 - cur0
         self.last_decode_busy_ms = busy
         self.last_decode_bytes = turns * sum(e.cfg.decode_steps * e.kv_bytes_per_token() for e in self.groups)
-        self.last_decode_launches = turns * sum(e.cfg.num_layers * e.launches_per_layer() * e.cfg.decode_steps
-                                                for e in self.groups)
+        self.last_decode_launches = turns * sum(e.launches_per_token() * e.cfg.decode_steps for e in self.groups)
         for eng in self.groups:
             eng.window_log = None
         return ms, sum(h2d) // max(turns, 1), self.groups[0].turn_breakdown_ms(), self.groups[0].last_kept
@@ -689,3 +716,6 @@ class GroupedDecoder:
 
     def kernel_launches_per_turn(self):
         return sum(e.kernel_launches_per_turn() for e in self.groups)
+
+    def decode_kernel_desc(self):
+        return self.groups[0].decode_kernel_desc()

@@ -134,3 +134,28 @@ def test_persistent_split_k_at_small_batches_subprocess():
     env = dict(os.environ, RK_DECODE_CLUSTER="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_cluster_decode_on_engine_layer_views_at_capacity():
+    """Caches as the engine holds them: layer l's K / V are strided views of one
+    [B][L][2][S][Hkv][d] tensor (dialogue stride = L*2*S rows), every dialogue
+    filled to capacity by the appended row — the last view ends at the end of
+    the allocation, so no tail box may read past it."""
+    B, L, S, hkv, G, d = 4, 3, 1500, 4, 7, 128
+    big = torch.randn(B, L, 2, S, hkv, d, device="cuda").bfloat16()
+    q = torch.randn(B, hkv * G, d, device="cuda")
+    kn = torch.randn(B, hkv, d, device="cuda").bfloat16()
+    vn = torch.randn(B, hkv, d, device="cuda").bfloat16()
+    for layer in range(L):
+        kc, vc = big[:, layer, 0], big[:, layer, 1]
+        sl = torch.tensor([S - 1, S - 700, S - 1, S - 30], dtype=torch.int32, device="cuda")
+        assert kernels.decode_plan(B, hkv * G, hkv, d, torch.bfloat16, S, kc.stride(0)) > 0
+        out = kernels.decode_attention(q, kc, vc, sl, S, k_new=kn, v_new=vn)
+        torch.cuda.synchronize()
+        for b in range(B):
+            n = int(sl[b]) + 1
+            kk = kc[b, :n].float().cpu().numpy()
+            vv = vc[b, :n].float().cpu().numpy()
+            ref, _ = oatt.attention_forward_gqa(q[b:b + 1].cpu().numpy(), kk, vv, [n - 1], np.arange(n))
+            err = np.abs(out[b].reshape(1, -1).cpu().numpy() - ref).max() / np.abs(ref).max()
+            assert err < 2e-5, (layer, b, err)

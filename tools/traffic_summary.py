@@ -24,7 +24,9 @@ data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(h
 agg = collections.defaultdict(float)
 unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 for d in data:
-    name = "decode_mma" if "decode_mma" in d["Kernel Name"] else "merge" if "merge" in d["Kernel Name"] else None
+    kn = d["Kernel Name"]
+    name = ("decode_mma" if "decode_mma" in kn else "decode_cluster" if "decode_cluster" in kn
+            else "merge" if "merge" in kn else None)
     if name is None:
         continue
     v = float(d["Metric Value"].replace(",", "")) * unit.get(d["Metric Unit"], 1)
