@@ -74,7 +74,6 @@ constexpr int XCH_BYTES = (2 * 256 + 3 * 128) * 4;  // row-max exchange (2 tiles
 constexpr size_t SMEM = 1024 + Q_BYTES + STAGES * (K_STAGE + V_STAGE) + BAR_BYTES + XCH_BYTES;
 constexpr uint32_t TMEM_COLS = 512;      // S/P buffers NB x 128 at 0.., O (128) at NB * 128 (= 384)
 constexpr float TAU = 8.f;               // lazy rescale threshold (log2 units)
-constexpr float FALLBACK = 100.f;        // item statistics recomputed when keys sit this far below m
 
 constexpr uint32_t kIdescQK = idesc_f16(PM, BN);             // S[256 x 128] = Q K^T (both K-major, smem)
 constexpr uint32_t kIdescPV = idesc_f16(PM, D, true);        // O[256 x 128] += P V (P from TMEM, V MN-major)
@@ -694,15 +693,21 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           }
           const float rs = acc2.x + acc2.y;
           l_half = (rescale ? l_half * fac : l_half) + rs;
-          // ---- per-item scoring statistics (exact (m, l) pair of this half's keys)
+          // ---- per-item scoring statistics: this half's tile-local (max, sum), recomputed
+          // from S instead of rescaling rs (which is relative to the running max m_run and
+          // so depends on the keys before the item): identical rounds then get bit-identical
+          // masses wherever they sit in a unit, and exact ties resolve to the lower index
+          // as the reference's stable argsort does (tests/test_gpu_selection_variants.py)
           if (p.item_m && hmax != -INFINITY) {
-            float tm = mu, tl = rs;
-            if (hmax < mu - FALLBACK) {        // keys far below the reference: recompute exactly
-              tm = hmax;
-              tl = 0.f;
+            const float tm = hmax;
+            float2 t2 = make_float2(0.f, 0.f);
+            const float2 nh = make_float2(-hmax, -hmax);
 #pragma unroll
-              for (int i = 0; i < HK; ++i) tl += fast_exp2(sc[i] - hmax);
+            for (int i = 0; i < HK; i += 2) {
+              const float2 dlt = ffma2(make_float2(sc[i], sc[i + 1]), one, nh);
+              t2 = ffma2(make_float2(fast_exp2(dlt.x), fast_exp2(dlt.y)), one, t2);
             }
+            const float tl = t2.x + t2.y;
             if (m_it == -INFINITY) {
               m_it = tm;
               l_it = tl;
