@@ -165,3 +165,9 @@ def test_exact_ties_multirow_prefill_scoring():
     ref_kept = orr.select(orr.normalize(ref_raw), pol)
     assert ref_kept == (2, 9) and kept == ref_kept
     np.testing.assert_allclose(raw, ref_raw, rtol=2e-5, atol=1e-9)
+    # the scores-only form (rk_round_scores, the multi-row watershed scorer)
+    from paper_2502_15294_b200 import stats
+    raw2 = stats.round_scores(t(q), t(k).bfloat16(), qp, kp, bounds, n_r, chunk=1024).cpu().numpy()
+    assert raw2[2] == raw2[5] == raw2[13], raw2[[2, 5, 13]]
+    assert orr.select(orr.normalize(raw2), pol) == ref_kept
+    np.testing.assert_allclose(raw2, ref_raw, rtol=2e-5, atol=1e-9)
