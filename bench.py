@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--question-noise", type=float, default=None,
                     help="per-turn question variation (EngineConfig.question_noise)")
+    ap.add_argument("--input-period", type=int, default=None,
+                    help="per-token input slots (EngineConfig.input_period; e2e loads run P-2 tokens ahead)")
     ap.add_argument("--no-round-cache", action="store_true",
                     help="fetch every kept round every turn (the reference's transfer pattern)")
     ap.add_argument("--groups", type=int, default=None,
@@ -192,6 +194,8 @@ def main():
         w["round_cache"] = False
     if args.question_noise is not None:
         w["question_noise"] = args.question_noise
+    if args.input_period:
+        w["input_period"] = args.input_period
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)

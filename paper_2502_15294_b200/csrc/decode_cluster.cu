@@ -446,7 +446,7 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
     cmax = e ? std::atoi(e) : 16;
   }
   const int pairs = batch * hkv;
-  for (int C : {16, 12, 8, 6, 4, 3, 2, 1}) {
+  for (int C : {16, 12, 8, 6, 4, 3, 2, 1}) {   // 10 (11 co-resident) measured slower at B=1 upper layers
     if (C > cmax) continue;
     if ((int64_t)pairs * C > sm_count()) continue;
     if (C > 1 && max_len / C < 64) continue;          // >= 64 keys per CTA
