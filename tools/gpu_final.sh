@@ -3,5 +3,5 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; e
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 6000 -c 3000 --csv --log-file gpurun_out/launches_bench_c2.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --decode-steps 16 > gpurun_out/launches_bench.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 1500 -c 3000 --csv --log-file gpurun_out/launches_bench_c2.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --decode-steps 16 > gpurun_out/launches_bench.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json | cut -c1-400; cat gpurun_out/bench_ref.json | cut -c1-300; tail -2 gpurun_out/launches_bench.log
