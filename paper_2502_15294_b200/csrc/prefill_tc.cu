@@ -41,6 +41,7 @@
 //   warp 10    TMA producer of V [128 keys x 128] per tile (2-stage ring, freed
 //              after its PV).  All tiles SWIZZLE_128B.
 #include <cmath>
+#include <cstdlib>
 
 #include <algorithm>
 
@@ -895,7 +896,12 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
     pl.n_items = s > 0 ? (s + pl.item_keys - 1) / pl.item_keys : 1;
   }
   // ~8 units per SM: balance over the persistent CTAs, >= 1 item per chunk
-  const int target = 8 * (sm_count() / 2);                  // ~8 units per CTA pair
+  static int per_pair = -1;                                 // RK_PREFILL_UNITS overrides (experiments)
+  if (per_pair < 0) {
+    const char* e = std::getenv("RK_PREFILL_UNITS");
+    per_pair = e ? std::max(1, std::atoi(e)) : 8;
+  }
+  const int target = per_pair * (sm_count() / 2);           // units per CTA pair
   int nc = (target + mt_total - 1) / mt_total;
   nc = std::max(1, std::min(nc, pl.n_items));
   pl.items_per_chunk = (pl.n_items + nc - 1) / nc;
