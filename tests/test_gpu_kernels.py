@@ -182,7 +182,7 @@ def _rounds_layout(rng, n_rounds, lo=50, hi=400):
 
 @pytest.mark.parametrize("n_q,G,dtype", [(1, 4, torch.bfloat16), (7, 4, torch.float32), (33, 1, torch.float32),
                                          (5, 7, torch.bfloat16),
-                                         # >= 64 stacked rows, bf16, d=128: the tcgen05 scorer (score_tc.cu)
+                                         # >= 64 stacked rows, bf16, d=128: the tcgen05 scorer (scores-only prefill_tc.cu)
                                          (64, 4, torch.bfloat16), (100, 7, torch.bfloat16), (130, 1, torch.bfloat16)])
 def test_round_scores_vs_capture_aggregate(rng, n_q, G, dtype):
     n_rounds, hkv, d = 9, 2, 128

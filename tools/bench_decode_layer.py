@@ -1,4 +1,4 @@
-"""Per-call time of the decode attention (decode_mma + merge) on one layer
+"""Per-call time of the decode attention (rk_decode_attention: cluster decode, or persistent split-K + merge with RK_DECODE_CLUSTER=0) on one layer
 shape, replayed back to back from a CUDA graph (N dependent calls, as the
 layers of one decode token): separates the fixed per-layer cost from the
 bandwidth term at small batch.
