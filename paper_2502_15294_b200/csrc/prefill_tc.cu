@@ -906,6 +906,34 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
   nc = std::max(1, std::min(nc, pl.n_items));
   pl.items_per_chunk = (pl.n_items + nc - 1) / nc;
   pl.n_chunks = (pl.n_items + pl.items_per_chunk - 1) / pl.items_per_chunk;
+  static int balance = -1;                                  // RK_PREFILL_BALANCE=0: the plain target
+  if (balance < 0) {
+    const char* e = std::getenv("RK_PREFILL_BALANCE");
+    balance = e ? std::atoi(e) : 1;
+  }
+  if (balance) {
+    // units are dealt round-robin to the persistent pairs, so the pairs' time is
+    // ceil(units / pairs) units: pick the chunking (items per chunk) that minimises
+    // waves x (work per unit + a fixed per-unit cost), around the target count
+    // (C3, 56 M tiles x 11 chunks = 616 units = 8.3 waves on 74 pairs; 13 chunks:
+    // 728 units = 9.8 waves)
+    const int pairs = std::max(1, sm_count() / 2);
+    const double unit_cost = 0.03;                          // per unit, in whole-M-tile work (fitted: n_q 128..1024)
+    double best = 1e30;
+    for (int ipc = 1; ipc <= pl.n_items; ++ipc) {
+      const int ncks = (pl.n_items + ipc - 1) / ipc;
+      if (ipc > 1 && (pl.n_items + ipc - 2) / (ipc - 1) == ncks) continue;   // same chunk count, fewer items
+      const int64_t units = (int64_t)mt_total * ncks;
+      if (units > 4 * (int64_t)target) continue;
+      const int64_t waves = (units + pairs - 1) / pairs;
+      const double cost = (double)waves * (1.0 / ncks + unit_cost);
+      if (cost < best - 1e-12) {
+        best = cost;
+        pl.items_per_chunk = ipc;
+        pl.n_chunks = ncks;
+      }
+    }
+  }
   pl.n_units = mt_total * pl.n_chunks;
   pl.qs_bytes = align_up((size_t)hkv * 2 * pl.mpad * pf::D * 2, 256);
   const size_t rh = (size_t)n_q * hq;
