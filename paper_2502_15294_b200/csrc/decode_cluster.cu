@@ -18,9 +18,11 @@
 //               math is decode_mma's (mma.sync m16n8k16, q and P split into
 //               bf16 hi/lo rows so the products carry ~16 mantissa bits, lazy
 //               rescale), with swizzled ldmatrix addresses;
-//   epilogue    warps -> CTA partial in smem -> barrier.cluster -> CTA rank r
-//               merges its share of the (query head, dim) outputs from all C
-//               CTAs' partials (ld.shared::cluster) and writes them.
+//   epilogue    warps -> CTA partial, pushed with st.shared::cluster into the
+//               inbox of the CTA that finalises each (query head, dim) output
+//               (CTA rank r owns a contiguous 1/C of them) -> one
+//               barrier.cluster -> each CTA reduces its inbox locally and
+//               writes its outputs (no remote loads, no round trips).
 // The appended token (k_new/v_new) is written into the cache row len-1 by the
 // producer of the slice that owns it, before its TMA reads that row
 // (fence.proxy.async orders the generic stores before the async-proxy loads).
@@ -80,10 +82,14 @@ __device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
-__device__ __forceinline__ float ld_cluster(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
+__device__ __forceinline__ void st_cluster(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
                                         uint64_t pol) {
@@ -126,8 +132,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
   uint8_t* vst = smem + kStg * OP;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStg * OP);
   uint64_t* empty = full + kStg;
-  __shared__ float c_m[8], c_l[8];
-  __shared__ __align__(16) float c_acc[8][D];
+  // cluster merge inbox of this CTA: the outputs [rank*per, rank*per + per) it
+  // finalises, pushed by every CTA q of the cluster (row q), plus their (m, l)
+  __shared__ float in_acc[8 * D + 64];
+  __shared__ float in_m[16][8], in_l[16][8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.z, h = blockIdx.y;
@@ -143,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  cl_arrive();            // this CTA is running: peers may push into its inbox after their wait
   pdl_trigger();          // the next layer's CTAs may start their prologue (no workspace is shared)
   const int64_t row0 = (int64_t)b * p.rows_per_b;
 
@@ -302,6 +311,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
       }
     }
     csync();
+  }
+  // ---- cluster merge, push model: every CTA scatters its partial (m, l, acc) into
+  // the inbox of the CTA that finalises each output (remote stores do not wait for a
+  // round trip), one cluster barrier publishes them, each CTA reduces its inbox locally
+  const int per = ((G * D + (int)C - 1) / (int)C + 3) & ~3;      // outputs finalised per CTA
+  __syncwarp();
+  cl_wait();              // every peer has started (its inbox exists)
+  if (warp < kCW) {
+    const float* wm = reinterpret_cast<const float*>(kst);
+    const float* wl = wm + kCW * 8;
+    const float* wacc = wl + kCW * 8;
     for (int e = threadIdx.x; e < G * D; e += kCW * 32) {
       const int gg = e / D, dd = e % D;
       float M = -INFINITY;
@@ -315,31 +335,32 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
         L += wl[w * 8 + gg] * sc;
         A += wacc[(w * 8 + gg) * D + dd] * sc;
       }
-      c_acc[gg][dd] = A;
-      if (dd == 0) {
-        c_m[gg] = M;
-        c_l[gg] = L;
-      }
+      const int r = e / per;
+      st_cluster(cl_map(&in_acc[rank * per + (e - r * per)], r), A);
+      if (dd == 0)
+        for (uint32_t q = 0; q < C; ++q) {
+          st_cluster(cl_map(&in_m[rank][gg], q), M);
+          st_cluster(cl_map(&in_l[rank][gg], q), L);
+        }
     }
   }
-  // ---- cluster merge: CTA rank r finalises outputs e = r, r + C, ... of the G*D
   __syncwarp();
-  cl_sync();
-  for (int e = rank * kThreads + threadIdx.x; e < G * D; e += C * kThreads) {
+  cl_sync();              // release the pushes / acquire the peers'
+  for (int el = threadIdx.x; el < per; el += kThreads) {
+    const int e = (int)rank * per + el;
+    if (e >= G * D) break;
     const int gg = e / D, dd = e % D;
     float M = -INFINITY;
-    for (uint32_t q = 0; q < C; ++q) M = fmaxf(M, ld_cluster(cl_map(&c_m[gg], q)));
+    for (uint32_t q = 0; q < C; ++q) M = fmaxf(M, in_m[q][gg]);
     const float mu = (M == -INFINITY) ? 0.f : M;
     float L = 0.f, A = 0.f;
     for (uint32_t q = 0; q < C; ++q) {
-      const float sc = fast_exp2(ld_cluster(cl_map(&c_m[gg], q)) - mu);
-      L += ld_cluster(cl_map(&c_l[gg], q)) * sc;
-      A += ld_cluster(cl_map(&c_acc[gg][dd], q)) * sc;
+      const float sc = fast_exp2(in_m[q][gg] - mu);
+      L += in_l[q][gg] * sc;
+      A += in_acc[q * per + el] * sc;
     }
     p.out[((int64_t)b * p.hq + h * G + gg) * D + dd] = A / L;
   }
-  __syncwarp();
-  cl_sync();      // peers may still be reading this CTA's partial
 }
 
 int g_max_clusters[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};   // by cluster size
