@@ -117,6 +117,31 @@ __global__ void advance_kernel(int32_t* len, int n, int delta) {
   if (i < n) len[i] += delta;
 }
 
+// the same, launched as a programmatic dependent of a decode kernel: it becomes
+// resident while the decode runs and waits for its completion (every reader of
+// the lengths is done); it never triggers early, so the kernel after it starts
+// only once the lengths are advanced
+__global__ void advance_after_kernel(int32_t* len, int n, int delta) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) len[i] += delta;
+}
+
+static int advance_after(int32_t* len, int n, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((n + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, advance_after_kernel, len, n, 1);
+  if (e != cudaSuccess) return cuda_status(e, "advance_after_kernel launch");
+  return RK_OK;
+}
+
 // ---------------------------------------------------------------- score finalize
 // Per row: per head M_h, L_h over items; per bin mass = sum_h sum_items(bin)
 // l*exp2(m - M_h)/L_h (fp64); row sum over all bins (incl. current and
@@ -338,7 +363,7 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
       st = launch_decode_cluster(C, q, batch, hq, d, k_cache, v_cache, hkv, cache_stride, seq_len, max_seq_len,
                                  k_new, v_new, out, cs);
       if (st) return st;
-      if (advance_len) return rk_advance_lengths(advance_len, batch, 1, stream);
+      if (advance_len) return advance_after(advance_len, batch, cs);
       return RK_OK;
     }
   }
