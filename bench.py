@@ -124,6 +124,23 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def pcie_h2d_peak(torch, dev_index: int) -> float:
+    """Practical H2D peak of this GPU's link: a 256 MiB pinned copy."""
+    n = 256 << 20
+    src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev_index}")
+    best = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = max(best, n / (a.elapsed_time(b) / 1000.0) / 1e9)
+    del src, dst
+    return best
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -202,6 +219,7 @@ def main():
     groups = args.groups if args.groups else (2 if cfg.batch >= 2 and cfg.batch % 2 == 0 else 1)
     eng = GroupedDecoder(cfg, groups=groups, seed=1000 * shard[0])
     eng.prepare(e2e=not args.no_e2e)
+    link_peak = pcie_h2d_peak(torch, local)
 
     def barrier():
         if world > 1:
@@ -285,7 +303,9 @@ def main():
                                 "rounds_fetched_group0_last_turn": g0.last_copied_rounds,
                                 "rounds_kept_group0": g0.cfg.batch * g0.K},
                 "GBps": g0.last_h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None,
-                "link": "PCIe Gen5 x16 (~63 GB/s/dir theoretical)"},
+                "link": "PCIe Gen5 x16 (~63 GB/s/dir theoretical)",
+                "link_peak_GBps": link_peak,
+                "link_peak_how": "one 256 MiB pinned-host -> HBM copy, best of 5, CUDA events, before the timed region"},
         "gpu_kv_saved": {"resident_bytes": resident, "full_cache_bytes": full, "saved_frac": 1 - resident / full},
         "breakdown_ms_group0": brk,
         "clocks": clocks,
