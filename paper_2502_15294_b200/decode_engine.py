@@ -547,7 +547,7 @@ class RoundDecodeEngine:
         self.last_kept = kept
         return kept
 
-    def run_turn(self, e2e: bool = False):
+    def run_turn(self, e2e: bool = False, on_gather=None):
         """One turn on the compute stream with the captured graphs.  Returns the
         kept rounds per dialogue (host) and the H2D bytes moved.  Timing marks
         (compute stream): 0 start, 1 after scoring+select, 2 after the
@@ -572,6 +572,8 @@ class RoundDecodeEngine:
             self.copy_marks[0].record(self.copy_stream)
             nbytes = self.issue_gather(plans)
             self.copy_marks[1].record(self.copy_stream)
+            if on_gather is not None:
+                on_gather()
             self.last_h2d_bytes = nbytes
             self._phase_b1_any(kept, layer_wait=True)
             m[2].record()
@@ -649,6 +651,8 @@ class GroupedDecoder:
                                   host_unique=max(1, cfg.host_unique // groups) if cfg.host_unique else 0)
         self.cfg = cfg
         self.groups = [RoundDecodeEngine(sub, device=device, seed=seed + 97 * g) for g in range(groups)]
+        import os
+        self.stagger = os.environ.get("RK_STAGGER", "1") != "0"
 
     def prepare(self, e2e: bool = False):
         for eng in self.groups:
@@ -664,12 +668,20 @@ class GroupedDecoder:
         h2d = [0] * len(self.groups)
         errors = []
 
+        gathered = [threading.Event() for _ in self.groups]
+
         def work(g):
             eng = self.groups[g]
             try:
+                if self.stagger and g > 0:
+                    # start after the previous group's first KV gather has landed, so
+                    # the groups' gathers alternate on the PCIe link instead of
+                    # splitting it (each group's gather then overlaps the others' decode)
+                    gathered[g - 1].wait(timeout=600)
+                    eng.compute_stream.wait_event(self.groups[g - 1].copy_marks[1])
                 starts[g].record(eng.compute_stream)
-                for _ in range(turns):
-                    _, nb = eng.run_turn(e2e=e2e)
+                for i in range(turns):
+                    _, nb = eng.run_turn(e2e=e2e, on_gather=gathered[g].set if i == 0 else None)
                     h2d[g] += nb
                 eng.compute_stream.wait_stream(eng.copy_stream)
                 ends[g].record(eng.compute_stream)
