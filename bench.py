@@ -281,6 +281,14 @@ def main():
                    "lower_layers_tflops_group0": lower_flops / (brk["score_select"] / 1000.0) / 1e12,
                    "note": "lower-layer prefill + fused Lw-1 scoring + select, timed on group 0's stream while "
                            "the other group decodes; kernel-alone figures: profiles/r01_prefill_c3.json"}
+        pk = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+        tpk = float(pk.get("bf16_tflops", 2250.0))
+        achieved_tf = prefill["lower_layers_tflops_group0"]
+        prefill["roofline"] = {"bound": "tensor", "achieved": achieved_tf, "peak": tpk, "unit": "TFLOP/s",
+                               "frac": achieved_tf / tpk,
+                               "peak_source": "measured" if pk else "nominal dense bf16",
+                               "note": "algorithmic FLOPs (QK^T + PV once over causal-visible pairs); the kernel "
+                                       "issues 2x (q and P hi/lo bf16 splits for fp32-class accuracy)"}
     line = {
         "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
