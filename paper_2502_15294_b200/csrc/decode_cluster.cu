@@ -472,6 +472,10 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
     if ((int64_t)pairs * C > sm_count()) continue;
     if (C > 1 && max_len / C < 64) continue;          // >= 64 keys per CTA
     if (max_clusters(C) < pairs) continue;             // one co-resident wave
+    // a long single-dialogue layer on under half the SMs streams faster through the
+    // persistent kernel's full wave (B=1: 65 K keys 45.1 vs 42.9 us, 131 K keys 87.7 vs
+    // 81.9 us; at 32 K keys they tie and below it the cluster decode wins)
+    if (2 * (int64_t)pairs * C < sm_count() && max_len / C > 6144) return 0;
     return C;
   }
   return 0;
