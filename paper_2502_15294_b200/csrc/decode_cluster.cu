@@ -18,11 +18,12 @@
 //               math is decode_mma's (mma.sync m16n8k16, q and P split into
 //               bf16 hi/lo rows so the products carry ~16 mantissa bits, lazy
 //               rescale), with swizzled ldmatrix addresses;
-//   epilogue    warps -> CTA partial, pushed with st.shared::cluster into the
-//               inbox of the CTA that finalises each (query head, dim) output
-//               (CTA rank r owns a contiguous 1/C of them) -> one
-//               barrier.cluster -> each CTA reduces its inbox locally and
-//               writes its outputs (no remote loads, no round trips).
+//   epilogue    warps -> CTA partial, pushed with st.async into the inbox of
+//               the CTA that finalises each (query head, dim) output (CTA rank
+//               r owns a contiguous 1/C of them); the stores count their bytes
+//               on the owner's inbox mbarrier, so each CTA just waits for its
+//               inbox and reduces it locally (no remote loads, no closing
+//               cluster barrier).
 // The appended token (k_new/v_new) is written into the cache row len-1 by the
 // producer of the slice that owns it, before its TMA reads that row
 // (fence.proxy.async orders the generic stores before the async-proxy loads).
@@ -74,16 +75,15 @@ __device__ __forceinline__ uint32_t cl_size() {
   asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cl_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void st_cluster(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+// asynchronous remote store that counts its bytes on the destination CTA's mbarrier
+__device__ __forceinline__ void st_async(uint32_t addr, float v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+               ::"r"(addr), "r"(__float_as_uint(v)), "r"(remote_bar) : "memory");
 }
 __device__ __forceinline__ void cl_arrive() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
   // finalises, pushed by every CTA q of the cluster (row q), plus their (m, l)
   __shared__ float in_acc[8 * D + 64];
   __shared__ float in_m[16][8], in_l[16][8];
+  __shared__ __align__(8) uint64_t in_bar;      // completes when every peer's bytes have landed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.z, h = blockIdx.y;
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCW);
     }
+    mbar_init(&in_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -313,11 +315,40 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
     csync();
   }
   // ---- cluster merge, push model: every CTA scatters its partial (m, l, acc) into
-  // the inbox of the CTA that finalises each output (remote stores do not wait for a
-  // round trip), one cluster barrier publishes them, each CTA reduces its inbox locally
+  // the inbox of the CTA that finalises each output with st.async, whose bytes count
+  // on the owner's inbox mbarrier; each CTA waits for its own inbox only (no closing
+  // cluster barrier, no GPU-scope fence) and reduces it locally
+  if (C == 1) {           // one CTA per (dialogue, kv-head): its partial is the answer
+    __syncwarp();
+    cl_wait();
+    if (warp < kCW) {
+      const float* wm = reinterpret_cast<const float*>(kst);
+      const float* wl = wm + kCW * 8;
+      const float* wacc = wl + kCW * 8;
+      for (int e = threadIdx.x; e < G * D; e += kCW * 32) {
+        const int gg = e / D, dd = e % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kCW; ++w) M = fmaxf(M, wm[w * 8 + gg]);
+        const float mu = (M == -INFINITY) ? 0.f : M;
+        float L = 0.f, A = 0.f;
+#pragma unroll
+        for (int w = 0; w < kCW; ++w) {
+          const float sc = fast_exp2(wm[w * 8 + gg] - mu);
+          L += wl[w * 8 + gg] * sc;
+          A += wacc[(w * 8 + gg) * D + dd] * sc;
+        }
+        p.out[((int64_t)b * p.hq + h * G + gg) * D + dd] = A / L;
+      }
+    }
+    return;
+  }
   const int per = ((G * D + (int)C - 1) / (int)C + 3) & ~3;      // outputs finalised per CTA
+  const int mine = max(0, min(per, G * D - (int)rank * per));    // outputs this CTA finalises
+  if (threadIdx.x == 0)
+    mbar_expect_tx(&in_bar, (unsigned)(C * (mine + 2 * G) * 4));
   __syncwarp();
-  cl_wait();              // every peer has started (its inbox exists)
+  cl_wait();              // every peer has started (its inbox and barrier exist)
   if (warp < kCW) {
     const float* wm = reinterpret_cast<const float*>(kst);
     const float* wl = wm + kCW * 8;
@@ -336,16 +367,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
         A += wacc[(w * 8 + gg) * D + dd] * sc;
       }
       const int r = e / per;
-      st_cluster(cl_map(&in_acc[rank * per + (e - r * per)], r), A);
+      st_async(cl_map(&in_acc[rank * per + (e - r * per)], r), A, cl_map(&in_bar, r));
       if (dd == 0)
         for (uint32_t q = 0; q < C; ++q) {
-          st_cluster(cl_map(&in_m[rank][gg], q), M);
-          st_cluster(cl_map(&in_l[rank][gg], q), L);
+          st_async(cl_map(&in_m[rank][gg], q), M, cl_map(&in_bar, q));
+          st_async(cl_map(&in_l[rank][gg], q), L, cl_map(&in_bar, q));
         }
     }
   }
-  __syncwarp();
-  cl_sync();              // release the pushes / acquire the peers'
+  mbar_wait(&in_bar, 0);  // every peer's share of this CTA's outputs has landed
   for (int el = threadIdx.x; el < per; el += kThreads) {
     const int e = (int)rank * per + el;
     if (e >= G * D) break;
