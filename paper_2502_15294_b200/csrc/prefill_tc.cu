@@ -881,6 +881,20 @@ bool prefill_tc_supported(int kv_dtype, int d, int n_q, int G) {
   return kv_dtype == RK_BF16 && d == 128 && (int64_t)n_q * G >= 64 && G <= 16;
 }
 
+// CTA pairs the persistent prefill grid may occupy: all SMs by default;
+// RK_PREFILL_MAX_PAIRS caps it so a concurrent decode keeps SMs of its own
+// (experiment: C3 with 48 / 37 / 26 pairs ran 2.94 / 2.93 / 2.92 K tok/s vs ~2.98 K
+// uncapped — the other group's decode speeds up exactly as much as the prefill slows)
+static int prefill_pairs() {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = std::getenv("RK_PREFILL_MAX_PAIRS");
+    cap = e ? std::max(0, std::atoi(e)) : 0;       // 0 = no cap
+  }
+  const int all = std::max(1, sm_count() / 2);
+  return cap > 0 ? std::min(cap, all) : all;
+}
+
 // item table: `items` (n_items given) or uniform items of item_keys keys over s
 PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool stats, bool with_output) {
   PrefillPlan pl{};
@@ -901,7 +915,7 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
     const char* e = std::getenv("RK_PREFILL_UNITS");
     per_pair = e ? std::max(1, std::atoi(e)) : 8;
   }
-  const int target = per_pair * (sm_count() / 2);           // units per CTA pair
+  const int target = per_pair * prefill_pairs();            // units per CTA pair
   int nc = (target + mt_total - 1) / mt_total;
   nc = std::max(1, std::min(nc, pl.n_items));
   pl.items_per_chunk = (pl.n_items + nc - 1) / nc;
@@ -917,7 +931,7 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
     // waves x (work per unit + a fixed per-unit cost), around the target count
     // (C3, 56 M tiles x 11 chunks = 616 units = 8.3 waves on 74 pairs; 13 chunks:
     // 728 units = 9.8 waves)
-    const int pairs = std::max(1, sm_count() / 2);
+    const int pairs = prefill_pairs();
     const double unit_cost = 0.03;                          // per unit, in whole-M-tile work (fitted: n_q 128..1024)
     double best = 1e30;
     for (int ipc = 1; ipc <= pl.n_items; ++ipc) {
@@ -1013,7 +1027,7 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
                                  (int)pf::SMEM), "prefill_tc smem attribute");
     configured = true;
   }
-  const int grid = 2 * std::min(sm_count() / 2, pl.n_units);   // CTA pairs (__cluster_dims__(2,1,1))
+  const int grid = 2 * std::min(prefill_pairs(), pl.n_units);   // CTA pairs (__cluster_dims__(2,1,1))
   if (score_only) {
     pf::prefill_tc_kernel<true, true><<<grid, pf::THREADS, pf::SMEM, st>>>(qmap, kmap, vmap, p);
     RK_CHECK_LAUNCH("prefill_tc_kernel<score>");
