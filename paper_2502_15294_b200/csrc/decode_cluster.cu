@@ -497,6 +497,12 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
     cmax = e ? std::atoi(e) : 16;
   }
   const int pairs = batch * hkv;
+  // RK_DECODE_CLUSTER=2 (experiment): beyond one wave, one CTA per pair in several
+  // waves.  Measured vs the persistent kernel (C2 shapes, equal lengths): better when
+  // the waves are nearly full (B=32: 45.5 vs 50.1 us upper, 297.6 vs 301.4 us lower;
+  // B=48 67.0 vs 70.5 us), worse otherwise (B=20: 38.5 vs 33.4 us) and exposed to
+  // ragged lengths, so the default keeps the persistent kernel there
+  if (mode == 2 && pairs > sm_count()) return 1;
   for (int C : {16, 12, 8, 6, 4, 3, 2, 1}) {   // 10 (11 co-resident) measured slower at B=1 upper layers
     if (C > cmax) continue;
     if ((int64_t)pairs * C > sm_count()) continue;
