@@ -159,3 +159,26 @@ def test_cluster_decode_on_engine_layer_views_at_capacity():
             ref, _ = oatt.attention_forward_gqa(q[b:b + 1].cpu().numpy(), kk, vv, [n - 1], np.arange(n))
             err = np.abs(out[b].reshape(1, -1).cpu().numpy() - ref).max() / np.abs(ref).max()
             assert err < 2e-5, (layer, b, err)
+
+
+def test_randomized_shapes_vs_oracle():
+    """Seeded sweep over batch (1-18), kv-heads, group, head dim, ragged lengths
+    and append on/off: every shape goes through rk_decode_attention's planner
+    (cluster sizes 1-16, or the persistent kernel) and matches the oracle."""
+    rng = np.random.default_rng(2024)
+    plans = set()
+    for i in range(24):
+        hkv = int(rng.choice([2, 4, 8]))
+        G = int(rng.choice([1, 2, 4, 7, 8]))
+        d = int(rng.choice([64, 128]))
+        B = int(rng.integers(1, 19))
+        lens = [int(x) for x in rng.integers(0, 4000, size=B)]
+        if rng.random() < 0.5:
+            lens = [max(lens)] * B                     # equal lengths (the engine's batches)
+        append = bool(rng.random() < 0.8)
+        if not append:
+            lens = [max(1, x) for x in lens]
+        plan, err = _run(lens, hkv, G, d, append=append, seed=100 + i)
+        plans.add(plan)
+        assert err < 2e-5, (i, B, hkv, G, d, append, plan, err)
+    assert any(p > 1 for p in plans) and any(p >= 0 for p in plans), plans
