@@ -153,3 +153,35 @@ def test_prefill_single_pass_bf16_path(rng):
     items = torch.from_numpy(build_round_items([(0, hist, 0), (hist, hist + n_q, 1)], 1024)).cuda()
     with pytest.raises(DomainError):
         kernels.prefill_attention(*args, items=items, n_bins=1, single_pass=True)
+
+
+def test_prefill_randomized_shapes_vs_oracle():
+    """Seeded sweep of question rows, history, kv-heads and groups (>= 64 stacked
+    rows), with the fused round masses on half of them: outputs vs the oracle
+    (2e-5) and masses vs capture + aggregate (2e-5) through the balanced planner."""
+    rng = np.random.default_rng(77)
+    for i in range(10):
+        hkv = int(rng.choice([1, 2, 4, 8]))
+        G = int(rng.choice([1, 2, 4, 7, 8]))
+        n_q = int(rng.integers(max(1, -(-64 // G)), 300))
+        n_r = int(rng.integers(1, 9))
+        lens = rng.integers(1, 600, size=n_r)
+        starts = np.concatenate([[0], np.cumsum(lens)])
+        hist = int(starts[-1])
+        q, k, v, qp, kp = _inputs(rng, n_q, hist, hkv, G, scale=1.5)
+        s = hist + n_q
+        ref, cap = oatt.attention_forward_gqa(q, k, v, qp, kp, capture=True)
+        args = _dev(q, k, v, qp, kp)[:5]
+        if i % 2:
+            bounds = [(int(starts[m]), int(starts[m + 1]), m) for m in range(n_r)] + [(hist, s, n_r)]
+            items = torch.from_numpy(build_round_items(bounds, 1024)).cuda()
+            out, raw, _ = kernels.prefill_attention(*args, items=items, n_bins=n_r)
+            rounds = [orr.Round(m, (int(starts[m]), int(starts[m]) + 1), (int(starts[m]) + 1, int(starts[m + 1])))
+                      for m in range(n_r)]
+            rounds.append(orr.Round(n_r, (hist, s), (s, s)))
+            ref_raw = orr.aggregate_round_attention(cap, rounds, "question", n_r, row_offset=hist)
+            np.testing.assert_allclose(raw.cpu().numpy(), ref_raw, rtol=2e-5, atol=1e-9)
+        else:
+            out, _, _ = kernels.prefill_attention(*args)
+        err = _rel(out.reshape(n_q, -1).cpu().numpy(), ref)
+        assert err < 2e-5, (i, n_q, hist, hkv, G, err)
