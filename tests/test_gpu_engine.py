@@ -240,3 +240,47 @@ def test_grouped_decoder_e2e_staggered_matches_single_engine():
         assert [tuple(int(x) for x in k) for k in kept] == [tuple(int(x) for x in k) for k in eng.last_kept]
         T = cfg.decode_steps
         assert torch.equal(eng.host_out[T], ref.out.cpu())
+
+
+def test_engine_c2_full_shapes_turn_matches_oracle():
+    """One graph-replayed turn at the bench's C2 shapes (32 layers, Lw=5, 32 heads
+    over 8 kv-heads, 32 rounds x 512 keys, K=4; two dialogues): the kept rounds
+    equal the oracle's selection from the capture at layer Lw-1 over all 16 K
+    history keys, and the last token's outputs at layers 0, Lw-1, Lw, L-1 equal the
+    oracle over the full history / the kept rounds plus the turn's rows."""
+    cfg = EngineConfig(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512,
+                       batch=2, decode_steps=3, policy=SelectionPolicy("top_percent", fraction=0.10),
+                       input_period=3, plant=2, plant_beta=0.25, question_variants=1)
+    eng = RoundDecodeEngine(cfg, seed=5)
+    lw, L, T, R = cfg.watershed, cfg.num_layers, cfg.round_tokens, cfg.rounds
+    lower0 = {(b, l): (_f(eng.lower[b, l, 0, : eng.hist]), _f(eng.lower[b, l, 1, : eng.hist]))
+              for b in range(cfg.batch) for l in (0, lw - 1)}
+    eng.prepare(e2e=False)
+    kept, _ = eng.run_turn()
+    torch.cuda.synchronize()
+    P, steps = eng.period, eng.turn_tokens
+    assert eng.K == 4
+    for b in range(cfg.batch):
+        q0 = _f(eng.q_in[0, lw - 1, b])[None]
+        kq = np.concatenate([lower0[(b, lw - 1)][0], _f(eng.kv_in[0, lw - 1, 0, b])[None]])
+        _, cap = oatt.attention_forward_gqa(q0, kq, kq, [eng.hist], np.arange(eng.hist + 1), capture=True)
+        raw = np.array([cap[0, r * T:(r + 1) * T].sum() for r in range(R)])
+        want = orr.select(orr.normalize(raw), orr.SelectionPolicy("top_percent", fraction=0.10))
+        assert tuple(int(x) for x in kept[b]) == want
+        tl = steps - 1
+        for l in (0, lw - 1, lw, L - 1):
+            rows_k = np.stack([_f(eng.kv_in[t % P, l, 0, b]) for t in range(steps)])
+            rows_v = np.stack([_f(eng.kv_in[t % P, l, 1, b]) for t in range(steps)])
+            if l < lw:
+                K = np.concatenate([lower0[(b, l)][0], rows_k])
+                V = np.concatenate([lower0[(b, l)][1], rows_v])
+            else:
+                hs = b % eng.host_sets
+                blocks = [eng.host_blocks[hs][int(r)][l - lw] for r in kept[b]]
+                K = np.concatenate([_f(bk[0]) for bk in blocks] + [rows_k])
+                V = np.concatenate([_f(bk[1]) for bk in blocks] + [rows_v])
+            q = _f(eng.q_in[tl % P, l, b])[None]
+            ref, _ = oatt.attention_forward_gqa(q, K, V, [len(K) - 1], np.arange(len(K)))
+            got = _f(eng.out[l, b]).reshape(1, -1)
+            err = np.abs(got - ref).max() / np.abs(ref).max()
+            assert err < 1e-4, (b, l, err)
