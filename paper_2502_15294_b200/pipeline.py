@@ -8,7 +8,9 @@ the reference step by step (pipeline.py:192-394):
      masses at layer Lw-1 computed by the fused librk scorer (`round_scores`:
      softmax statistics per round, no capture matrix) over the same keys the
      reference's capture sees (every prior round incl. dropped ones + the causal
-     question prefix); `normalize` + `select` on the device (bit-exact);
+     question prefix); with capture_mode="pre" the head-summed-logit capture is
+     materialised and aggregated instead (engine.py:187-200); `normalize` +
+     `select` on the device (bit-exact);
   3. ONE batched H2D of the kept rounds' upper blocks (TieredStore.fetch_upper,
      rk_h2d_gather);
   4. upper-layer prefill over kept rounds + the question;
@@ -30,7 +32,7 @@ import torch
 from .engine import KVCache, Model
 from .errors import DomainError
 from .selection import ActivityLedger, SelectionPolicy, SelectionResult, select
-from .stats import SEGMENT_QUESTION, Round, RoundDistribution, normalize, round_scores
+from .stats import SEGMENT_QUESTION, Round, RoundDistribution, aggregate_round_attention, normalize, round_scores
 from .store import TieredStore
 
 SEP_TOKEN = 256
@@ -140,6 +142,14 @@ class RoundPipeline:
             r = rounds_now[m]
             bounds.append((r.start, r.end, m))
         bounds.append((q_start, len(kv), n))
+        if c.capture_mode == "pre":
+            # head-summed-logit capture (engine.py:187-200, config capture_mode="pre"):
+            # materialise it on the device, then Eq. 1 with rk_aggregate_rounds
+            pos = torch.as_tensor(np.asarray(q_pos), dtype=torch.int64, device=kv.positions.device)
+            cap = self.model._capture_pre(q, kv, pos, None)
+            raw = aggregate_round_attention(cap, rounds_now, SEGMENT_QUESTION, n, active_rounds=active,
+                                            row_offset=q_start)
+            return raw.cpu().numpy()
         active_mask = [m in set(active) for m in range(n)]
         raw = round_scores(q, kv.keys.view(-1, c.num_heads, c.d_k), q_pos, kv.positions, bounds, n,
                            active=active_mask)

@@ -128,14 +128,17 @@ def test_fetch_upper_moves_bytes():
     ("drop2", dict(policy=SelectionPolicy("top_percent", fraction=0.25), drop_window=2, drop_protect=1)),
     ("fixed", dict(policy=SelectionPolicy("fixed", v=0.12))),
     ("adaptive", dict(policy=SelectionPolicy("adaptive", kappa=0.5))),
+    ("pre", dict(policy=SelectionPolicy("top_percent", fraction=0.25))),    # capture_mode="pre" model
 ])
 def test_c1_policy_and_drop_variants_match_reference(name, kw):
     """Inactivity drop policy (ActivityLedger.update_and_drop + store.drop_upper,
-    selection.py:168-204, store.py:280-285) and the fixed / adaptive strategies
+    selection.py:168-204, store.py:280-285), the fixed / adaptive strategies and
+    the head-summed-logit capture (capture_mode="pre", engine.py:187-200)
     through whole turns: kept rounds, dropped set, answers and transfer ledger
     equal the reference's (tests/golden/c1_variants.npz)."""
     z = np.load(GOLDEN / "c1_variants.npz")
-    model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42))
+    model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42,
+                              capture_mode="pre" if name == "pre" else "post"))
     pipe = RoundPipeline(model, 2, **kw)
     for t in range(6):
         res = pipe.run_turn(list(z[f"{name}_t{t}_q"]), max_decode_steps=15)

@@ -346,14 +346,17 @@ def pipeline_variants(ref):
     from roundkv_ref.engine import Model, ModelConfig
     from roundkv_ref.pipeline import RoundPipeline
     from roundkv_ref.selection import SelectionPolicy
-    model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42))
     variants = {
         "drop2": dict(policy=SelectionPolicy("top_percent", fraction=0.25), drop_window=2, drop_protect=1),
         "fixed": dict(policy=SelectionPolicy("fixed", v=0.12)),
         "adaptive": dict(policy=SelectionPolicy("adaptive", kappa=0.5)),
+        # the head-summed-logit capture (ModelConfig.capture_mode="pre", engine.py:187-200)
+        "pre": dict(policy=SelectionPolicy("top_percent", fraction=0.25)),
     }
     out = {}
     for name, kw in variants.items():
+        mode = "pre" if name == "pre" else "post"
+        model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42, capture_mode=mode))
         pipe = RoundPipeline(model, 2, **kw)
         qrng = np.random.default_rng(5)
         for t in range(6):
