@@ -129,6 +129,8 @@ def test_fetch_upper_moves_bytes():
     ("fixed", dict(policy=SelectionPolicy("fixed", v=0.12))),
     ("adaptive", dict(policy=SelectionPolicy("adaptive", kappa=0.5))),
     ("pre", dict(policy=SelectionPolicy("top_percent", fraction=0.25))),    # capture_mode="pre" model
+    ("baseline", dict(mode="baseline")),                                    # full-cache baseline mode
+    ("mask", dict(policy=SelectionPolicy("top_percent", fraction=0.25))),   # attend_mode="mask"
 ])
 def test_c1_policy_and_drop_variants_match_reference(name, kw):
     """Inactivity drop policy (ActivityLedger.update_and_drop + store.drop_upper,
@@ -140,6 +142,8 @@ def test_c1_policy_and_drop_variants_match_reference(name, kw):
     model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42,
                               capture_mode="pre" if name == "pre" else "post"))
     pipe = RoundPipeline(model, 2, **kw)
+    if name == "mask":
+        pipe.attend_mode = "mask"
     for t in range(6):
         res = pipe.run_turn(list(z[f"{name}_t{t}_q"]), max_decode_steps=15)
         m = res.metrics

@@ -352,12 +352,18 @@ def pipeline_variants(ref):
         "adaptive": dict(policy=SelectionPolicy("adaptive", kappa=0.5)),
         # the head-summed-logit capture (ModelConfig.capture_mode="pre", engine.py:187-200)
         "pre": dict(policy=SelectionPolicy("top_percent", fraction=0.25)),
+        # full-cache baseline mode (pipeline.py:115-150, mode="baseline")
+        "baseline": dict(mode="baseline"),
+        # masked attention over every upper block instead of splicing (attend_mode="mask")
+        "mask": dict(policy=SelectionPolicy("top_percent", fraction=0.25)),
     }
     out = {}
     for name, kw in variants.items():
         mode = "pre" if name == "pre" else "post"
         model = Model(ModelConfig(num_layers=4, num_heads=8, d_model=512, rng_seed=42, capture_mode=mode))
         pipe = RoundPipeline(model, 2, **kw)
+        if name == "mask":
+            pipe.attend_mode = "mask"
         qrng = np.random.default_rng(5)
         for t in range(6):
             q = [int(x) for x in qrng.integers(0, 256, size=31)]
