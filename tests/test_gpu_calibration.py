@@ -49,3 +49,16 @@ def test_calibration_matches_reference():
     assert cal.detect_watershed(curves).layer == int(z["ws_max_drop_0.1"])
     res = cal.calibrate_watershed(model, convs, criterion="threshold", tau=1e-3)
     assert res.layer == int(z["ws_threshold_0.001"]) and res.corpus_size == len(convs)
+
+
+def test_calibration_pre_capture_matches_reference():
+    """capture_mode="pre" (softmax of the head-summed logits, engine.py:187-200):
+    the per-layer round distributions of every conversation equal the
+    reference's capture_all_layers + layer_distributions."""
+    z = np.load(GOLDEN / "calib_cases.npz")
+    model = Model(ModelConfig(num_layers=int(z["num_layers"]), num_heads=int(z["num_heads"]),
+                              d_model=int(z["d_model"]), rng_seed=int(z["seed"]), capture_mode="pre"))
+    for i, conv in enumerate(_corpus(z)):
+        n = cal.analysis_round_index(conv)
+        masses = cal.layer_round_masses(model, conv, n)
+        np.testing.assert_allclose(masses, z[f"c{i}_masses_pre"], rtol=1e-4, atol=1e-7)

@@ -310,6 +310,7 @@ def calibration_cases(ref, rng, n_conv=4):
     from roundkv_ref.pipeline import analysis_round_index, capture_all_layers, layer_distributions
     from roundkv_ref.stats import detect_watershed, kl_curve
     model = Model(ModelConfig(num_layers=6, num_heads=4, d_model=128, rng_seed=7))
+    model_pre = Model(ModelConfig(num_layers=6, num_heads=4, d_model=128, rng_seed=7, capture_mode="pre"))
     out = {"n_conv": np.array(n_conv), "num_layers": np.array(6), "num_heads": np.array(4),
            "d_model": np.array(128), "seed": np.array(7)}
     curves = []
@@ -331,6 +332,9 @@ def calibration_cases(ref, rng, n_conv=4):
         out[f"c{i}_spans"] = np.array(spans, dtype=np.int64)
         out[f"c{i}_n"] = np.array(n)
         out[f"c{i}_masses"] = np.stack([d.masses for d in dists])
+        caps_pre = capture_all_layers(model_pre, conv)          # head-summed-logit capture (engine.py:187-200)
+        out[f"c{i}_masses_pre"] = np.stack([d.masses for d in layer_distributions([caps_pre[l] for l in range(6)],
+                                                                                  conv.rounds, n)])
         out[f"c{i}_curve"] = curve.values
     for crit, tau in (("max_drop", 0.1), ("threshold", 0.1), ("threshold", 1e-3)):
         w = detect_watershed(curves, criterion=crit, tau=tau)
