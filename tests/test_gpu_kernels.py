@@ -278,3 +278,22 @@ def test_selection_errors_and_empty():
     with pytest.raises(DomainError):
         selection.SelectionPolicy(kind="token_baseline").__class__  # valid kind
         selection.select(stats.normalize(np.ones(3)), selection.SelectionPolicy(kind="token_baseline"))
+
+
+@pytest.mark.parametrize("idx", [0, 3, 7, 25, 27])
+def test_engine_attention_layer_on_golden(idx):
+    """engine.attention_layer (engine.py:120-143): flat (rows, d_model) operands,
+    default causal positions, capture on by default — equals the reference's
+    attention_forward golden output / scores for the same case."""
+    from paper_2502_15294_b200.engine import attention_layer
+    c = KERNEL[idx]
+    n, h, d = c["q"].shape
+    s = c["k"].shape[0]
+    flat = lambda x: x.reshape(x.shape[0], h * d)  # noqa: E731
+    out, scores = attention_layer(flat(c["q"]), flat(c["k"]), flat(c["v"]), num_heads=h, allowed=c["allowed"])
+    assert np.array_equal(c["q_pos"], np.arange(s - n, s)) and np.array_equal(c["k_pos"], np.arange(s))
+    np.testing.assert_allclose(out, c["out"], rtol=1e-5, atol=1e-5)
+    if c["capture"]:
+        np.testing.assert_allclose(scores, c["scores"], rtol=1e-5, atol=1e-7)
+    with pytest.raises(DomainError):
+        attention_layer(c["q"], flat(c["k"]), flat(c["v"]), num_heads=h)
