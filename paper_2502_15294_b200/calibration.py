@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .errors import DomainError
-from .stats import Round, normalize, round_scores
+from .stats import SEGMENT_QUESTION, Round, aggregate_round_attention, normalize, round_scores
 
 KL_EPSILON = 1e-10          # stats.py:22 smoothing
 SEP_TOKEN = 256             # conversation.py:24
@@ -165,6 +165,25 @@ def layer_round_masses(model, conv, n: int, *, chunk: int = 256) -> np.ndarray:
                         layer_hook=hook)
     torch.cuda.synchronize()
     return np.stack([normalize(r.cpu().numpy(), layer=l).masses for l, r in enumerate(raws)])
+
+
+def capture_all_layers(model, conv) -> dict:
+    """pipeline.py:452-460: teacher-forced full prefill capturing every layer's
+    (tokens, tokens) score matrix on the device — the reference's materialised
+    route (and the one capture_mode="pre" needs); layer_round_masses computes the
+    same distributions without the matrices."""
+    L = model.config.num_layers
+    positions = np.arange(conv.num_tokens, dtype=np.int64)
+    _, captures = model.forward_range(model.new_cache(), 0, L, tokens=conv.token_ids, positions=positions,
+                                      capture_layers=range(L))
+    return captures
+
+
+def layer_distributions(matrices, rounds, current_round: int, segment: str = SEGMENT_QUESTION) -> list:
+    """pipeline.py:463-471: per-layer normalised round distributions from full
+    score matrices (rk_aggregate_rounds + the device normalisation)."""
+    return [normalize(aggregate_round_attention(m, rounds, segment, current_round), layer=l, segment=segment)
+            for l, m in enumerate(matrices)]
 
 
 def conversation_kl_curve(model, conv) -> KLCurve:

@@ -34,6 +34,9 @@ from .errors import DomainError
 from .selection import ActivityLedger, SelectionPolicy, SelectionResult, select
 from .stats import SEGMENT_QUESTION, Round, RoundDistribution, aggregate_round_attention, normalize, round_scores
 from .store import TieredStore
+# the reference module's calibration entry points (pipeline.py:439-494) live in calibration.py
+from .calibration import (analysis_round_index, calibrate_watershed, capture_all_layers,  # noqa: F401
+                          conversation_kl_curve, layer_distributions)
 
 SEP_TOKEN = 256
 EOT_TOKEN = 257

@@ -179,3 +179,17 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
               _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(items), n_items, n_bins, _lib.ptr(act),
               _lib.ptr(raw), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     return raw[:n_out]
+
+
+# The reference's stats module also carries the KL / watershed helpers
+# (stats.py:118-181); they live in calibration.py (which imports this module),
+# re-exported here lazily.
+_CALIBRATION_NAMES = ("KL_EPSILON", "KLCurve", "WatershedResult", "kl_divergence", "kl_curve", "mean_curve",
+                      "detect_watershed")
+
+
+def __getattr__(name):
+    if name in _CALIBRATION_NAMES:
+        from . import calibration
+        return getattr(calibration, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -62,3 +62,26 @@ def test_calibration_pre_capture_matches_reference():
         n = cal.analysis_round_index(conv)
         masses = cal.layer_round_masses(model, conv, n)
         np.testing.assert_allclose(masses, z[f"c{i}_masses_pre"], rtol=1e-4, atol=1e-7)
+
+
+@pytest.mark.parametrize("mode", ["post", "pre"])
+def test_reference_calibration_entry_points(mode):
+    """The reference module names (pipeline.capture_all_layers, layer_distributions,
+    conversation_kl_curve; stats.kl_curve): the materialised route gives the
+    golden distributions and curves too."""
+    from paper_2502_15294_b200 import pipeline as pl
+    from paper_2502_15294_b200 import stats as st
+    z = np.load(GOLDEN / "calib_cases.npz")
+    model = Model(ModelConfig(num_layers=int(z["num_layers"]), num_heads=int(z["num_heads"]),
+                              d_model=int(z["d_model"]), rng_seed=int(z["seed"]), capture_mode=mode))
+    key = "masses" if mode == "post" else "masses_pre"
+    for i, conv in enumerate(_corpus(z)):
+        n = pl.analysis_round_index(conv)
+        caps = pl.capture_all_layers(model, conv)
+        dists = pl.layer_distributions([caps[l] for l in range(int(z["num_layers"]))], conv.rounds, n)
+        masses = np.stack([np.asarray(d.masses) for d in dists])
+        np.testing.assert_allclose(masses, z[f"c{i}_{key}"], rtol=1e-4, atol=1e-7)
+        if mode == "post":
+            np.testing.assert_allclose(st.kl_curve(masses).values, z[f"c{i}_curve"], rtol=1e-3, atol=1e-7)
+            np.testing.assert_allclose(pl.conversation_kl_curve(model, conv).values, z[f"c{i}_curve"],
+                                       rtol=1e-3, atol=1e-7)
