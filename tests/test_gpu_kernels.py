@@ -297,3 +297,27 @@ def test_engine_attention_layer_on_golden(idx):
         np.testing.assert_allclose(scores, c["scores"], rtol=1e-5, atol=1e-7)
     with pytest.raises(DomainError):
         attention_layer(c["q"], flat(c["k"]), flat(c["v"]), num_heads=h)
+
+
+def test_backend_contract_edge_cases_like_reference(rng):
+    """The reference's backend contract tests (test_backend.py:26-90) against
+    this backend: one query / one key, rows normalised and causal, empty query
+    set, capture off -> None, no visible key -> InvariantError("...no visible
+    key..."), shape mismatches -> DomainError."""
+    q, k, v, q_pos, k_pos, _ = _case(rng, n=5, s=12, heads=4, d_k=8)
+    o1, s1 = backend.attention_forward(q[:1], k[:1], v[:1], np.array([0]), np.array([0]), capture=True)
+    np.testing.assert_allclose(o1.reshape(1, 4, 8), v[:1], rtol=1e-6, atol=1e-6)   # one key: out = v
+    assert s1.shape == (1, 1) and s1[0, 0] == 1.0
+    out, sc = backend.attention_forward(q, k, v, q_pos, k_pos, capture=True)
+    np.testing.assert_allclose(sc.sum(axis=1), 1.0, rtol=1e-12, atol=1e-12)
+    for i, p in enumerate(q_pos):
+        assert np.all(sc[i, k_pos > p] == 0.0)
+    oe, se = backend.attention_forward(q[:0], k, v, np.zeros(0, dtype=np.int64), k_pos, capture=True)
+    assert oe.shape == (0, 32) and se.shape == (0, 12)
+    assert backend.attention_forward(q, k, v, q_pos, k_pos)[1] is None
+    with pytest.raises(InvariantError, match="no visible key"):
+        backend.attention_forward(q, k, v, q_pos, k_pos, allowed=np.zeros(12, dtype=bool))
+    with pytest.raises(DomainError):
+        backend.attention_forward(q, k, v[:, :2], q_pos, k_pos)
+    with pytest.raises(DomainError):
+        backend.attention_forward(q, k, v, q_pos[:2], k_pos)
