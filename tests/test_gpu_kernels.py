@@ -321,3 +321,19 @@ def test_backend_contract_edge_cases_like_reference(rng):
         backend.attention_forward(q, k, v[:, :2], q_pos, k_pos)
     with pytest.raises(DomainError):
         backend.attention_forward(q, k, v, q_pos[:2], k_pos)
+
+
+def test_normalize_properties_like_reference(rng):
+    """stats.normalize (device) on the reference's test_stats.TestNormalize cases."""
+    d = stats.normalize(np.array([2.0, 2.0]))
+    np.testing.assert_allclose(d.masses, [0.5, 0.5])
+    assert not d.degenerate
+    d = stats.normalize(np.zeros(3))
+    np.testing.assert_allclose(d.masses, [1 / 3] * 3)
+    assert d.degenerate
+    np.testing.assert_allclose(stats.normalize(np.array([0.75, 0.25])).masses, [0.75, 0.25])
+    with pytest.raises(DomainError, match="non-negative"):
+        stats.normalize(np.array([0.5, -0.1]))
+    for _ in range(50):
+        raw = rng.random(int(rng.integers(1, 30))) * rng.integers(1, 100)
+        assert abs(np.asarray(stats.normalize(raw).masses).sum() - 1.0) <= 1e-6
