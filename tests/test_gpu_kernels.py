@@ -337,3 +337,58 @@ def test_normalize_properties_like_reference(rng):
     for _ in range(50):
         raw = rng.random(int(rng.integers(1, 30))) * rng.integers(1, 100)
         assert abs(np.asarray(stats.normalize(raw).masses).sum() - 1.0) <= 1e-6
+
+
+def test_aggregate_round_attention_like_reference(rng):
+    """stats.aggregate_round_attention (rk_aggregate_rounds) on the reference's
+    test_stats.TestAggregate cases: hand-built rows, split across rounds, zero
+    block, 50 random matrices vs the double-loop oracle (both segments),
+    row_offset mapping, missing rows / empty span rejected."""
+    agg = stats.aggregate_round_attention
+
+    def causal(s):
+        m = np.zeros((s, s))
+        for i in range(s):
+            r = rng.random(i + 1)
+            m[i, :i + 1] = r / r.sum()
+        return m
+
+    def brute(m, rounds, seg, n, k):
+        rnd = rounds[n]
+        span = rnd.q_span if seg == "question" else rnd.a_span
+        cols = list(range(*rounds[k].q_span)) + list(range(*rounds[k].a_span))
+        return sum(float(m[i][j]) for i in range(*span) for j in cols)
+
+    rounds = orr.make_rounds([(2, 1), (1, 0)])
+    mat = np.zeros((4, 4))
+    mat[3, :4] = 0.25
+    for i in range(3):
+        mat[i, :i + 1] = 1.0 / (i + 1)
+    np.testing.assert_allclose(agg(mat, rounds, "question", 1), [0.75])
+    rounds = orr.make_rounds([(2, 1), (1, 0), (1, 0)])
+    mat = np.zeros((5, 5))
+    mat[4, :4] = 0.25
+    for i in range(4):
+        mat[i, :i + 1] = 1.0 / (i + 1)
+    np.testing.assert_allclose(agg(mat, rounds, "question", 2), [0.75, 0.25])
+    rounds = orr.make_rounds([(1, 1), (1, 1)])
+    mat = np.zeros((4, 4))
+    mat[2, 2] = mat[3, 3] = 1.0
+    np.testing.assert_array_equal(agg(mat, rounds, "question", 1), [0.0])
+    for _ in range(50):
+        layout = [(int(rng.integers(1, 4)), int(rng.integers(1, 4))) for _ in range(int(rng.integers(2, 5)))]
+        rounds = orr.make_rounds(layout)
+        n = len(rounds) - 1
+        mat = causal(rounds[-1].end)
+        for seg in ("question", "answer"):
+            raw = agg(mat, rounds, seg, n)
+            for k in range(n):
+                assert abs(raw[k] - brute(mat, rounds, seg, n, k)) <= 1e-9
+    rounds = orr.make_rounds([(2, 2), (3, 0)])
+    full = causal(7)
+    np.testing.assert_allclose(agg(full, rounds, "question", 1), agg(full[4:7], rounds, "question", 1, row_offset=4),
+                               atol=1e-12)
+    with pytest.raises(DomainError, match="absent"):
+        agg(full[5:], rounds, "question", 1, row_offset=5)
+    with pytest.raises(DomainError, match="empty"):
+        agg(np.zeros((7, 7)), rounds, "answer", 1)
