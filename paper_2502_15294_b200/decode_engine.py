@@ -175,8 +175,10 @@ class RoundDecodeEngine:
 
         # ---- scratch
         self.raw = torch.empty((B, R), dtype=torch.float64, device=self.dev)
-        self.ws = kernels.decode_workspace(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8),
-                                           self.dev, tag="engine")
+        # this engine's own decode workspace (split-K partials, scoring statistics, arrival counters):
+        # groups run concurrently on their own streams, so nothing here may be shared between engines
+        ws_bytes = _lib.lib.rk_decode_workspace_bytes(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8))
+        self.ws = torch.zeros(max(256, int(ws_bytes)), dtype=torch.uint8, device=self.dev)
         self.copy_stream = torch.cuda.Stream(self.dev)
         self.compute_stream = torch.cuda.Stream(self.dev)
         # torch creates CUDA events lazily: record once so the handles exist
@@ -678,6 +680,8 @@ class GroupedDecoder:
                     # the groups' gathers alternate on the PCIe link instead of
                     # splitting it (each group's gather then overlaps the others' decode)
                     gathered[g - 1].wait(timeout=600)
+                    if errors:           # the previous group failed before its gather: fail fast
+                        return
                     eng.compute_stream.wait_event(self.groups[g - 1].copy_marks[1])
                 starts[g].record(eng.compute_stream)
                 for i in range(turns):
@@ -687,6 +691,7 @@ class GroupedDecoder:
                 ends[g].record(eng.compute_stream)
             except Exception as exc:  # surfaced in the caller
                 errors.append(exc)
+                gathered[g].set()        # release a group waiting on this one's first gather
 
         for eng in self.groups:
             eng.window_log = []

@@ -83,11 +83,12 @@ def select_batch(raw: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, nor
     """rk_select_batch over rows of a (B, n) float64 device tensor.  Returns
     device (masses (B, n), kept (B, n) int32, meta (B, 3) int32 = n_kept,
     degenerate, status)."""
+    raw = raw.contiguous()         # select_kernel offsets raw, masses and kept by the same ld
     B, n = raw.shape
     masses = torch.empty((B, n), dtype=torch.float64, device=raw.device)
     kept = torch.zeros((B, n), dtype=torch.int32, device=raw.device)
     meta = torch.zeros((3, B), dtype=torch.int32, device=raw.device)
-    _lib.call("rk_select_batch", _lib.ptr(raw), n, raw.stride(0), B, 1 if normalize else 0, _lib.SEL_KINDS[kind],
+    _lib.call("rk_select_batch", _lib.ptr(raw), n, n, B, 1 if normalize else 0, _lib.SEL_KINDS[kind],
               float(v), int(k_top), float(kappa), _lib.ptr(masses), _lib.ptr(kept), _lib.ptr(meta[0]),
               _lib.ptr(meta[1]), _lib.ptr(meta[2]), _lib.stream_ptr(stream))
     return masses, kept, meta

@@ -175,7 +175,8 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
     ws = scratch(ws_bytes, dev, "scores")
     q_pos = torch.as_tensor(q_pos, dtype=torch.int64, device=dev)
     k_pos = torch.as_tensor(k_pos, dtype=torch.int64, device=dev)
-    _lib.call("rk_round_scores", _lib.ptr(q.contiguous()), n_q, hq, d, _lib.ptr(k), kv_dtype, s, hkv,
+    qc = q.contiguous()            # bound to a name: alive until the call is enqueued
+    _lib.call("rk_round_scores", _lib.ptr(qc), n_q, hq, d, _lib.ptr(k), kv_dtype, s, hkv,
               _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(items), n_items, n_bins, _lib.ptr(act),
               _lib.ptr(raw), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
     return raw[:n_out]

@@ -214,22 +214,25 @@ def test_engine_round_cache_reuses_slots():
         prev = now
 
 
-def test_grouped_decoder_e2e_staggered_matches_single_engine():
+@pytest.mark.parametrize("stagger", [True, False])
+def test_grouped_decoder_e2e_matches_single_engine(stagger):
     """The bench's serving shape: two dialogue groups on their own streams, the
-    second starting after the first group's first KV gather (stagger), every
-    token's activations loaded from pinned host memory and outputs read back
-    (e2e).  Kept rounds and the last token's outputs equal a standalone engine's
-    eager turn bit for bit."""
+    second starting after the first group's first KV gather (stagger) or both at
+    once (their scoring layers and selections overlap on the device: each engine
+    must own its decode workspace), every token's activations loaded from pinned
+    host memory and outputs read back (e2e).  Kept rounds and the last token's
+    outputs equal a standalone engine's eager turn bit for bit."""
     import dataclasses
 
     from paper_2502_15294_b200.decode_engine import GroupedDecoder
     cfg = EngineConfig(num_layers=4, watershed=2, hq=8, hkv=2, head_dim=128, rounds=7, round_tokens=64,
                        batch=4, decode_steps=5, policy=SelectionPolicy("top_percent", fraction=0.3),
-                       item_chunk=32, input_period=3, plant=2, plant_beta=0.3, question_variants=1)
+                       item_chunk=32, input_period=3, plant=0, question_variants=1)
     gd = GroupedDecoder(cfg, groups=2, seed=11)
-    assert gd.stagger
+    gd.stagger = stagger
+    assert gd.groups[0].ws.data_ptr() != gd.groups[1].ws.data_ptr()
     gd.prepare(e2e=True)
-    gd.run_turns(2, e2e=True)
+    gd.run_turns(3, e2e=True)
     torch.cuda.synchronize()
     sub = dataclasses.replace(cfg, batch=2)
     for g, eng in enumerate(gd.groups):
