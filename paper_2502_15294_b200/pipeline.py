@@ -79,7 +79,13 @@ class TurnMetrics:
     device_used_peak: int
     hist_tokens: int
     hist_tokens_attended: int
+    # the reference's simulated cost fields (costs.py, out of scope: real timings come from CUDA
+    # events in bench.py); kept so TurnMetrics has the reference's field names and order
+    total_cost_us: float | None = None
+    curves: object = None
+    shape: object = None
     distribution: RoundDistribution | None = None
+    token_stats: object = None
     dropped_rounds: tuple = ()
 
 
@@ -93,8 +99,8 @@ class RoundPipeline:
     """Owns one conversation's serving state; strictly sequential per turn."""
 
     def __init__(self, model: Model, watershed: int, *, policy: SelectionPolicy | None = None,
-                 mode: str = "round", store: TieredStore | None = None, drop_window: float = float("inf"),
-                 drop_protect: int = 2, conversation_id: str = "conv0"):
+                 mode: str = "round", store: TieredStore | None = None, cost_model=None,
+                 drop_window: float = float("inf"), drop_protect: int = 2, conversation_id: str = "conv0"):
         if mode not in MODES:
             raise DomainError(f"mode must be one of {MODES}")
         L = model.config.num_layers
@@ -106,6 +112,7 @@ class RoundPipeline:
         self.watershed = watershed
         self.policy = policy
         self.mode = mode
+        self.cost_model = cost_model          # accepted like the reference (cli.py:212-222); not simulated here
         self.store = store or TieredStore(L, watershed, model.config.d_model, conversation_id=conversation_id,
                                           device=model.device)
         self.activity = ActivityLedger(window=drop_window if mode == "round" else float("inf"),

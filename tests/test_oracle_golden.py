@@ -200,3 +200,30 @@ def test_package_calibration_host_math_matches_reference():
     assert cal.kl_divergence([0.5, 0.5], [0.5, 0.5]) == 0.0
     with pytest.raises(cal.DomainError):
         cal.detect_watershed(curves, "nope")
+
+
+def test_package_memory_model_matches_reference():
+    """The product package's Eq. 2 functions (paper_2502_15294_b200.store,
+    store.py:308-357) against the reference's own outputs, bit-exact, plus the
+    reference's validation errors."""
+    from paper_2502_15294_b200 import store as pst
+    from paper_2502_15294_b200.errors import DomainError
+    data = load_store_cases()
+    for m in data["memory"]:
+        if "args" in m:
+            L, lw, K, T = m["args"]
+            assert pst.memory_ratio(L, lw, K, T) == float.fromhex(m["ratio"])
+            assert pst.save_percent(L, lw) == m["save"]
+            fp = pst.footprint_report(1, 1024, 4096, L, lw, K, T)
+            for key, val in m["fp"].items():
+                want = float.fromhex(val) if isinstance(val, str) else val
+                assert fp[key] == want, (key, fp[key], want)
+        else:
+            L, lw = m["table5"]
+            assert pst.save_percent(L, lw) == m["save"] == m["published"]
+    assert pst.block_nbytes(1, 1920, 1) == 7680 and pst.block_nbytes(1, 3200, 1) == 12800
+    for bad in ((4, 0, 1, 8), (4, 4, 1, 8), (4, 2, 9, 8), (4, 2, 1, 0)):
+        with pytest.raises(DomainError):
+            pst.memory_ratio(*bad)
+    with pytest.raises(DomainError):
+        pst.footprint_report(0, 1024, 4096, 32, 5, 4, 32)
