@@ -171,6 +171,41 @@ int rk_select_batch(const double* raw, int n, int ld, int batch, int normalize, 
                     int k_top, double kappa, double* masses_out, int32_t* kept_out, int32_t* n_kept_out,
                     int32_t* degenerate_out, int32_t* status_out, rk_stream_t stream);
 
+/* Decision margin of the selection made from `masses` (rows ld apart):
+ * top_percent (m_(K) - m_(K+1)) / m_(K) of the K-th / (K+1)-th largest masses;
+ * fixed min |m - v| / v; adaptive min |m - cut| / |cut|; all +inf.
+ * margin_out [batch] float64.  The fp32-class scorers (rk_round_scores, the
+ * fused decode / prefill scoring) reproduce the reference's kept set whenever
+ * the margin exceeds twice their relative error; below that the caller
+ * re-scores with rk_round_scores_exact (the engines use 1e-4). */
+int rk_selection_margin(const double* masses, int n, int ld, int batch, int kind, double v, int k_top,
+                        double kappa, double* margin_out, rk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * 4b. Exact (fp64) watershed round scoring with the reference kernel's
+ *    arithmetic (_attn_ext.pyx:52-76,113-114 + stats.py:59-94): logits are the
+ *    same sequential fp64 dot products (every q*k product is exact in fp64, so
+ *    they are bit-identical), softmax statistics per (row, head, round-aligned
+ *    item) in fp64, Eq. 1 masses in fp64 — the kept set is the reference's up
+ *    to fp64 rounding (~1e-16 relative), and identical rounds tie exactly.
+ *    batch dialogues: q [batch][n_q][hq][d] f32; dialogue b's keys start at
+ *    k + b*k_batch_stride elements, [s_b][hkv][d] (s_b = seq_len[b], or s when
+ *    seq_len is NULL); q_pos [n_q] int64 (shared), k_pos [s] int64 or NULL
+ *    (key j at position j); key j is visible to row i iff k_pos[j] <= q_pos[i].
+ *    items [batch][items_stride][3] = (key_lo, key_hi, bin), round-aligned,
+ *    sorted by bin, covering every visible key (bin n_bins = the current
+ *    question); n_items [batch] device or NULL (= items_stride).
+ *    raw_out [batch][n_out]: one float64 per ACTIVE bin (active [n_bins] uint8,
+ *    nullable; n_out = number of active bins).  hq/hkv <= 8, d % 8 == 0.
+ * ---------------------------------------------------------------------- */
+size_t rk_round_scores_exact_workspace_bytes(int batch, int n_q, int hq, int items_stride, int n_bins);
+int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d,
+                          const void* k, int kv_dtype, int hkv, int64_t k_batch_stride,
+                          const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                          const int32_t* items, int items_stride, const int32_t* n_items,
+                          int n_bins, const uint8_t* active, int n_out, double* raw_out,
+                          void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * 5. Batched host->HBM gather of kept rounds' upper-layer blocks
  *    (store.fetch_upper store.py:254-263 + pipeline._assemble :158-169).

@@ -56,3 +56,28 @@ def attention_forward(q, k, v, q_pos, k_pos, allowed=None, capture=False, thread
     if bad >= 0:
         raise InvariantError(f"query row {bad} has no visible key")
     return out, cap
+
+
+def round_masses(q, k, q_pos, k_pos, spans, n_bins, threads=None):
+    """Eq. 1 raw masses per bin from q (n, Hq, d) and K (S, Hkv, d) with the
+    reference kernel's capture arithmetic (attn_ref.c:attn_ref_round_masses);
+    spans = [(key_lo, key_hi, bin)], bins >= n_bins ignored."""
+    import os
+    global _LIB
+    if _LIB is None:
+        _LIB = _lib()
+    fn = _LIB.attn_ref_round_masses
+    fn.restype = None
+    fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                   C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int]
+    q = np.ascontiguousarray(q, np.float32)
+    k = np.ascontiguousarray(k, np.float32)
+    q_pos = np.ascontiguousarray(q_pos, np.int64)
+    k_pos = np.ascontiguousarray(k_pos, np.int64)
+    sp = np.ascontiguousarray(np.asarray(spans, dtype=np.int32).reshape(-1, 3))
+    n, hq, d = q.shape
+    s, hkv = k.shape[0], k.shape[1]
+    raw = np.zeros(n_bins, np.float64)
+    fn(q.ctypes.data, n, hq, d, k.ctypes.data, s, hkv, q_pos.ctypes.data, k_pos.ctypes.data, sp.ctypes.data,
+       len(sp), n_bins, raw.ctypes.data, int(threads or os.cpu_count() or 1))
+    return raw

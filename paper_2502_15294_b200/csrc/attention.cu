@@ -156,9 +156,9 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
                                   const uint8_t* __restrict__ active, double* __restrict__ out_rows) {
   extern __shared__ double sh[];
   double* mass = sh;                                   // [n_bins + 1]
-  float* Mh = reinterpret_cast<float*>(mass + n_bins + 1);   // [hq]
-  float* Lh = Mh + hq;                                 // [hq]
-  int* bin_lo = reinterpret_cast<int*>(Lh + hq);       // [n_bins + 2]
+  double* Lh = mass + n_bins + 1;                      // [hq] fp64 denominators
+  float* Mh = reinterpret_cast<float*>(Lh + hq);       // [hq]
+  int* bin_lo = reinterpret_cast<int*>(Mh + hq);       // [n_bins + 2]
   const int row = blockIdx.x;
   const int32_t* tab = items + (size_t)row * items_stride * 3;
   int n_items = n_items_dev ? n_items_dev[items_stride ? row : 0] : n_items_static;
@@ -172,7 +172,7 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
     for (int it = 0; it < n_slots; ++it)
       L += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - mx);
     Mh[h] = mx;
-    Lh[h] = (float)L;
+    Lh[h] = L;
   }
   if (threadIdx.x == 0) {          // items are sorted by bin: first item of each bin
     int it = 0;
@@ -188,7 +188,7 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
       double hs = 0.0;
       for (int it = bin_lo[b] * slots; it < bin_lo[b + 1] * slots; ++it)
         hs += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - Mh[h]);
-      acc += hs / (double)Lh[h];
+      acc += hs / Lh[h];
     }
     mass[b] = acc;
   }
@@ -220,7 +220,7 @@ __global__ void score_sum_rows_kernel(const double* __restrict__ rows_mass, int 
 }
 
 static size_t score_rows_smem(int n_bins, int hq) {
-  return sizeof(double) * (n_bins + 1) + sizeof(float) * 2 * hq + sizeof(int) * (n_bins + 2);
+  return sizeof(double) * (n_bins + 1 + hq) + sizeof(float) * hq + sizeof(int) * (n_bins + 2);
 }
 
 // the tensor-core multi-row path (prefill_tc.cu) serves bf16 K/V, d = 128,

@@ -1,0 +1,376 @@
+// Exact (fp64) watershed round scoring: the Eq. 1 masses with the reference
+// kernel's arithmetic, so the kept-round indices are bit-exact by
+// construction rather than within a tolerance.
+//
+// Reference (_attn_ext.pyx:52-76, 113-114; stats.py:59-94): for query row i and
+// head h, score_j = (sum_t (double)q[t] * (double)k[j][t]) * (1/sqrt(d)) summed
+// sequentially over t; w_j = exp(score_j - max); p_hj = w_j / sum_j w_j;
+// cap_ij = sum_h p_hj; capn = cap / rowsum; raw_k = sum over the question rows
+// and round k's keys of capn.
+//
+// Here:
+//  * logits: one thread per key, the same sequential fp64 sum over t.  q is fp32
+//    and K fp32 or bf16, so every product q*k is EXACT in fp64 (<= 48 of 53
+//    mantissa bits): an FMA and the reference's separate multiply + add round
+//    identically, and the logits are bit-identical to the reference's;
+//  * per (row, head, round-aligned item): (m, l = sum exp(s - m)) in fp64,
+//    reduced in a fixed tree relative to the item's first key, so identical
+//    rounds get bit-identical statistics wherever they sit (exact ties go to
+//    the lower index, as the reference's stable argsort);
+//  * finalize: per (row, head) M = max m, D = sum l exp(m - M); per bin
+//    sum_h (sum_items l exp(m - M)) / D; rowsum over every bin (the current
+//    question's keys and inactive rounds' keys included, as the reference's
+//    row normalisation); raw = sum over rows of mass / rowsum.
+// The remaining differences from the reference are fp64 roundings in the exp and
+// in the summation order (~1e-16 relative); a kept-set flip needs a K-boundary gap
+// below ~1e-14, which rk_selection_margin reports.
+//
+// Cost (C2, one decode row): 16 K keys x 32 heads x 128 DFMA = 67 M DFMA per
+// dialogue plus one read of layer Lw-1's K (32 MiB): ~5 us per dialogue.
+#include "rk_common.cuh"
+
+namespace rk {
+
+constexpr int kExThreads = 128;
+constexpr int kExMaxG = 8;       // query heads per kv-head handled per block
+constexpr int kExWarps = kExThreads / 32;
+
+template <typename KT>
+struct KLoad;
+
+template <>
+struct KLoad<__nv_bfloat16> {
+  // 8 bf16 -> 8 doubles (exact)
+  static __device__ __forceinline__ void load8(const __nv_bfloat16* p, double* out) {
+    uint4 w = *reinterpret_cast<const uint4*>(p);
+    uint32_t a[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = bf16x2_to_f2(a[i]);
+      out[2 * i] = (double)f.x;
+      out[2 * i + 1] = (double)f.y;
+    }
+  }
+};
+
+template <>
+struct KLoad<float> {
+  static __device__ __forceinline__ void load8(const float* p, double* out) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    float4 b = *reinterpret_cast<const float4*>(p + 4);
+    out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
+    out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+  }
+};
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// grid (items_stride, hkv, batch * row_tiles), block kExThreads.
+// part_m / part_l: [batch][n_q][hq][items_stride] fp64.
+template <typename KT, int RT, int G>
+__global__ void __launch_bounds__(kExThreads) exact_stats_kernel(
+    const float* __restrict__ q, int n_q, int hq, int d, const KT* __restrict__ k, int64_t k_bstride, int hkv,
+    const int32_t* __restrict__ seq_len, int s_static, const int64_t* __restrict__ q_pos,
+    const int64_t* __restrict__ k_pos, const int32_t* __restrict__ items, int items_stride,
+    const int32_t* __restrict__ n_items_dev, double scale, int row_tiles, double* __restrict__ part_m,
+    double* __restrict__ part_l) {
+  extern __shared__ double qs[];                       // [RT][G][d]
+  __shared__ double red[kExWarps][RT * G];
+  __shared__ double run_m[RT * G], run_l[RT * G], sub_m[RT * G];
+  const int it = blockIdx.x, g = blockIdx.y;
+  const int b = blockIdx.z / row_tiles;
+  const int r0 = (blockIdx.z % row_tiles) * RT;
+  const int n_items = n_items_dev ? n_items_dev[b] : items_stride;
+  if (it >= n_items) return;
+  const int32_t* tab = items + ((size_t)b * items_stride + it) * 3;
+  const int s_b = seq_len ? seq_len[b] : s_static;
+  const int lo = tab[0];
+  const int hi = min(tab[1], s_b);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nr = min(RT, n_q - r0);
+
+  for (int x = tid; x < RT * G * d; x += kExThreads) {
+    const int r = x / (G * d), rem = x - r * G * d;
+    const int h = rem / d, t = rem - h * d;
+    qs[x] = r < nr ? (double)q[(((size_t)b * n_q + r0 + r) * hq + g * G + h) * d + t] : 0.0;
+  }
+  for (int x = tid; x < RT * G; x += kExThreads) {
+    run_m[x] = -INFINITY;
+    run_l[x] = 0.0;
+  }
+  int64_t qp[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) qp[r] = r < nr ? q_pos[r0 + r] : INT64_MIN;
+  __syncthreads();
+
+  const KT* kb = k + (size_t)b * k_bstride + (size_t)g * d;
+  const int64_t row_stride = (int64_t)hkv * d;
+  for (int c0 = lo; c0 < hi; c0 += kExThreads) {
+    const int j = c0 + tid;
+    const bool in = j < hi;
+    const int64_t kp = in ? (k_pos ? k_pos[j] : (int64_t)j) : 0;
+    double acc[RT][G];
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int h = 0; h < G; ++h) acc[r][h] = 0.0;
+    if (in) {
+      const KT* kr = kb + (int64_t)j * row_stride;
+      for (int t0 = 0; t0 < d; t0 += 8) {
+        double kv[8];
+        KLoad<KT>::load8(kr + t0, kv);
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+#pragma unroll
+          for (int r = 0; r < RT; ++r) {
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              // sequential over t as the reference; the product is exact in fp64
+              acc[r][h] = __fma_rn(qs[(r * G + h) * d + t0 + tt], kv[tt], acc[r][h]);
+            }
+          }
+        }
+      }
+    }
+    // logits (masked keys -> -inf), sub-chunk max per (row, head)
+    double s[RT][G];
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const bool vis = in && kp <= qp[r];
+        s[r][h] = vis ? __dmul_rn(acc[r][h], scale) : -INFINITY;
+        double m = warp_max_d(s[r][h]);
+        if (lane == 0) red[warp][r * G + h] = m;
+      }
+    __syncthreads();
+    if (tid < RT * G) {
+      double m = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kExWarps; ++w) m = fmax(m, red[w][tid]);
+      sub_m[tid] = m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const double m = sub_m[r * G + h];
+        double e = (s[r][h] == -INFINITY) ? 0.0 : exp(__dsub_rn(s[r][h], m));
+        e = warp_sum_d(e);
+        if (lane == 0) red[warp][r * G + h] = e;
+      }
+    __syncthreads();
+    if (tid < RT * G) {
+      double l = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kExWarps; ++w) l = __dadd_rn(l, red[w][tid]);
+      const double m = sub_m[tid];
+      if (m != -INFINITY) {
+        const double M = run_m[tid];
+        if (M == -INFINITY) {
+          run_m[tid] = m;
+          run_l[tid] = l;
+        } else if (m > M) {
+          run_l[tid] = __fma_rn(run_l[tid], exp(__dsub_rn(M, m)), l);
+          run_m[tid] = m;
+        } else {
+          run_l[tid] = __fma_rn(l, exp(__dsub_rn(m, M)), run_l[tid]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < RT * G) {
+    const int r = tid / G, h = tid % G;
+    if (r < nr) {
+      const size_t o = (((size_t)b * n_q + r0 + r) * hq + g * G + h) * items_stride + it;
+      part_m[o] = run_m[tid];
+      part_l[o] = run_l[tid];
+    }
+  }
+}
+
+// one block per (dialogue, row): row mass per bin / rowsum -> rowmass[b][row][bin]
+__global__ void exact_rows_kernel(const double* __restrict__ part_m, const double* __restrict__ part_l, int n_q,
+                                  int hq, const int32_t* __restrict__ items, int items_stride,
+                                  const int32_t* __restrict__ n_items_dev, int n_bins,
+                                  double* __restrict__ rowmass) {
+  extern __shared__ double sh[];
+  double* mass = sh;                       // [n_bins + 1]
+  double* Mh = mass + n_bins + 1;          // [hq]
+  double* Dh = Mh + hq;                    // [hq]
+  int* bin_lo = reinterpret_cast<int*>(Dh + hq);   // [n_bins + 2]
+  const int b = blockIdx.x / n_q, row = blockIdx.x % n_q;
+  const int n_items = n_items_dev ? n_items_dev[b] : items_stride;
+  const int32_t* tab = items + (size_t)b * items_stride * 3;
+  const double* pm = part_m + ((size_t)b * n_q + row) * hq * items_stride;
+  const double* pl = part_l + ((size_t)b * n_q + row) * hq * items_stride;
+  for (int h = threadIdx.x; h < hq; h += blockDim.x) {
+    double mx = -INFINITY;
+    for (int it = 0; it < n_items; ++it) mx = fmax(mx, pm[h * items_stride + it]);
+    double D = 0.0;
+    for (int it = 0; it < n_items; ++it) {
+      const double m = pm[h * items_stride + it];
+      if (m != -INFINITY) D = __fma_rn(pl[h * items_stride + it], exp(__dsub_rn(m, mx)), D);
+    }
+    Mh[h] = mx;
+    Dh[h] = D;
+  }
+  if (threadIdx.x == 0) {                  // items are sorted by bin: first item of each bin
+    int it = 0;
+    for (int bn = 0; bn <= n_bins + 1; ++bn) {
+      while (it < n_items && tab[it * 3 + 2] < bn) ++it;
+      bin_lo[bn] = it;
+    }
+  }
+  __syncthreads();
+  for (int bn = threadIdx.x; bn <= n_bins; bn += blockDim.x) {
+    double acc = 0.0;
+    for (int h = 0; h < hq; ++h) {         // head order as the reference's cap accumulation
+      if (Dh[h] <= 0.0) continue;
+      double hs = 0.0;
+      for (int it = bin_lo[bn]; it < bin_lo[bn + 1]; ++it) {
+        const double m = pm[h * items_stride + it];
+        if (m != -INFINITY) hs = __fma_rn(pl[h * items_stride + it], exp(__dsub_rn(m, Mh[h])), hs);
+      }
+      acc = __dadd_rn(acc, __ddiv_rn(hs, Dh[h]));
+    }
+    mass[bn] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int bn = 0; bn <= n_bins; ++bn) tot = __dadd_rn(tot, mass[bn]);
+    double* out = rowmass + ((size_t)b * n_q + row) * n_bins;
+    for (int bn = 0; bn < n_bins; ++bn) out[bn] = tot > 0.0 ? __ddiv_rn(mass[bn], tot) : 0.0;
+  }
+}
+
+// raw[b][a] over active bins (ascending) = sum over rows (in order) of rowmass
+__global__ void exact_sum_rows_kernel(const double* __restrict__ rowmass, int n_q, int n_bins,
+                                      const uint8_t* __restrict__ active, int n_out, double* __restrict__ raw) {
+  const int b = blockIdx.y;
+  const int bn = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bn >= n_bins) return;
+  if (active && !active[bn]) return;
+  int a = bn;
+  if (active) {
+    a = 0;
+    for (int x = 0; x < bn; ++x) a += active[x] ? 1 : 0;
+  }
+  double acc = 0.0;
+  for (int r = 0; r < n_q; ++r) acc = __dadd_rn(acc, rowmass[((size_t)b * n_q + r) * n_bins + bn]);
+  raw[(size_t)b * n_out + a] = acc;
+}
+
+static size_t exact_ws_parts(int batch, int n_q, int hq, int items_stride, int n_bins, size_t* off_l,
+                             size_t* off_rows) {
+  const size_t part = align_up(sizeof(double) * (size_t)batch * n_q * hq * items_stride, 256);
+  *off_l = part;
+  *off_rows = 2 * part;
+  return 2 * part + align_up(sizeof(double) * (size_t)batch * n_q * n_bins, 256);
+}
+
+template <typename KT, int RT, int G>
+static int launch_exact_stats_g(const float* q, int batch, int n_q, int hq, int d, const void* k, int64_t k_bstride,
+                                int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                                const int32_t* items, int items_stride, const int32_t* n_items, double scale,
+                                double* pm, double* pl, cudaStream_t st) {
+  const int row_tiles = (n_q + RT - 1) / RT;
+  dim3 grid(items_stride, hkv, batch * row_tiles);
+  const size_t smem = sizeof(double) * RT * G * d;
+  auto kern = exact_stats_kernel<KT, RT, G>;
+  if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                                "exact_stats smem");
+  kern<<<grid, kExThreads, smem, st>>>(q, n_q, hq, d, reinterpret_cast<const KT*>(k), k_bstride, hkv, seq_len, s,
+                                       q_pos, k_pos, items, items_stride, n_items, scale, row_tiles, pm, pl);
+  RK_CHECK_LAUNCH("exact_stats_kernel");
+  return RK_OK;
+}
+
+template <typename KT, int RT>
+static int launch_exact_stats(const float* q, int batch, int n_q, int hq, int d, const void* k, int64_t k_bstride,
+                              int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                              const int32_t* items, int items_stride, const int32_t* n_items, double scale,
+                              double* pm, double* pl, cudaStream_t st) {
+#define RK_EXACT_G(GG)                                                                                          \
+  case GG:                                                                                                      \
+    return launch_exact_stats_g<KT, RT, GG>(q, batch, n_q, hq, d, k, k_bstride, hkv, seq_len, s, q_pos, k_pos,  \
+                                            items, items_stride, n_items, scale, pm, pl, st);
+  switch (hq / hkv) {
+    RK_EXACT_G(1) RK_EXACT_G(2) RK_EXACT_G(3) RK_EXACT_G(4) RK_EXACT_G(5) RK_EXACT_G(6) RK_EXACT_G(7) RK_EXACT_G(8)
+    default:
+      return fail(RK_ERR_DOMAIN, "exact scoring: group %d", hq / hkv);
+  }
+#undef RK_EXACT_G
+}
+
+}  // namespace rk
+
+using namespace rk;
+
+extern "C" {
+
+size_t rk_round_scores_exact_workspace_bytes(int batch, int n_q, int hq, int items_stride, int n_bins) {
+  size_t a, b;
+  return exact_ws_parts(batch, n_q, hq, items_stride, n_bins, &a, &b);
+}
+
+int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d, const void* k, int kv_dtype, int hkv,
+                          int64_t k_batch_stride, const int32_t* seq_len, int s, const int64_t* q_pos,
+                          const int64_t* k_pos, const int32_t* items, int items_stride, const int32_t* n_items,
+                          int n_bins, const uint8_t* active, int n_out, double* raw_out, void* workspace,
+                          size_t workspace_bytes, rk_stream_t stream) {
+  if (batch <= 0 || n_q <= 0 || n_bins <= 0) return RK_OK;
+  if (hkv <= 0 || hq % hkv != 0 || hq / hkv > kExMaxG)
+    return fail(RK_ERR_DOMAIN, "exact scoring: %d query heads over %d kv-heads (group <= %d)", hq, hkv, kExMaxG);
+  if (d <= 0 || d % 8 != 0 || d > 256) return fail(RK_ERR_DOMAIN, "exact scoring: head_dim %d (multiple of 8, <= 256)", d);
+  if (kv_dtype != RK_F32 && kv_dtype != RK_BF16) return fail(RK_ERR_DOMAIN, "kv dtype %d", kv_dtype);
+  if (items == nullptr || items_stride <= 0 || q_pos == nullptr || raw_out == nullptr)
+    return fail(RK_ERR_DOMAIN, "exact scoring needs items, q_pos and raw_out");
+  size_t off_l, off_rows;
+  const size_t need = exact_ws_parts(batch, n_q, hq, items_stride, n_bins, &off_l, &off_rows);
+  if (workspace_bytes < need) return fail(RK_ERR_CAPACITY, "exact scoring workspace %zu < %zu", workspace_bytes, need);
+  char* ws = reinterpret_cast<char*>(workspace);
+  double* pm = reinterpret_cast<double*>(ws);
+  double* pl = reinterpret_cast<double*>(ws + off_l);
+  double* rows = reinterpret_cast<double*>(ws + off_rows);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const double scale = 1.0 / sqrt((double)d);        // the reference's inv_scale (_attn_ext.pyx:36)
+  int rc;
+  if (kv_dtype == RK_BF16)
+    rc = n_q == 1 ? launch_exact_stats<__nv_bfloat16, 1>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s,
+                                                         q_pos, k_pos, items, items_stride, n_items, scale, pm, pl, st)
+                  : launch_exact_stats<__nv_bfloat16, 4>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s,
+                                                         q_pos, k_pos, items, items_stride, n_items, scale, pm, pl, st);
+  else
+    rc = n_q == 1 ? launch_exact_stats<float, 1>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos,
+                                                 k_pos, items, items_stride, n_items, scale, pm, pl, st)
+                  : launch_exact_stats<float, 4>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos,
+                                                 k_pos, items, items_stride, n_items, scale, pm, pl, st);
+  if (rc != RK_OK) return rc;
+  const size_t smem = sizeof(double) * (n_bins + 1 + 2 * hq) + sizeof(int) * (n_bins + 2);
+  if (smem > 48 * 1024) {
+    RK_CUDA(cudaFuncSetAttribute(exact_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "exact_rows smem");
+  }
+  exact_rows_kernel<<<batch * n_q, 128, smem, st>>>(pm, pl, n_q, hq, items, items_stride, n_items, n_bins, rows);
+  RK_CHECK_LAUNCH("exact_rows_kernel");
+  dim3 g2((n_bins + 127) / 128, batch);
+  exact_sum_rows_kernel<<<g2, 128, 0, st>>>(rows, n_q, n_bins, active, n_out, raw_out);
+  RK_CHECK_LAUNCH("exact_sum_rows_kernel");
+  return RK_OK;
+}
+
+}  // extern "C"

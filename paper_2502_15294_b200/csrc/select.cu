@@ -121,6 +121,69 @@ __global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int
   }
 }
 
+// Decision margin of one selection (relative distance of the deciding masses
+// from the decision threshold; +inf when nothing is decided by a comparison):
+//   top_percent: (m_(K) - m_(K+1)) / m_(K), the K-th and (K+1)-th largest masses;
+//   fixed:       min_i |m_i - v| / v;
+//   adaptive:    min_i |m_i - cut| / |cut|, cut = mean + kappa * std;
+//   all:         +inf.
+// A kept set computed from masses accurate to a relative error e is the
+// reference's kept set whenever margin > 2e (exact ties, margin 0, are decided
+// by index on both sides when the masses tie exactly).
+__global__ void margin_kernel(const double* __restrict__ masses, int n, int ld, int kind, double v, int k_top,
+                              double kappa, double* __restrict__ margin) {
+  masses += (size_t)blockIdx.x * ld;
+  __shared__ double red[256];
+  __shared__ double s_cut, s_a, s_b;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    s_a = -1.0;
+    s_b = -1.0;
+    if (kind == RK_SEL_ADAPTIVE) {
+      double mean = __ddiv_rn(pw_sum([&](int i) { return masses[i]; }, 0, n), (double)n);
+      double var = __ddiv_rn(pw_sum([&](int i) {
+                               double dv = __dsub_rn(masses[i], mean);
+                               return __dmul_rn(dv, dv);
+                             }, 0, n), (double)n);
+      s_cut = __dadd_rn(mean, __dmul_rn(kappa, __dsqrt_rn(var)));
+    } else {
+      s_cut = v;
+    }
+  }
+  __syncthreads();
+  double best = INFINITY;
+  if (kind == RK_SEL_TOP_PERCENT) {
+    if (k_top > 0 && k_top < n) {
+      for (int i = t; i < n; i += blockDim.x) {    // stable rank as select_kernel
+        const double mi = masses[i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+          const double mj = masses[j];
+          rank += (mj > mi) || (mj == mi && j < i);
+        }
+        if (rank == k_top - 1) s_a = mi;
+        if (rank == k_top) s_b = mi;
+      }
+    }
+  } else if (kind == RK_SEL_FIXED || kind == RK_SEL_ADAPTIVE) {
+    const double cut = s_cut;
+    const double den = fabs(cut) > 0.0 ? fabs(cut) : 1.0;
+    for (int i = t; i < n; i += blockDim.x) best = fmin(best, fabs(masses[i] - cut) / den);
+  }
+  red[t] = best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (t < o) red[t] = fmin(red[t], red[t + o]);
+    __syncthreads();
+  }
+  if (t == 0) {
+    double m = red[0];
+    if (kind == RK_SEL_TOP_PERCENT && k_top > 0 && k_top < n)
+      m = s_a > 0.0 ? (s_a - s_b) / s_a : 0.0;
+    margin[blockIdx.x] = m;
+  }
+}
+
 __global__ void aggregate_kernel(const double* __restrict__ scores, int64_t ld, int row_lo, int row_hi,
                                  const int64_t* __restrict__ spans, double* __restrict__ raw) {
   __shared__ double red[256];
@@ -169,6 +232,17 @@ int rk_select_batch(const double* raw, int n, int ld, int batch, int normalize, 
   select_kernel<<<batch, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       raw, n, ld, normalize, kind, v, k_top, kappa, masses_out, kept_out, n_kept_out, degenerate_out, status_out);
   RK_CHECK_LAUNCH("select_kernel");
+  return RK_OK;
+}
+
+int rk_selection_margin(const double* masses, int n, int ld, int batch, int kind, double v, int k_top,
+                        double kappa, double* margin_out, rk_stream_t stream) {
+  if (n < 0 || n > kSelMax || ld < n) return fail(RK_ERR_DOMAIN, "selection over %d rounds (max %d)", n, kSelMax);
+  if (kind < RK_SEL_FIXED || kind > RK_SEL_ALL) return fail(RK_ERR_DOMAIN, "selection kind %d unknown", kind);
+  if (batch <= 0) return RK_OK;
+  margin_kernel<<<batch, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(masses, n, ld, kind, v, k_top, kappa,
+                                                                           margin_out);
+  RK_CHECK_LAUNCH("margin_kernel");
   return RK_OK;
 }
 

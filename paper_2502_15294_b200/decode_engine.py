@@ -64,6 +64,8 @@ class EngineConfig:
     round_cache: bool = True      # keep rounds kept again in their working-cache slots (no re-fetch)
     question_variants: int = 4    # distinct questions cycled over turns (noisy copies of question 0)
     question_noise: float = 1.0   # variants about as far from question 0 as it is long
+    refine_margin: float = 1e-3   # multi-row questions: re-score in fp64 when the K-boundary gap of the
+                                  # fp32-class fused scoring is below this (1-row questions always score in fp64)
 
     @property
     def group(self) -> int:
@@ -179,6 +181,13 @@ class RoundDecodeEngine:
         # groups run concurrently on their own streams, so nothing here may be shared between engines
         ws_bytes = _lib.lib.rk_decode_workspace_bytes(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8))
         self.ws = torch.zeros(max(256, int(ws_bytes)), dtype=torch.uint8, device=self.dev)
+        ex_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, nq, c.hq, self.items.shape[1], R)
+        self.ws_exact = torch.zeros(max(256, int(ex_bytes)), dtype=torch.uint8, device=self.dev)
+        self.q_pos_1 = torch.full((1,), self.hist, dtype=torch.int64, device=self.dev)
+        self.margin = torch.zeros(B, dtype=torch.float64, device=self.dev)
+        self.margin_host = torch.zeros(B, dtype=torch.float64, pin_memory=True)
+        self.min_margin = math.inf            # smallest K-boundary margin seen (fp64 masses)
+        self.refined_turns = 0                # multi-row turns re-scored in fp64
         self.copy_stream = torch.cuda.Stream(self.dev)
         self.compute_stream = torch.cuda.Stream(self.dev)
         # torch creates CUDA events lazily: record once so the handles exist
@@ -267,22 +276,45 @@ class RoundDecodeEngine:
     def launches_question_token(self) -> int:
         """Kernels of the 1-row question token (_phase_a + _phase_b1)."""
         c = self.cfg
-        return sum(self._layer_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1),
-                                        items=(l == c.watershed - 1)) for l in range(c.num_layers))
+        return sum(self._layer_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
+                   for l in range(c.num_layers))
 
     def _phase_a(self):
-        """Question through the lower layers, fused scoring, selection."""
+        """Question through the lower layers, watershed scoring, selection.
+
+        A 1-row question is scored exactly: after layer Lw-1 appended the
+        question's key, rk_round_scores_exact recomputes the layer's logits with
+        the reference kernel's fp64 arithmetic (one extra read of that layer's
+        keys, ~5 us per dialogue), so the kept rounds are the reference's by
+        construction, not within a tolerance."""
         if self.nq > 1:
             return self._phase_a_prefill()
         c = self.cfg
         self.lower_len.copy_(self.lower_len0)
         self.upper_len.copy_(self.upper_len0)
         for l in range(c.watershed):
-            self._layer(l, 0, advance=(l == c.watershed - 1), items=(l == c.watershed - 1))
-        kernels.decode_scores_finalize(c.batch, c.hq, c.hkv, c.head_dim, self.items, self.n_items, c.rounds,
-                                       self.ws, raw=self.raw, kv_dtype=self.dtype)
-        self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(
-            self.raw, "top_percent", k_top=self.K)
+            self._layer(l, 0, advance=(l == c.watershed - 1))
+        lw1 = c.watershed - 1
+        kernels.round_scores_exact(self.q_in[0, lw1].unsqueeze(1), self.lower[:, lw1, 0], self.q_pos_1, self.items,
+                                   c.rounds, seq_len=self.lower_len, n_items=self.n_items, raw=self.raw,
+                                   ws=self.ws_exact)
+        self._select()
+
+    def _select(self):
+        self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(self.raw, "top_percent", k_top=self.K)
+        kernels.selection_margin(self.masses, "top_percent", k_top=self.K, out=self.margin)
+
+    def _refine_exact(self):
+        """Multi-row question whose fused fp32-class scoring left a K-boundary
+        gap below cfg.refine_margin: re-score every dialogue of the group with
+        rk_round_scores_exact (fp64, the reference's arithmetic) and select
+        again (eager, on the current stream)."""
+        c = self.cfg
+        lw1 = c.watershed - 1
+        kernels.round_scores_exact(self.qq_in[lw1], self.lower[:, lw1, 0], self.q_pos, self.items, c.rounds,
+                                   seq_len=self.lower_len, n_items=self.n_items, raw=self.raw, ws=self.ws_exact)
+        self._select()
+        self.refined_turns += 1
 
     # ---- multi-row question: tensor-core prefill (rk_prefill_attention) ------
     def _phase_a_prefill(self):
@@ -301,7 +333,7 @@ class RoundDecodeEngine:
                     items=self.items[b, :self.n_items_host[b]] if last else None,
                     n_bins=c.rounds if last else 0, raw=self.raw[b] if last else None)
         self.lower_len.copy_(self.lower_len_q)
-        self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(self.raw, "top_percent", k_top=self.K)
+        self._select()
 
     def _phase_b1_prefill(self, kept, layer_wait: bool):
         """n_q question rows through the upper layers over the kept rounds +
@@ -512,12 +544,17 @@ class RoundDecodeEngine:
                     self._phase_b2(e2e=True)
         torch.cuda.synchronize()
 
-    def _select_to_host(self):
+    def _select_to_host(self, refine: bool = True):
         self.kept_host.copy_(self.kept_pos, non_blocking=True)
         self.meta_host.copy_(self.sel_meta, non_blocking=True)
+        self.margin_host.copy_(self.margin, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         if int(self.meta_host[2].abs().sum()) != 0:
             raise RuntimeError("selection reported a negative raw mass")
+        if refine and self.nq > 1 and float(self.margin_host.min()) < self.cfg.refine_margin:
+            self._refine_exact()
+            return self._select_to_host(refine=False)
+        self.min_margin = min(self.min_margin, float(self.margin_host.min()))
         kept = []
         for b in range(self.cfg.batch):
             n = int(self.meta_host[0, b])
@@ -609,9 +646,9 @@ class RoundDecodeEngine:
         c = self.cfg
         answer = self.launches_per_token() * c.decode_steps
         if self.nq > 1:   # prefill per (layer, dialogue): bad-row fill, q prep, tcgen05 pass, merge (+2 scoring)
-            return c.num_layers * c.batch * 4 + 2 * c.batch + answer + 1
+            return c.num_layers * c.batch * 4 + 2 * c.batch + answer + 2       # + select + margin
         return (self.launches_question_token() + answer
-                + 2)                                    # score finalize + batched select
+                + 3 + 2)                                # exact scorer (3 kernels) + select + margin
 
     # ------------------------------------------------------------------ accounting
     def kv_bytes_per_token(self) -> int:

@@ -94,6 +94,46 @@ def select_batch(raw: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, nor
     return masses, kept, meta
 
 
+def selection_margin(masses: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, out=None, stream=None):
+    """rk_selection_margin over rows of a (B, n) float64 device tensor of masses:
+    the relative distance of the deciding masses from the decision threshold
+    (top_percent: (m_(K) - m_(K+1)) / m_(K)).  Returns (B,) float64 device."""
+    masses = masses.contiguous()
+    B, n = masses.shape
+    if out is None:
+        out = torch.empty(B, dtype=torch.float64, device=masses.device)
+    _lib.call("rk_selection_margin", _lib.ptr(masses), n, n, B, _lib.SEL_KINDS[kind], float(v), int(k_top),
+              float(kappa), _lib.ptr(out), _lib.stream_ptr(stream))
+    return out
+
+
+def round_scores_exact(q: torch.Tensor, k_cache: torch.Tensor, q_pos: torch.Tensor, items: torch.Tensor,
+                       n_bins: int, *, seq_len: torch.Tensor | None = None, n_items: torch.Tensor | None = None,
+                       k_pos: torch.Tensor | None = None, active: torch.Tensor | None = None,
+                       raw: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Exact (fp64) Eq. 1 masses for B dialogues (rk_round_scores_exact).
+
+    q (B, n_q, Hq, d) f32; k_cache (B, S_cap, Hkv, d) with any batch stride
+    (layer Lw-1 keys); q_pos (n_q,) int64 device; items (B, n_items_max, 3)
+    int32 round-aligned (bin n_bins = the question) + n_items (B,) int32;
+    seq_len (B,) int32 = visible keys per dialogue (None: S_cap); k_pos (S,)
+    int64 or None (key j at position j).  Returns raw (B, n_active) float64."""
+    B, n_q, hq, d = q.shape
+    hkv = k_cache.shape[2]
+    stride = k_cache.stride(0)
+    n_out = n_bins if active is None else int(active.sum().item())
+    if raw is None:
+        raw = torch.empty((B, max(1, n_out)), dtype=torch.float64, device=q.device)
+    if ws is None:
+        nbytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, n_q, hq, items.shape[1], n_bins)
+        ws = scratch(nbytes, q.device, "scores_exact")
+    _lib.call("rk_round_scores_exact", _lib.ptr(q), B, n_q, hq, d, _lib.ptr(k_cache), kv_code(k_cache), hkv, stride,
+              _lib.ptr(seq_len), k_cache.shape[1], _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(items), items.shape[1],
+              _lib.ptr(n_items), n_bins, _lib.ptr(active), max(1, n_out), _lib.ptr(raw), _lib.ptr(ws), ws.numel(),
+              _lib.stream_ptr(stream))
+    return raw
+
+
 def advance_lengths(seq_len: torch.Tensor, delta: int = 1, stream=None) -> None:
     _lib.call("rk_advance_lengths", _lib.ptr(seq_len), seq_len.numel(), int(delta), _lib.stream_ptr(stream))
 

@@ -151,12 +151,16 @@ def build_round_items(bounds, chunk: int = 256):
     return np.asarray(items, dtype=np.int32).reshape(-1, 3)
 
 
-def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: int = 256):
+def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: int = 256, exact: bool = True):
     """Fused capture + Eq. 1: raw mass per ACTIVE prior round (float64, device).
 
     q: (n_q, Hq, d) float32 cuda; k: (S, Hkv, d) fp32/bf16 cuda (layer Lw-1
     keys, ascending positions); key_bounds: [(lo, hi, bin)] covering [0, S)
     with bin == n_bins for the current round's keys (denominator only).
+    exact=True (default): rk_round_scores_exact, the reference kernel's fp64
+    arithmetic (kept sets bit-exact by construction); exact=False: the
+    fp32-class rk_round_scores (tcgen05 scores-only pass for large bf16
+    questions).
     """
     torch, dev = _device()
     n_q, hq, d = q.shape
@@ -171,6 +175,17 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
         act = torch.from_numpy(a).to(dev)
     raw = torch.zeros(max(n_out, 1), dtype=torch.float64, device=dev)
     kv_dtype = _lib.RK_BF16 if k.dtype == torch.bfloat16 else _lib.RK_F32
+    if exact:
+        q_pos = torch.as_tensor(q_pos, dtype=torch.int64, device=dev)
+        k_pos = torch.as_tensor(k_pos, dtype=torch.int64, device=dev)
+        qc = q.contiguous().float()
+        kc = k.contiguous()
+        ws_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(1, n_q, hq, n_items, n_bins)
+        ws = scratch(ws_bytes, dev, "scores_exact")
+        _lib.call("rk_round_scores_exact", _lib.ptr(qc), 1, n_q, hq, d, _lib.ptr(kc), kv_dtype, hkv, 0, None, s,
+                  _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(items), n_items, None, n_bins, _lib.ptr(act),
+                  max(n_out, 1), _lib.ptr(raw), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        return raw[:n_out]
     ws_bytes = _lib.lib.rk_round_scores_workspace_bytes(n_q, hq, hkv, n_items, d, n_bins)
     ws = scratch(ws_bytes, dev, "scores")
     q_pos = torch.as_tensor(q_pos, dtype=torch.int64, device=dev)
