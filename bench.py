@@ -1,22 +1,29 @@
-"""Round-Attention decode benchmark (B200, sm_100a).
+"""Round-Attention serving benchmark (B200, sm_100a).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4]
                     [--batch B] [--decode-steps T] [--impl ours|reference]
 
-A "step" is one serving TURN for every dialogue on the GPU: the question token
-through the lower layers with fused watershed scoring (layer Lw-1), device
-round selection, the kept rounds' deep-layer KV gathered from pinned host
-memory, the question's upper layers, then T answer tokens through all L
-layers (BASELINE.json north star).  `value` = decode tokens/s
-of the whole job (B * (T + 1) tokens per turn per GPU, summed over GPUs) with
-per-token activations already in HBM; `e2e` = the same with every token's
-q/k/v read from pinned host memory and every layer's attention output written
-back to host inside the timed region.  Dialogues are independent: each rank
-runs its own batch (weak scaling, no collective on the data path).
+A "step" is one serving TURN for every dialogue on the GPU, with the model
+(the reference's attention + residual transformer, engine.py:146-287, at the
+Llama-3-8B / Qwen2-7B shapes with bf16 weights) running every token on the GPU:
+the question through the lower layers (fused QKV projection + RoPE + KV append,
+decode attention, output projection per layer), exact fp64 watershed scoring at
+layer Lw-1, device round selection, the kept rounds' deep-layer KV gathered
+from pinned host memory, the question's upper layers, then T greedy answer
+tokens (SEP + argmax of the tied logits) through all L layers (BASELINE.json
+north star).  `value` = decode tokens/s of the whole job
+(B * (T + 1) tokens per turn per GPU, summed over GPUs) with the questions
+already in HBM; `e2e` = the same through the public turn API: every turn's
+question ids come from pinned host memory and its answer ids (plus the kept
+ids and the new round's KV writeback) go back to it.  Dialogues are
+independent: each rank runs its own batch (weak scaling, no collective on the
+data path).
 
 Under torchrun (N > 1) every rank runs its own engine; rank 0 prints ONE JSON
-line with the max-over-ranks device time.  `--impl reference` times the
-reference's own CPU kernel (oracle/_ref, else the C port) on the host cores.
+line with the max-over-ranks device time.  RK_SHARE_GPU=1 maps every rank to
+GPU local_rank % device_count (the multi-rank path on a one-GPU box; the
+barrier then runs on gloo).  `--impl reference` times the reference package's
+own CPU path (oracle/_ref) on the host cores.
 """
 
 from __future__ import annotations
@@ -37,13 +44,15 @@ WORKLOADS = {
     # Llama-3-8B-shaped GQA, 32 rounds x 512 tokens, single-token decode (BASELINE configs[1]);
     # 32 independent dialogues per GPU served as 2 groups of 16 (8 GPUs x 32 = the 256-dialogue end of
     # the configs[4] batch sweep); --batch 1 --groups 1 for a single dialogue
+    # every dialogue has its own pinned host rounds (32 x 32 x 54 MiB = 55 GiB of the box's 196 GB)
     "c2": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=32, round_tokens=512, batch=32,
-               decode_steps=128, host_unique=4),
+               decode_steps=128, host_unique=0),
     # Qwen2-7B-shaped, 64 rounds x 1K tokens, 512-row question: tcgen05 prefill of the lower layers with the
     # round scoring fused at layer Lw-1, then the upper layers over the kept rounds, then 128 answer tokens
     "c3": dict(num_layers=28, watershed=10, hq=28, hkv=4, head_dim=128, rounds=64, round_tokens=1024, batch=8,
-               decode_steps=128, host_unique=2, question_rows=512),
-    # Llama-3-8B-shaped 128K context, 16 dialogues, deep layers in pinned host memory
+               decode_steps=128, host_unique=0, question_rows=512),
+    # Llama-3-8B-shaped 128K context, 16 dialogues, deep layers in pinned host memory; unique host rounds
+    # would need 16 x 128 x 108 MiB = 216 GiB > the box's 196 GB, so 2 host round sets are shared (aliased)
     "c4": dict(num_layers=32, watershed=5, hq=32, hkv=8, head_dim=128, rounds=128, round_tokens=1024, batch=16,
                decode_steps=64, host_unique=2),
 }
@@ -60,10 +69,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--question-noise", type=float, default=None,
-                    help="per-turn question variation (EngineConfig.question_noise)")
-    ap.add_argument("--input-period", type=int, default=None,
-                    help="per-token input slots (EngineConfig.input_period; e2e loads run P-2 tokens ahead)")
+    ap.add_argument("--host-unique", type=int, default=None,
+                    help="distinct pinned host round sets (0 = one per dialogue)")
+    ap.add_argument("--no-fetch-all", action="store_true",
+                    help="skip the reference transfer pattern pass (every kept round fetched every turn)")
     ap.add_argument("--no-round-cache", action="store_true",
                     help="fetch every kept round every turn (the reference's transfer pattern)")
     ap.add_argument("--groups", type=int, default=None,
@@ -199,11 +208,16 @@ def main():
     import torch.distributed as dist
 
     from paper_2502_15294_b200.decode_engine import EngineConfig, GroupedDecoder
-    from paper_2502_15294_b200.sharding import dialogues_for_rank, max_over_ranks
+    from paper_2502_15294_b200.sharding import bind_numa_local, dialogues_for_rank, gpu_for_rank, max_over_ranks
 
-    torch.cuda.set_device(local)
+    dev_index, shared = gpu_for_rank(local)
+    torch.cuda.set_device(dev_index)
+    numa = bind_numa_local(dev_index)            # pinned host pools are allocated NUMA-local to the GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:       # several ranks on one GPU (a one-GPU box): NCCL refuses duplicate devices
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
     w = dict(WORKLOADS[args.workload])
     if args.batch:
         w["batch"] = args.batch
@@ -211,17 +225,15 @@ def main():
         w["decode_steps"] = args.decode_steps
     if args.no_round_cache:
         w["round_cache"] = False
-    if args.question_noise is not None:
-        w["question_noise"] = args.question_noise
-    if args.input_period:
-        w["input_period"] = args.input_period
+    if args.host_unique is not None:
+        w["host_unique"] = args.host_unique
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
     groups = args.groups if args.groups else (2 if cfg.batch >= 2 and cfg.batch % 2 == 0 else 1)
-    eng = GroupedDecoder(cfg, groups=groups, seed=1000 * shard[0])
+    eng = GroupedDecoder(cfg, groups=groups, dialogues=shard)
     eng.prepare(e2e=not args.no_e2e)
-    link_peak = pcie_h2d_peak(torch, local)
+    link_peak = pcie_h2d_peak(torch, dev_index)
 
     def barrier():
         if world > 1:
@@ -231,15 +243,16 @@ def main():
     def timed(e2e: bool, k: int):
         eng.run_turns(args.warmup, e2e=e2e)
         barrier()
-        with ClockSampler(local) as clk:
+        with ClockSampler(dev_index) as clk:
             ms, h2d, brk, kept = eng.run_turns(k, e2e=e2e)
         barrier()
         ms = max_over_ranks(ms)                  # the job ends with its slowest rank
         return ms, clk.summary(), brk, h2d, kept
 
     ms, clocks, brk, h2d_bytes, kept0 = timed(False, args.steps)
-    # decode-kernel statistics of THIS (device-resident) timed run, before the e2e run overwrites them
-    dec_busy_ms, dec_bytes, dec_launches = eng.last_decode_busy_ms, eng.last_decode_bytes, eng.last_decode_launches
+    # decode-loop statistics of THIS (device-resident) timed run, before the next runs overwrite them
+    dec_busy_ms, dec_bytes, dec_kv_bytes = eng.last_decode_busy_ms, eng.last_decode_bytes, eng.last_decode_kv_bytes
+    dec_launches = eng.last_decode_launches
     tokens_per_turn = cfg.batch * eng.turn_tokens
     value = world * tokens_per_turn * args.steps / (ms / 1000.0)
     g0 = eng.groups[0]
@@ -247,30 +260,41 @@ def main():
     e2e = None
     if not args.no_e2e:
         ms_e, _, brk_e, h2d_e, _ = timed(True, args.steps)
-        step_in = sum(e.turn_tokens * (e.q_in[0].numel() * 4 + e.kv_in[0].numel() * 2)
-                      + (e.qq_in.numel() * 4 + e.qkv_in.numel() * 2 + e.q_var[0].numel() * 4 if e.nq > 1 else 0)
-                      for e in eng.groups)
-        step_out = sum(e.cfg.decode_steps * e.out.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
-                       for e in eng.groups)
+        # the public turn API's own transfers: question ids in; answer ids, kept ids + selection
+        # metadata and the new round's upper KV (writeback) out; plus the kept rounds' KV gathers
+        step_in = sum(e.q_tok.numel() * 4 for e in eng.groups)
+        step_out = sum(e.answer_host.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
+                       + e.meta_host.numel() * 4 + e.margin_host.numel() * 8 for e in eng.groups)
         e2e = {"value": world * tokens_per_turn * args.steps / (ms_e / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out),
                "ms_per_step": ms_e / args.steps, "breakdown_ms_group0": brk_e}
 
-    # roofline of the dominant kernel (the decode attention) from the timed turns:
-    # decode-loop time per token vs algorithmic KV bytes per token
+    fetch_all = None
+    if cfg.round_cache and not args.no_fetch_all:
+        # the reference's transfer pattern (store.fetch_upper of every kept round, every turn)
+        for e in eng.groups:
+            e.cfg.round_cache = False
+        ms_f, _, _, h2d_f, _ = timed(False, args.steps)
+        for e in eng.groups:
+            e.cfg.round_cache = True
+        fetch_all = {"value": world * tokens_per_turn * args.steps / (ms_f / 1000.0), "unit": "tokens/s",
+                     "h2d_bytes_per_turn_all_groups": h2d_f,
+                     "note": "round cache off: every kept round's deep-layer KV crosses PCIe every turn"}
+
+    # roofline: the decode loop streams the KV of every visible key AND every layer's weights per token step
+    # (SURVEY §8d end-to-end row); achieved = algorithmic bytes of every timed decode token / the union of
+    # the groups' decode-loop intervals on the device timeline (CUDA events on each group's compute stream)
     peak, peak_kind = measured_peaks()
-    # decode kernels of all groups: algorithmic KV bytes of
-    # every timed decode token / the union of the decode-loop intervals on the
-    # device timeline (CUDA events on each group's compute stream)
-    bytes_tok = eng.kv_bytes_per_token()
+    bytes_tok = eng.kv_bytes_per_token() + eng.weight_bytes_per_token()
     achieved = dec_bytes / (dec_busy_ms / 1000.0) / 1e9
     step_bw = bytes_tok * eng.turn_tokens * args.steps / (ms / 1000.0) / 1e9
     resident, full = eng.gpu_kv_bytes()
-    traffic = None      # DRAM bytes per token-step from the committed ncu capture of this kernel (same shapes)
-    tp = REPO / "profiles" / "r01_traffic_c2_tokenstep.json"
+    traffic = None      # DRAM bytes per token-step from the committed ncu capture (same shapes)
+    tp = REPO / "profiles" / "r02_traffic_c2_tokenstep.json"
     if tp.exists() and args.workload == "c2":
         t = json.loads(tp.read_text())
-        traffic = t["per_dialogue_token_bytes"] * cfg.batch
+        if t.get("batch_per_group") == g0.cfg.batch:
+            traffic = t["per_token_step_bytes_per_group"] * len(eng.groups)
 
     prefill = None
     if g0.nq > 1:
@@ -280,34 +304,37 @@ def main():
         lower_flops = 4.0 * cfg.hq * cfg.head_dim * lw * (nq * g0.hist + nq * (nq + 1) / 2) * g0.cfg.batch
         prefill = {"question_rows": nq, "flops_per_turn_all_layers": sum(e.prefill_flops_per_turn() for e in eng.groups),
                    "lower_layers_ms_group0": brk["score_select"],
-                   "lower_layers_tflops_group0": lower_flops / (brk["score_select"] / 1000.0) / 1e12,
-                   "note": "lower-layer prefill + fused Lw-1 scoring + select, timed on group 0's stream while "
-                           "the other group decodes; kernel-alone figures: profiles/r01_prefill_c3.json"}
-        pk = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
-        tpk = float(pk.get("bf16_tflops", 2250.0))
-        achieved_tf = prefill["lower_layers_tflops_group0"]
-        prefill["roofline"] = {"bound": "tensor", "achieved": achieved_tf, "peak": tpk, "unit": "TFLOP/s",
-                               "frac": achieved_tf / tpk,
-                               "peak_source": "measured" if pk else "nominal dense bf16",
-                               "note": "algorithmic FLOPs (QK^T + PV once over causal-visible pairs); the kernel "
-                                       "issues 2x (q and P hi/lo bf16 splits for fp32-class accuracy)"}
+                   "lower_layers_attention_tflops_group0": lower_flops / (brk["score_select"] / 1000.0) / 1e12,
+                   "note": "lower-layer prefill (projections + attention + fused Lw-1 scoring) + select, timed on "
+                           "group 0's stream while the other group decodes; attention FLOPs only; kernel-alone "
+                           "figures: profiles/r01_prefill_c3.json"}
     line = {
         "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16 KV, fp32 accumulate", "data": "synthetic (random KV + activations)",
+        "vs_baseline": None, "dtype": "bf16 weights + KV, fp32 activations / accumulate",
+        "data": "synthetic (random-init weights of the config's shape, random KV history, random question ids)",
         "config": {"workload": f"{args.workload}: L={cfg.num_layers} Lw={cfg.watershed} Hq={cfg.hq} "
                                f"Hkv={cfg.hkv} d={cfg.head_dim} rounds={cfg.rounds}x{cfg.round_tokens} "
                                f"K={g0.K} batch/GPU={cfg.batch} in {groups} groups question_rows={g0.nq} "
-                               f"decode tokens/turn={eng.turn_tokens}",
+                               f"decode tokens/turn={eng.turn_tokens} (fixed; EOT ignored) "
+                               f"host_round_sets/group={g0.host_sets} (unique per dialogue: "
+                               f"{g0.host_sets == g0.cfg.batch}) round_cache={cfg.round_cache} "
+                               f"question_variants={cfg.question_variants}",
+                   "model": "reference toy transformer (attention + residual, RoPE, tied logits) at "
+                            f"{'Llama-3-8B' if cfg.hq == 32 else 'Qwen2-7B'} shapes, GQA, bf16 weights",
                    "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
-                   "l2": "inputs larger than L2 (KV read per token >> 126 MB)"},
+                   "l2": "inputs larger than L2 (KV + weights read per token step >> 126 MB)"},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": f"rk decode attention ({eng.decode_kernel_desc()}): KV bytes of every timed decode "
-                                                "token / union of the groups' decode-loop intervals (CUDA events)",
+                     "traffic": traffic,
+                     "kernel": f"decode step (per layer: rk_qkv_rope + rk decode attention [{eng.decode_kernel_desc()}]"
+                               " + rk_out_proj; rk_lm_head): KV + weight bytes of every timed decode token / union "
+                               "of the groups' decode-loop intervals (CUDA events)",
                      "decode_busy_ms": dec_busy_ms, "launches": dec_launches,
+                     "kv_GBps": dec_kv_bytes / (dec_busy_ms / 1000.0) / 1e9,
                      "whole_step_GBps": step_bw, "whole_step_frac": step_bw / peak,
-                     "bytes_per_token": bytes_tok, "peak_source": peak_kind},
+                     "bytes_per_token_step": bytes_tok, "kv_bytes_per_token_step": eng.kv_bytes_per_token(),
+                     "weight_bytes_per_token_step": eng.weight_bytes_per_token(), "peak_source": peak_kind},
         "h2d": {"bytes_per_turn_all_groups": h2d_bytes, "group0_bytes": g0.last_h2d_bytes, "group0_ms": brk["h2d"],
                 "round_cache": {"enabled": cfg.round_cache, "question_variants": cfg.question_variants,
                                 "rounds_fetched_group0_last_turn": g0.last_copied_rounds,
@@ -316,11 +343,20 @@ def main():
                 "link": "PCIe Gen5 x16 (~63 GB/s/dir theoretical)",
                 "link_peak_GBps": link_peak,
                 "link_peak_how": "one 256 MiB pinned-host -> HBM copy, best of 5, CUDA events, before the timed region"},
+        "k_boundary": {"min_rel_gap": eng.min_margin, "scorer": "fp64 exact (rk_round_scores_exact)" if g0.nq == 1
+                       else "tcgen05 fused fp32-class, fp64 re-score below the margin",
+                       "refine_margin": cfg.refine_margin, "refined_turns": eng.refined_turns,
+                       "note": "relative gap between the K-th and (K+1)-th largest masses, minimum over every "
+                               "dialogue and turn of the run"},
         "gpu_kv_saved": {"resident_bytes": resident, "full_cache_bytes": full, "saved_frac": 1 - resident / full},
         "breakdown_ms_group0": brk,
         "clocks": clocks,
         "kept_dialogue0": [int(x) for x in kept0[0]],
+        "host": {"numa_node": numa, "pinned_round_bytes": sum(e.host_sets * e.cfg.rounds for e in eng.groups)
+                 * g0.host_blocks[0][0].numel() * 2},
     }
+    if fetch_all:
+        line["fetch_all"] = fetch_all
     if prefill:
         line["prefill"] = prefill
     if e2e:
@@ -334,9 +370,9 @@ def main():
                                                  hkv=cfg.hkv, d=cfg.head_dim, rounds=cfg.rounds,
                                                  T=cfg.round_tokens, K=g0.K, processes=cores)
             line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": cores, "kind": kind,
-                                    "sample": f"{cores} dialogues x 1 decode token ({args.workload} shapes, fp32 KV), "
-                                              f"one process per core, timed {r['timed_s']:.1f}s after input "
-                                              f"generation"}
+                                    "sample": f"{cores} dialogues x 1 decode token ({args.workload} shapes, fp32 KV, "
+                                              f"attention path only: no projections), one process per core, timed "
+                                              f"{r['timed_s']:.1f}s after input generation"}
         except Exception as exc:  # the GPU number stands on its own
             line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
     if rank == 0:

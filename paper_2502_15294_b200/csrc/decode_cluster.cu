@@ -159,23 +159,29 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
 
   if (warp == kCW) {
     // ================= producer
-    if (append && hi == len && hi > lo) {
-      // appended key -> cache row len-1 (head h's 256 bytes of K and V), then TMA may read it
-      const int64_t dst = (row0 + len - 1) * p.hkv * D + (int64_t)h * D;
-      const int64_t src = ((int64_t)b * p.hkv + h) * D;
-      for (int e = lane; e < D / 8; e += 32) {
-        reinterpret_cast<uint4*>(p.k + dst)[e] = reinterpret_cast<const uint4*>(p.k_new + src)[e];
-        reinterpret_cast<uint4*>(p.v + dst)[e] = reinterpret_cast<const uint4*>(p.v_new + src)[e];
+    // the cache rows before the appended key do not depend on the previous kernel
+    // (PDL): their TMA boxes stream while it finishes.  The appended key (k_new /
+    // v_new) is the previous kernel's output (the fused QKV projection): the stage
+    // that holds cache row len-1 waits for it, copies head h's 256 bytes of K and
+    // V into that row, and fences them for the async proxy before its TMA reads.
+    const bool owns_new = append && hi == len && hi > lo;
+    const uint64_t pol = evict_first_policy();
+    int t = 0;
+    for (int j0 = lo; j0 < hi; j0 += kTK, ++t) {
+      const int nk = min(kTK, hi - j0);
+      if (owns_new && j0 + nk == hi) {
+        pdl_wait();
+        const int64_t dst = (row0 + len - 1) * p.hkv * D + (int64_t)h * D;
+        const int64_t src = ((int64_t)b * p.hkv + h) * D;
+        for (int e = lane; e < D / 8; e += 32) {
+          reinterpret_cast<uint4*>(p.k + dst)[e] = reinterpret_cast<const uint4*>(p.k_new + src)[e];
+          reinterpret_cast<uint4*>(p.v + dst)[e] = reinterpret_cast<const uint4*>(p.v_new + src)[e];
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
       }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
-      int t = 0;
-      for (int j0 = lo; j0 < hi; j0 += kTK, ++t) {
+      if (lane == 0) {
         const int s = t % kStg;
-        const int nk = min(kTK, hi - j0);
         const int ng = (nk + kBoxRows - 1) / kBoxRows;
         if (t >= kStg) mbar_wait(&empty[s], ((t / kStg) - 1) & 1);
         mbar_expect_tx(&full[s], (unsigned)(2 * ng * NH * kBoxBytes));

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
             bulk_g2s(vd, vb + (int64_t)j * ROW, (unsigned)(from_cache * ROW * 2), &full[s], pol);
           }
           if (has_new) {
+            pdl_wait();   // k_new / v_new are the previous kernel's output (the fused QKV projection)
             bulk_g2s(kd + from_cache * ROW * 2, reinterpret_cast<const __nv_bfloat16*>(p.k_new) + (int64_t)sgm.b * ROW,
                      ROW * 2, &full[s], pol);
             bulk_g2s(vd + from_cache * ROW * 2, reinterpret_cast<const __nv_bfloat16*>(p.v_new) + (int64_t)sgm.b * ROW,

@@ -1,43 +1,53 @@
-"""Batched round-sparse decode engine: one GPU, B independent dialogues.
+"""Batched round-sparse serving engine: one GPU, B independent dialogues.
 
-This is the B200 restatement of one serving turn of `RoundPipeline.run_turn`
-(pipeline.py:192-394) for large GQA configurations, driven by synthetic
-activations (no projections: the attention path of SURVEY.md §8a, as in the
-CPU-baseline composition of BASELINE.md §3):
+The B200 restatement of `RoundPipeline.run_turn` (pipeline.py:192-394) for the
+BASELINE configurations, with the reference's model (engine.py:146-287:
+attention + residual, RoPE, tied logits; here GQA-shaped with bf16 weights,
+decode_model.py) running on the GPU for every token:
 
   1. lower layers [0, Lw) hold every round's KV in HBM
      (`lower`  [B][Lw][K|V][S_lo][Hkv][d]);
      upper layers [Lw, L) of every round live in pinned host memory, one
      contiguous block per round ([L-Lw][K|V][T][Hkv][d], store.py:225-242);
-  2. the question token runs the lower layers; at layer Lw-1 the decode kernel
-     works on round-aligned items and leaves per-round softmax statistics,
-     finalised into Eq. 1 masses (pipeline.py:225-245) — no capture matrix;
+  2. the question runs the lower layers (fused QKV projection + RoPE + KV
+     append, decode attention, output projection + residual per layer); at
+     layer Lw-1 the exact fp64 scorer (rk_round_scores_exact) gives the Eq. 1
+     masses (pipeline.py:225-245), no capture matrix;
   3. rk_select_batch picks the kept rounds bit-exactly (selection.py:87-97),
      and the K ids come back to the host (the API returns a host tuple);
   4. rk_h2d_gather copies the kept rounds' upper KV into the per-dialogue
      working cache (`upper` [B][L-Lw][K|V][S_up][Hkv][d]) on a copy stream, one
      event per upper layer, so upper layer l starts as soon as its rows land
      (store.fetch_upper :254-263 + _assemble :158-169);
-  5. the question's upper layers, then `steps` decode tokens over all L
-     layers, replayed from a CUDA graph (pipeline.py:298-313);
+  5. the question's upper layers, then the greedy decode (pipeline.py:298-313):
+     SEP, then argmax tokens, every token through all L layers and the tied
+     logits, replayed from a CUDA graph;
   6. the new round's upper rows are written back to pinned host memory
      (writeback_upper :265-278).
 
-All attention runs in librk's pipelined bulk-copy decode kernel; the only
-host round trip per turn is the kept-round ids.
+A multi-row question (n_q > 1) takes the tensor-core prefill
+(rk_prefill_attention) with the Lw-1 scoring fused, its projections as library
+GEMMs (bf16 hi + lo halves of the activations, fp32 output), and an fp64
+re-score when the fused scoring's K-boundary margin is small.
+
+Each dialogue's synthetic history (lower KV, host blocks, questions, planted
+relevance) is seeded by its GLOBAL dialogue id, so a dialogue gets the same
+data and the same kept rounds whichever rank or group serves it.  The decode
+runs a fixed number of answer tokens per turn (EOT does not stop a dialogue:
+the work per turn is fixed).
 """
 
 from __future__ import annotations
 
 import ctypes as C
 import math
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
 from . import _lib, kernels
+from .decode_model import SEP_TOKEN, DecodeModel, ModelShape
 from .selection import SelectionPolicy, top_k_count
 from .stats import build_round_items
 
@@ -52,68 +62,88 @@ class EngineConfig:
     rounds: int = 32              # prior rounds in the history
     round_tokens: int = 512       # tokens per prior round
     batch: int = 1                # dialogues on this GPU
-    decode_steps: int = 128       # answer tokens per turn (after the question token)
+    decode_steps: int = 128       # answer tokens per turn (SEP + generated), each through all L layers
     policy: SelectionPolicy = field(default_factory=lambda: SelectionPolicy("top_percent", fraction=0.10))
     host_unique: int = 0          # distinct host round sets (0 = one per dialogue); >0 aliases
     item_chunk: int = 1024        # keys per scoring work item (round-aligned)
-    input_period: int = 24        # per-token input slots, cycled; e2e loads run P-2 tokens ahead (>= the
-                                  # other group's KV gather: C2 e2e 10.3K -> 11.3K tok/s at 8 -> 24)
     plant: int = 2                # rounds per dialogue with planted relevance at L_w-1 (0 = none)
     plant_beta: float = 0.25
-    question_rows: int = 1        # n_q: 1 = single-token question (decode kernel); > 1 = tensor-core prefill
+    question_rows: int = 1        # n_q: 1 = single-token question (decode path); > 1 = tensor-core prefill
     round_cache: bool = True      # keep rounds kept again in their working-cache slots (no re-fetch)
-    question_variants: int = 4    # distinct questions cycled over turns (noisy copies of question 0)
-    question_noise: float = 1.0   # variants about as far from question 0 as it is long
+    question_variants: int = 4    # distinct questions cycled over turns
     refine_margin: float = 1e-3   # multi-row questions: re-score in fp64 when the K-boundary gap of the
                                   # fp32-class fused scoring is below this (1-row questions always score in fp64)
+    model_seed: int = 42
 
     @property
     def group(self) -> int:
         return self.hq // self.hkv
+
+    @property
+    def shape(self) -> ModelShape:
+        return ModelShape(self.num_layers, self.hq, self.hkv, self.head_dim)
 
 
 def _ptr_array(values) -> np.ndarray:
     return np.asarray(values, dtype=np.uint64)
 
 
+def _dialogue_gen(device, gid: int, salt: int) -> torch.Generator:
+    return torch.Generator(device=device).manual_seed(1_000_003 * (gid + 1) + salt)
+
+
 class RoundDecodeEngine:
-    def __init__(self, cfg: EngineConfig, device: str = "cuda", seed: int = 0):
+    def __init__(self, cfg: EngineConfig, device: str = "cuda", model: DecodeModel | None = None,
+                 dialogues=None, seed: int | None = None):
         self.cfg = c = cfg
         self.dev = torch.device(device)
         if c.policy.kind != "top_percent":
             raise ValueError("the batched engine sizes its working cache for top_percent selection")
         self.dtype = torch.bfloat16
         L, lw, B, T, R = c.num_layers, c.watershed, c.batch, c.round_tokens, c.rounds
+        if dialogues is None:
+            base = 0 if seed is None else int(seed)
+            dialogues = list(range(base, base + B))
+        self.dialogues = [int(x) for x in dialogues]
+        if len(self.dialogues) != B:
+            raise ValueError(f"{len(self.dialogues)} dialogue ids for batch {B}")
+        self.model = model if model is not None else DecodeModel(c.shape, self.dev, seed=c.model_seed,
+                                                                 prefill_gemm=c.question_rows > 1)
+        if self.model.shape != c.shape:
+            raise ValueError("model shape does not match the engine config")
         self.L_up = L - lw
         self.K = top_k_count(R, c.policy.fraction, c.policy.min_rounds)
         self.hist = R * T
         self.nq = nq = max(1, c.question_rows)
         # rows appended to the caches per turn; tokens the decode metric counts
-        # (a 1-row question runs through the decode kernel and counts as one)
+        # (a 1-row question runs through the decode path and counts as one)
         self.turn_rows = nq + c.decode_steps
         self.turn_tokens = 1 + c.decode_steps if nq == 1 else c.decode_steps
         self.s_lo = self.hist + self.turn_rows
         self.s_up = self.K * T + self.turn_rows
         self.row = c.hkv * c.head_dim                         # elements per key (all heads)
-        g = torch.Generator(device="cpu").manual_seed(seed)
-        gd = torch.Generator(device=self.dev).manual_seed(seed + 1)
+        D = c.hq * c.head_dim
 
-        # ---- HBM tiers
+        # ---- HBM tiers (per-dialogue synthetic history, seeded by the global dialogue id)
         self.lower = torch.empty((B, lw, 2, self.s_lo, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
         self.upper = torch.zeros((B, self.L_up, 2, self.s_up, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
-        self.lower[:, :, :, : self.hist].normal_(generator=gd)
+        for b, gid in enumerate(self.dialogues):
+            g = _dialogue_gen(self.dev, gid, 1)
+            self.lower[b, :, :, : self.hist] = torch.randn((lw, 2, self.hist, c.hkv, c.head_dim), generator=g,
+                                                           device=self.dev).to(self.dtype)
         # ---- pinned host tier: one contiguous upper block per (dialogue set, round)
         n_sets = B if c.host_unique <= 0 else min(B, c.host_unique)
         self.host_sets = n_sets
         self.host_blocks = []
-        pool = torch.randn(1 << 24, generator=g).to(self.dtype)         # 32 MiB of bf16 noise
-        offs = torch.randint(0, 1 << 23, (n_sets * R,), generator=g).tolist()
+        pool = torch.randn(1 << 24, generator=torch.Generator().manual_seed(7)).to(self.dtype)   # 32 MiB of bf16 noise
         for u in range(n_sets):
+            gid = self.dialogues[u]
+            offs = np.random.default_rng(gid + 17).integers(0, 1 << 23, size=R)
             blocks = []
             for r in range(R):
                 blk = torch.empty((self.L_up, 2, T, c.hkv, c.head_dim), dtype=self.dtype, pin_memory=True)
                 flat = blk.view(-1)
-                o = offs[u * R + r]
+                o = int(offs[r])
                 for s0 in range(0, flat.numel(), 1 << 23):       # distinct window of the pool per block
                     n = min(1 << 23, flat.numel() - s0)
                     flat[s0:s0 + n].copy_(pool[o:o + n])
@@ -122,63 +152,63 @@ class RoundDecodeEngine:
         self.writeback = torch.empty((B, self.L_up, 2, self.turn_rows, c.hkv, c.head_dim), dtype=self.dtype,
                                      pin_memory=True)
 
-        # ---- lengths (device) and their per-turn reset values
+        # ---- lengths and positions (device) and their per-turn reset values
         self.lower_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
         self.upper_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
         self.lower_len0 = torch.full((B,), self.hist, dtype=torch.int32, device=self.dev)
         self.upper_len0 = torch.full((B,), self.K * T, dtype=torch.int32, device=self.dev)
+        self.pos = torch.zeros(B, dtype=torch.int32, device=self.dev)
+        self.pos_q0 = torch.full((B,), self.hist, dtype=torch.int32, device=self.dev)        # 1-row question
+        self.pos_dec0 = torch.full((B,), self.hist + nq, dtype=torch.int32, device=self.dev)  # SEP of the answer
 
-        # ---- round-aligned scoring items at layer L_w-1 (prior rounds + the question token)
-        bounds = [[(r * T, (r + 1) * T, r) for r in range(R)] + [(self.hist, self.hist + self.nq, R)]
-                  for _ in range(B)]
+        # ---- round-aligned scoring items at layer L_w-1 (prior rounds + the question)
+        bounds = [[(r * T, (r + 1) * T, r) for r in range(R)] + [(self.hist, self.hist + nq, R)] for _ in range(B)]
         self.items, self.n_items = kernels.items_tensor(bounds, c.item_chunk, self.dev)
         self.n_items_host = [len(build_round_items(b_, c.item_chunk)) for b_ in bounds]
-        if self.items.shape[1] > 512:
-            raise ValueError("too many scoring items; raise item_chunk")
 
-        # ---- synthetic per-step activations (cycled with period input_period)
-        P = max(1, min(c.input_period, self.turn_tokens))
-        self.period = P
-        self.q_in = torch.randn((P, L, B, c.hq, c.head_dim), generator=gd, device=self.dev)
-        self.kv_in = torch.randn((P, L, 2, B, c.hkv, c.head_dim), generator=gd, device=self.dev).to(self.dtype)
-        # per-token attention outputs, double-buffered so the end-to-end path can
-        # read token t back to the host while token t+1 computes
-        self.out_buf = torch.empty((2, L, B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
-        self.out = self.out_buf[0]
+        # ---- activations (one decode row per dialogue)
+        self.x = torch.zeros((B, D), dtype=torch.float32, device=self.dev)          # residual stream
+        self.q_buf = torch.zeros((B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+        self.k_new = torch.zeros((B, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        self.v_new = torch.zeros((B, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        self.attn = torch.zeros((B, D), dtype=torch.float32, device=self.dev)       # attention output
+        self.tokens = torch.zeros(B, dtype=torch.int32, device=self.dev)
+        self.sep = torch.full((B,), SEP_TOKEN, dtype=torch.int32, device=self.dev)
+        # answer ids of the turn: [SEP, generated...] (the last entry is the argmax after the final forward)
+        self.answer = torch.full((B, c.decode_steps + 1), SEP_TOKEN, dtype=torch.int32, device=self.dev)
+        self.answer_host = torch.zeros((B, c.decode_steps + 1), dtype=torch.int32, pin_memory=True)
+        self.lm_ws = torch.zeros(max(256, _lib.lib.rk_lm_head_workspace_bytes(B, self.model.shape.vocab)),
+                                 dtype=torch.uint8, device=self.dev)
         if nq > 1:
-            # multi-row question: per-layer query rows and new K/V rows (positions hist ..)
-            self.qq_in = torch.randn((L, B, nq, c.hq, c.head_dim), generator=gd, device=self.dev)
-            self.qkv_in = torch.randn((L, 2, B, nq, c.hkv, c.head_dim), generator=gd, device=self.dev).to(self.dtype)
-            self.qout = torch.empty((B, nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+            self.xq = torch.zeros((B * nq, D), dtype=torch.float32, device=self.dev)
+            self.qq = torch.zeros((B * nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+            self.qout = torch.zeros((B, nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
             self.q_pos = torch.arange(self.hist, self.hist + nq, dtype=torch.int64, device=self.dev)
+            self.pos_rows = torch.arange(self.hist, self.hist + nq, dtype=torch.int32,
+                                         device=self.dev).repeat(B).contiguous()
             self.k_pos_lo = torch.arange(self.hist + nq, dtype=torch.int64, device=self.dev)
             self.k_pos_up = torch.zeros((B, self.K * T + nq), dtype=torch.int64, device=self.dev)
             self.k_pos_up_host = torch.zeros((B, self.K * T + nq), dtype=torch.int64, pin_memory=True)
             self.bad_row = torch.zeros(1, dtype=torch.int32, device=self.dev)
             self.lower_len_q = torch.full((B,), self.hist + nq, dtype=torch.int32, device=self.dev)
             self.upper_len_q = torch.full((B,), self.K * T + nq, dtype=torch.int32, device=self.dev)
-        if c.plant:
-            self._plant(gd)
-        # per-turn question variants (layer inputs of the question at L_w-1 and above vary, so
-        # consecutive turns keep overlapping but different round sets)
+
+        # ---- questions: `question_variants` token sequences per dialogue, cycled over turns
         V = max(1, c.question_variants)
+        qt = np.stack([np.stack([np.random.default_rng([gid, v, 99]).integers(0, 256, size=nq)
+                                 for gid in self.dialogues]) for v in range(V)]).astype(np.int32)   # (V, B, nq)
+        self.q_tok_all = torch.from_numpy(qt).to(self.dev)
+        self.q_tok_host = torch.from_numpy(qt).pin_memory()
+        self.q_tok = torch.zeros((B, nq), dtype=torch.int32, device=self.dev)      # this turn's question (graph input)
         self.turn = 0
-        if self.nq > 1:
-            base = self.qq_in[c.watershed - 1]
-            self.q_var = torch.stack([base + (c.question_noise * torch.randn(base.shape, generator=gd, device=self.dev)
-                                              if v else 0.0) for v in range(V)])
-        else:
-            base = self.q_in[0]
-            self.q_var = torch.stack([base + (c.question_noise * torch.randn(base.shape, generator=gd, device=self.dev)
-                                              if v else 0.0) for v in range(V)])
+        if c.plant:
+            self._plant()
         # working-cache slot -> round id per dialogue (-1 = empty); see assign_slots
         self.slot_round = np.full((B, self.K), -1, dtype=np.int64)
         self.last_copied_rounds = 0
 
-        # ---- scratch
+        # ---- scratch (this engine's own: groups run concurrently on their own streams)
         self.raw = torch.empty((B, R), dtype=torch.float64, device=self.dev)
-        # this engine's own decode workspace (split-K partials, scoring statistics, arrival counters):
-        # groups run concurrently on their own streams, so nothing here may be shared between engines
         ws_bytes = _lib.lib.rk_decode_workspace_bytes(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8))
         self.ws = torch.zeros(max(256, int(ws_bytes)), dtype=torch.uint8, device=self.dev)
         ex_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, nq, c.hq, self.items.shape[1], R)
@@ -203,27 +233,33 @@ class RoundDecodeEngine:
         self.meta_host = torch.empty((3, B), dtype=torch.int32, pin_memory=True)
         self.graph_a = None
         self.graph_b = None
-        self.graph_b_e2e = None
         self.last_kept = None
         self.marks = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         self.window_log = None        # list of (start, end) decode-loop events per turn when enabled
         self.copy_marks = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
     # ------------------------------------------------------------------ data
-    def _plant(self, gd):
-        """Raise the question's attention on `plant` rounds per dialogue at layer
-        L_w-1: add beta * |k| * unit(mean_g q_g) to those rounds' keys, so the
-        K-boundary gap is wide (SURVEY.md §8d planted relevance)."""
+    def _plant(self):
+        """Raise the question's attention on `plant` rounds per dialogue at
+        layer L_w-1 (SURVEY.md §8d planted relevance): add beta * sqrt(d) * u
+        to those rounds' keys, u the unit query direction of the question's
+        first variant at that layer, approximated by its last token's embedding
+        projected and rotated (x W_q, RoPE at that token's position)."""
         c = self.cfg
         lw1 = c.watershed - 1
-        if self.nq > 1:       # mean direction of the question rows
-            q = self.qq_in[lw1].mean(dim=1).view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)
-        else:
-            q = self.q_in[0, lw1].view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)   # (B, Hkv, d)
-        u = q / q.norm(dim=-1, keepdim=True)
-        rng = np.random.default_rng(1234)
+        m = self.model
+        tok = self.q_tok_all[0, :, -1].long()                            # (B,) last question token
+        x = m.emb[tok].float().contiguous()
+        q = torch.zeros((c.batch, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+        kd = torch.zeros((c.batch, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        vd = torch.zeros_like(kd)
+        pos = torch.full((c.batch,), self.hist + self.nq - 1, dtype=torch.int32, device=self.dev)
+        kernels.qkv_rope(x, m.w_qkv_packed[lw1], c.hq, c.hkv, c.head_dim, pos, m.freq, q, kd, vd)
+        qm = q.view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)
+        u = qm / qm.norm(dim=-1, keepdim=True)
         self.planted = []
-        for b in range(c.batch):
+        for b, gid in enumerate(self.dialogues):
+            rng = np.random.default_rng(gid + 1234)
             rs = sorted(rng.choice(c.rounds, size=min(c.plant, c.rounds), replace=False).tolist())
             self.planted.append(rs)
             for r in rs:
@@ -232,33 +268,34 @@ class RoundDecodeEngine:
                 self.lower[b, lw1, 0, r * c.round_tokens:(r + 1) * c.round_tokens] = sl.to(self.dtype)
 
     # ------------------------------------------------------------------ kernels
-    def _layer(self, l: int, step: int, advance: bool, items: bool = False, out=None):
+    def _caches(self, l: int):
         c = self.cfg
-        p = step % self.period
         if l < c.watershed:
-            kc, vc, ln = self.lower[:, l, 0], self.lower[:, l, 1], self.lower_len
-            cap = self.s_lo
-        else:
-            u = l - c.watershed
-            kc, vc, ln = self.upper[:, u, 0], self.upper[:, u, 1], self.upper_len
-            cap = self.s_up
-        kernels.decode_attention(self.q_in[p, l], kc, vc, ln, cap, k_new=self.kv_in[p, l, 0],
-                                 v_new=self.kv_in[p, l, 1], items=self.items if items else None,
-                                 n_items=self.n_items if items else None,
-                                 out=(self.out if out is None else out)[l], ws=self.ws,
-                                 advance=ln if advance else None)
+            return self.lower[:, l, 0], self.lower[:, l, 1], self.lower_len, self.s_lo
+        u = l - c.watershed
+        return self.upper[:, u, 0], self.upper[:, u, 1], self.upper_len, self.s_up
 
-    def _layer_launches(self, l: int, advance: bool = False, items: bool = False) -> int:
-        """Kernels one _layer call launches (rk_decode_plan): the cluster decode
-        is one kernel (+ the length advance), the persistent split-K decode is
-        decode + merge (the merge advances the lengths)."""
+    def _layer(self, l: int, advance: bool):
+        """One decode row per dialogue through layer l: fused QKV projection +
+        RoPE (rk_qkv_rope), decode attention with the KV append
+        (rk_decode_attention), output projection + residual (rk_out_proj)."""
+        c, m = self.cfg, self.model
+        kc, vc, ln, cap = self._caches(l)
+        kernels.qkv_rope(self.x, m.w_qkv_packed[l], c.hq, c.hkv, c.head_dim, self.pos, m.freq, self.q_buf,
+                         self.k_new, self.v_new)
+        kernels.decode_attention(self.q_buf, kc, vc, ln, cap, k_new=self.k_new, v_new=self.v_new,
+                                 out=self.attn.view(c.batch, c.hq, c.head_dim), ws=self.ws,
+                                 advance=ln if advance else None)
+        kernels.out_proj(self.attn, m.w_o_packed[l], self.x)
+
+    def _attn_launches(self, l: int, advance: bool = False) -> int:
         c = self.cfg
-        kc, cap = (self.lower[:, l, 0], self.s_lo) if l < c.watershed else (self.upper[:, l - c.watershed, 0], self.s_up)
-        plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0), items)
+        kc, _, _, cap = self._caches(l)
+        plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0), False)
         return (1 + int(advance)) if plan > 0 else 2
 
     def decode_kernel_desc(self) -> str:
-        """The decode kernels the answer tokens run (lower / upper layers)."""
+        """The decode attention kernels the answer tokens run (lower / upper layers)."""
         c = self.cfg
         out = []
         for name, kc, cap in (("lower", self.lower[:, 0, 0], self.s_lo), ("upper", self.upper[:, 0, 0], self.s_up)):
@@ -268,16 +305,15 @@ class RoundDecodeEngine:
         return "; ".join(out)
 
     def launches_per_token(self) -> int:
-        """Kernels of one answer token through all layers (as _phase_b2)."""
+        """Kernels of one answer token: per layer qkv_rope + attention (+ length
+        advance) + out_proj; then the logits GEMV + argmax/embed."""
         c = self.cfg
-        return sum(self._layer_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
-                   for l in range(c.num_layers))
+        return sum(2 + self._attn_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
+                   for l in range(c.num_layers)) + 2
 
-    def launches_question_token(self) -> int:
-        """Kernels of the 1-row question token (_phase_a + _phase_b1)."""
-        c = self.cfg
-        return sum(self._layer_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
-                   for l in range(c.num_layers))
+    def _set_turn_lengths(self):
+        self.lower_len.copy_(self.lower_len0)
+        self.upper_len.copy_(self.upper_len0)
 
     def _phase_a(self):
         """Question through the lower layers, watershed scoring, selection.
@@ -290,12 +326,13 @@ class RoundDecodeEngine:
         if self.nq > 1:
             return self._phase_a_prefill()
         c = self.cfg
-        self.lower_len.copy_(self.lower_len0)
-        self.upper_len.copy_(self.upper_len0)
+        self._set_turn_lengths()
+        self.pos.copy_(self.pos_q0)
+        kernels.embed(self.q_tok.view(-1), self.model.emb, self.x)
         for l in range(c.watershed):
-            self._layer(l, 0, advance=(l == c.watershed - 1))
+            self._layer(l, advance=(l == c.watershed - 1))
         lw1 = c.watershed - 1
-        kernels.round_scores_exact(self.q_in[0, lw1].unsqueeze(1), self.lower[:, lw1, 0], self.q_pos_1, self.items,
+        kernels.round_scores_exact(self.q_buf.unsqueeze(1), self.lower[:, lw1, 0], self.q_pos_1, self.items,
                                    c.rounds, seq_len=self.lower_len, n_items=self.n_items, raw=self.raw,
                                    ws=self.ws_exact)
         self._select()
@@ -311,31 +348,63 @@ class RoundDecodeEngine:
         again (eager, on the current stream)."""
         c = self.cfg
         lw1 = c.watershed - 1
-        kernels.round_scores_exact(self.qq_in[lw1], self.lower[:, lw1, 0], self.q_pos, self.items, c.rounds,
-                                   seq_len=self.lower_len, n_items=self.n_items, raw=self.raw, ws=self.ws_exact)
+        kernels.round_scores_exact(self.qq.view(c.batch, self.nq, c.hq, c.head_dim), self.lower[:, lw1, 0],
+                                   self.q_pos, self.items, c.rounds, seq_len=self.lower_len, n_items=self.n_items,
+                                   raw=self.raw, ws=self.ws_exact)
         self._select()
         self.refined_turns += 1
 
-    # ---- multi-row question: tensor-core prefill (rk_prefill_attention) ------
+    # ---- multi-row question: projections as library GEMMs, tensor-core prefill attention
+    @staticmethod
+    def _proj_rows(x: torch.Tensor, w_kn: torch.Tensor) -> torch.Tensor:
+        """x (m, k) f32 @ w (k, n) bf16 with fp32 output, x split into bf16
+        hi + lo halves (~16 mantissa bits, as the decode projections)."""
+        hi = x.to(torch.bfloat16)
+        lo = (x - hi.float()).to(torch.bfloat16)
+        return torch.mm(hi, w_kn, out_dtype=torch.float32) + torch.mm(lo, w_kn, out_dtype=torch.float32)
+
+    def _prefill_layer(self, l: int, items: bool):
+        c, m = self.cfg, self.model
+        nq, hist, KT = self.nq, self.hist, self.K * c.round_tokens
+        lower = l < c.watershed
+        qkv = self._proj_rows(self.xq, m.w_qkv_kn[l])
+        if lower:
+            kb, vb = self.lower[0, l, 0, hist], self.lower[0, l, 1, hist]
+            gstride = self.lower.stride(0)
+        else:
+            u = l - c.watershed
+            kb, vb = self.upper[0, u, 0, KT], self.upper[0, u, 1, KT]
+            gstride = self.upper.stride(0)
+        kernels.rope_rows(qkv, c.hq, c.hkv, c.head_dim, self.pos_rows, m.freq, self.qq, kb, vb, self.row, nq,
+                          gstride)
+        qq = self.qq.view(c.batch, nq, c.hq, c.head_dim)
+        for b in range(c.batch):
+            if lower:
+                kernels.prefill_attention(
+                    qq[b], self.lower[b, l, 0, :hist + nq], self.lower[b, l, 1, :hist + nq], self.q_pos,
+                    self.k_pos_lo, out=self.qout[b], bad_row=self.bad_row,
+                    items=self.items[b, :self.n_items_host[b]] if items else None,
+                    n_bins=c.rounds if items else 0, raw=self.raw[b] if items else None)
+            else:
+                u = l - c.watershed
+                kernels.prefill_attention(
+                    qq[b], self.upper[b, u, 0, :KT + nq], self.upper[b, u, 1, :KT + nq], self.q_pos,
+                    self.k_pos_up[b], out=self.qout[b], bad_row=self.bad_row)
+        self.xq += self._proj_rows(self.qout.view(c.batch * nq, -1), m.w_o_kn[l])
+
     def _phase_a_prefill(self):
         """n_q question rows through the lower layers (causal over the full
         history + the question, pipeline.py:225-230); at layer L_w-1 the same
         pass leaves the Eq. 1 round masses (fused scoring), then selection."""
         c = self.cfg
-        nq, hist = self.nq, self.hist
+        self._set_turn_lengths()
+        kernels.embed(self.q_tok.view(-1), self.model.emb, self.xq)
         for l in range(c.watershed):
-            last = l == c.watershed - 1
-            for b in range(c.batch):
-                self.lower[b, l, :, hist:hist + nq].copy_(self.qkv_in[l, :, b])     # append the question's K/V
-                kernels.prefill_attention(
-                    self.qq_in[l, b], self.lower[b, l, 0, :hist + nq], self.lower[b, l, 1, :hist + nq],
-                    self.q_pos, self.k_pos_lo, out=self.qout[b], bad_row=self.bad_row,
-                    items=self.items[b, :self.n_items_host[b]] if last else None,
-                    n_bins=c.rounds if last else 0, raw=self.raw[b] if last else None)
+            self._prefill_layer(l, items=(l == c.watershed - 1))
         self.lower_len.copy_(self.lower_len_q)
         self._select()
 
-    def _phase_b1_prefill(self, kept, layer_wait: bool):
+    def _phase_b1_prefill(self, layer_wait: bool):
         """n_q question rows through the upper layers over the kept rounds +
         the question (pipeline.py:292-296); positions keep their original
         values, so the splice equals the masked attention (engine.py:94-112)."""
@@ -348,25 +417,24 @@ class RoundDecodeEngine:
             pos[KT:KT + nq] = torch.arange(self.hist, self.hist + nq)
         self.k_pos_up.copy_(self.k_pos_up_host, non_blocking=True)
         for l in range(c.watershed, c.num_layers):
-            u = l - c.watershed
             if layer_wait:
-                torch.cuda.current_stream().wait_event(self.layer_events[u])
-            for b in range(c.batch):
-                self.upper[b, u, :, KT:KT + nq].copy_(self.qkv_in[l, :, b])
-                kernels.prefill_attention(
-                    self.qq_in[l, b], self.upper[b, u, 0, :KT + nq], self.upper[b, u, 1, :KT + nq],
-                    self.q_pos, self.k_pos_up[b], out=self.qout[b], bad_row=self.bad_row)
+                torch.cuda.current_stream().wait_event(self.layer_events[l - c.watershed])
+            self._prefill_layer(l, items=False)
         self.upper_len.copy_(self.upper_len_q)
 
-    def _phase_b1_any(self, kept, layer_wait: bool):
+    def _phase_b1(self, layer_wait: bool):
+        """The question through the upper layers (each waits for its rows)."""
         if self.nq > 1:
-            self._phase_b1_prefill(kept, layer_wait)
-        else:
-            self._phase_b1(layer_wait)
+            return self._phase_b1_prefill(layer_wait)
+        c = self.cfg
+        for l in range(c.watershed, c.num_layers):
+            if layer_wait:
+                torch.cuda.current_stream().wait_event(self.layer_events[l - c.watershed])
+            self._layer(l, advance=(l == c.num_layers - 1))
 
     def prefill_flops_per_turn(self) -> float:
-        """Algorithmic FLOPs of the question prefill (QK^T + PV once, causal
-        visible pairs only): 4 * Hq * d per visible (row, key) pair."""
+        """Algorithmic attention FLOPs of the question prefill (QK^T + PV once,
+        causal visible pairs only): 4 * Hq * d per visible (row, key) pair."""
         if self.nq == 1:
             return 0.0
         c = self.cfg
@@ -375,68 +443,19 @@ class RoundDecodeEngine:
         pairs = c.watershed * (nq * self.hist + causal) + self.L_up * (nq * self.K * c.round_tokens + causal)
         return 4.0 * c.hq * c.head_dim * pairs * c.batch
 
-    def _phase_b1(self, layer_wait: bool):
-        """Question token through the upper layers (each waits for its rows)."""
-        c = self.cfg
-        for l in range(c.watershed, c.num_layers):
-            if layer_wait:
-                torch.cuda.current_stream().wait_event(self.layer_events[l - c.watershed])
-            self._layer(l, 0, advance=(l == c.num_layers - 1))
-
-    def _phase_b2(self, e2e: bool = False):
-        """Answer tokens: all L layers per token.
-
-        End to end (e2e), every token's q/k/v come from pinned host memory and
-        its attention outputs go back to it.  The copies run on the e2e copy
-        stream, pipelined against the decode kernels: inputs load P-2 tokens
-        ahead (input slots cycle with period P, a slot is reloaded only after
-        the token that last read it finished), and token t's outputs (double
-        buffer) drain on a second copy stream while token t+1 computes."""
-        c = self.cfg
-        T = c.decode_steps
-        if not e2e:
-            for t in range(1, T + 1):
-                for l in range(c.num_layers):
-                    self._layer(l, t, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
-            return
-        # inputs and outputs on separate copy streams: a D2H output copy queued behind an
-        # H2D input load would wait out the other group's KV gather on the H2D engine,
-        # and the token two steps later waits for that output buffer (measured: ~10 %
-        # of the e2e decode loop)
-        cs, cp, co = torch.cuda.current_stream(), self.e2e_stream, self.e2e_out_stream
-        ev = self.e2e_events
-        cp.wait_stream(cs)                                   # fork
-        co.wait_stream(cs)
-        P = self.period
-
-        def load(t):
-            with torch.cuda.stream(cp):
-                if t - P >= 1:
-                    cp.wait_event(ev["done"][t - P])         # slot t % P free
-                p = t % P
-                self.q_in[p].copy_(self.host_q[p], non_blocking=True)
-                self.kv_in[p].copy_(self.host_kv[p], non_blocking=True)
-                ev["in"][t].record(cp)
-
-        ahead = max(1, P - 2)        # inputs prefetched this many tokens ahead (absorbs DMA queueing
-        for t in range(1, min(T, ahead) + 1):    # behind the other group's KV gather)
-            load(t)
-        for t in range(1, T + 1):
-            if t + ahead <= T:
-                load(t + ahead)
-            cs.wait_event(ev["in"][t])
-            if t - 2 >= 1:
-                cs.wait_event(ev["out"][t - 2])              # out buffer t % 2 drained
-            ob = self.out_buf[t % 2]
+    def _phase_b2(self):
+        """The answer (pipeline.py:298-313): SEP at the position after the
+        question, then `decode_steps` forwards through all L layers, each
+        followed by the tied logits + first-max argmax (rk_lm_head), which also
+        embeds the next token and advances the position."""
+        c, m = self.cfg, self.model
+        self.pos.copy_(self.pos_dec0)
+        kernels.embed(self.sep, m.emb, self.x)
+        for t in range(c.decode_steps):
             for l in range(c.num_layers):
-                self._layer(l, t, advance=(l == c.watershed - 1 or l == c.num_layers - 1), out=ob)
-            ev["done"][t].record(cs)
-            with torch.cuda.stream(co):
-                co.wait_event(ev["done"][t])
-                self.host_out[t].copy_(ob, non_blocking=True)
-                ev["out"][t].record(co)
-        cs.wait_stream(cp)                                   # join
-        cs.wait_stream(co)
+                self._layer(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
+            kernels.lm_head(self.x, m.emb_packed, m.shape.vocab, m.emb, self.x, self.tokens, self.pos,
+                            tokens_log=self.answer[:, t + 1:], log_stride=self.answer.shape[1], ws=self.lm_ws)
 
     def _phase_wb(self):
         """Writeback of the new round's upper rows to pinned host memory
@@ -470,7 +489,7 @@ class RoundDecodeEngine:
         self.last_copied_rounds = len(copies)
         return copies
 
-    def gather_plan(self, kept: np.ndarray):
+    def gather_plan(self, kept: list):
         """Per upper layer: (src, spitch, dst, dpitch, width, height) arrays, one
         2-row (K, V) strided copy per (dialogue, newly kept round)."""
         c = self.cfg
@@ -510,24 +529,6 @@ class RoundDecodeEngine:
     # ------------------------------------------------------------------ turn
     def prepare(self, e2e: bool = False):
         """Warm up (module attributes, workspace) and capture the CUDA graphs."""
-        c = self.cfg
-        if e2e and not hasattr(self, "host_q"):
-            self.host_q = torch.empty(self.q_in.shape, dtype=self.q_in.dtype, pin_memory=True)
-            self.host_q.copy_(self.q_in)
-            self.host_kv = torch.empty(self.kv_in.shape, dtype=self.kv_in.dtype, pin_memory=True)
-            self.host_kv.copy_(self.kv_in)
-            if self.nq > 1:
-                self.host_qq = torch.empty(self.qq_in.shape, dtype=self.qq_in.dtype, pin_memory=True)
-                self.host_qq.copy_(self.qq_in)
-                self.host_qkv = torch.empty(self.qkv_in.shape, dtype=self.qkv_in.dtype, pin_memory=True)
-                self.host_qkv.copy_(self.qkv_in)
-            self.host_q_var = torch.empty(self.q_var.shape, dtype=self.q_var.dtype, pin_memory=True)
-            self.host_q_var.copy_(self.q_var)
-            self.e2e_stream = torch.cuda.Stream(self.dev)          # per-token input loads (H2D)
-            self.e2e_out_stream = torch.cuda.Stream(self.dev)      # per-token output reads (D2H)
-            self.e2e_events = {k: [torch.cuda.Event() for _ in range(c.decode_steps + 2)] for k in ("in", "done", "out")}
-            self.host_out = torch.empty((c.decode_steps + 1,) + tuple(self.out.shape), dtype=torch.float32,
-                                        pin_memory=True)
         with torch.cuda.stream(self.compute_stream):
             self.run_turn_eager()                     # warm-up, sets kernel attributes
             torch.cuda.synchronize()
@@ -537,11 +538,7 @@ class RoundDecodeEngine:
                     self._phase_a()
                 self.graph_b = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self.graph_b, stream=self.compute_stream):
-                    self._phase_b2(e2e=False)
-            if e2e and self.graph_b_e2e is None:
-                self.graph_b_e2e = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(self.graph_b_e2e, stream=self.compute_stream):
-                    self._phase_b2(e2e=True)
+                    self._phase_b2()
         torch.cuda.synchronize()
 
     def _select_to_host(self, refine: bool = True):
@@ -562,11 +559,10 @@ class RoundDecodeEngine:
         return kept
 
     def _set_question(self, e2e: bool = False):
-        """This turn's question (variant turn % V) into the question inputs."""
-        v = self.turn % self.q_var.shape[0]
-        dst = self.qq_in[self.cfg.watershed - 1] if self.nq > 1 else self.q_in[0]
-        src = self.host_q_var[v] if e2e else self.q_var[v]
-        dst.copy_(src, non_blocking=True)
+        """This turn's question (variant turn % V) into the question input: from
+        pinned host memory through the public API (e2e), else device-resident."""
+        v = self.turn % self.q_tok_all.shape[0]
+        self.q_tok.copy_(self.q_tok_host[v] if e2e else self.q_tok_all[v], non_blocking=True)
         self.turn += 1
 
     def run_turn_eager(self):
@@ -576,7 +572,7 @@ class RoundDecodeEngine:
         kept = self._select_to_host()
         self.copy_stream.wait_stream(torch.cuda.current_stream())
         self.issue_gather(self.gather_plan(kept))
-        self._phase_b1_any(kept, layer_wait=True)
+        self._phase_b1(layer_wait=True)
         self._phase_b2()
         self.decode_done.record()
         self.copy_stream.wait_event(self.decode_done)
@@ -588,20 +584,15 @@ class RoundDecodeEngine:
 
     def run_turn(self, e2e: bool = False, on_gather=None):
         """One turn on the compute stream with the captured graphs.  Returns the
-        kept rounds per dialogue (host) and the H2D bytes moved.  Timing marks
-        (compute stream): 0 start, 1 after scoring+select, 2 after the
-        question's upper layers, 3 after the decode tokens, 4 after writeback;
-        copy_marks bracket the H2D gather on the copy stream."""
+        kept rounds per dialogue (host) and the H2D bytes moved.  With e2e the
+        question tokens come from pinned host memory and the answer ids go back
+        to it (the public API's input and output).  Timing marks (compute
+        stream): 0 start, 1 after scoring+select, 2 after the question's upper
+        layers, 3 after the decode tokens, 4 after writeback; copy_marks bracket
+        the H2D gather on the copy stream."""
         m = self.marks
         with torch.cuda.stream(self.compute_stream):
             m[0].record()
-            if e2e:
-                # the question's inputs come from pinned host memory too
-                if self.nq > 1:
-                    self.qq_in.copy_(self.host_qq, non_blocking=True)
-                    self.qkv_in.copy_(self.host_qkv, non_blocking=True)
-                else:
-                    self.kv_in[0].copy_(self.host_kv[0], non_blocking=True)
             self._set_question(e2e)
             self.graph_a.replay()
             m[1].record()
@@ -614,17 +605,19 @@ class RoundDecodeEngine:
             if on_gather is not None:
                 on_gather()
             self.last_h2d_bytes = nbytes
-            self._phase_b1_any(kept, layer_wait=True)
+            self._phase_b1(layer_wait=True)
             m[2].record()
             if self.window_log is not None:          # per-turn decode window (bench roofline)
                 a = torch.cuda.Event(enable_timing=True)
                 a.record(self.compute_stream)
-            (self.graph_b_e2e if e2e else self.graph_b).replay()
+            self.graph_b.replay()
             m[3].record()
             if self.window_log is not None:
                 b = torch.cuda.Event(enable_timing=True)
                 b.record(self.compute_stream)
                 self.window_log.append((a, b))
+            if e2e:
+                self.answer_host.copy_(self.answer, non_blocking=True)
             # writeback of the new round's upper rows on the copy stream: it
             # overlaps the next turn's scoring; the next gather queues behind it
             self.decode_done.record(self.compute_stream)
@@ -635,6 +628,11 @@ class RoundDecodeEngine:
         self.last_kept = kept
         return kept, nbytes
 
+    def answers(self) -> np.ndarray:
+        """(B, decode_steps) answer ids of the last turn (SEP first), as the reference's answer_ids."""
+        torch.cuda.synchronize()
+        return self.answer[:, : self.cfg.decode_steps].cpu().numpy()
+
     def turn_breakdown_ms(self) -> dict:
         """Elapsed times of the last turn (call after synchronising)."""
         m = self.marks
@@ -644,11 +642,13 @@ class RoundDecodeEngine:
 
     def kernel_launches_per_turn(self) -> int:
         c = self.cfg
-        answer = self.launches_per_token() * c.decode_steps
-        if self.nq > 1:   # prefill per (layer, dialogue): bad-row fill, q prep, tcgen05 pass, merge (+2 scoring)
-            return c.num_layers * c.batch * 4 + 2 * c.batch + answer + 2       # + select + margin
-        return (self.launches_question_token() + answer
-                + 3 + 2)                                # exact scorer (3 kernels) + select + margin
+        answer = 1 + self.launches_per_token() * c.decode_steps            # SEP embed + tokens
+        if self.nq > 1:   # embed; per layer rope_rows + per dialogue (bad-row fill, q prep, tcgen05 pass, merge)
+            return 1 + c.num_layers * (1 + c.batch * 4) + 2 * c.batch + 2 + answer    # (+2 scoring) + select + margin
+        upper_q = sum(2 + self._attn_launches(l, advance=(l == c.num_layers - 1))
+                      for l in range(c.watershed, c.num_layers))
+        lower_q = sum(2 + self._attn_launches(l, advance=(l == c.watershed - 1)) for l in range(c.watershed))
+        return 1 + lower_q + 3 + 2 + upper_q + answer       # embed, lower layers, exact scorer, select + margin
 
     # ------------------------------------------------------------------ accounting
     def kv_bytes_per_token(self) -> int:
@@ -660,6 +660,11 @@ class RoundDecodeEngine:
         lower = c.watershed * (self.hist + mid) * self.row * 2 * es
         upper = self.L_up * (self.K * c.round_tokens + mid) * self.row * 2 * es
         return c.batch * (lower + upper)
+
+    def weight_bytes_per_token(self) -> int:
+        """Weight bytes one token step of this group reads (projections of all
+        layers + the tied logits), SURVEY.md §8d end-to-end roofline row."""
+        return self.model.weight_bytes_per_token()
 
     def gpu_kv_bytes(self) -> tuple[int, int]:
         """(resident KV bytes of the round engine, full-cache bytes) at turn end."""
@@ -673,7 +678,8 @@ class RoundDecodeEngine:
 
 class GroupedDecoder:
     """B dialogues served as G independent groups, each a RoundDecodeEngine on
-    its own compute + copy streams, driven by one host thread per group.
+    its own compute + copy streams, driven by one host thread per group, all
+    sharing one model (weights are read-only).
 
     A group's turn has one host round trip (the kept ids) and an H2D gather
     that the decode cannot start without; with two or more groups in flight the
@@ -682,15 +688,21 @@ class GroupedDecoder:
     latency gaps.  Dialogues stay independent: no data crosses groups.
     """
 
-    def __init__(self, cfg: EngineConfig, groups: int = 2, device: str = "cuda", seed: int = 0):
+    def __init__(self, cfg: EngineConfig, groups: int = 2, device: str = "cuda", dialogues=None, seed: int = 0):
         import dataclasses
+        import os
         if cfg.batch % groups:
             raise ValueError(f"batch {cfg.batch} not divisible by groups {groups}")
-        sub = dataclasses.replace(cfg, batch=cfg.batch // groups,
+        per = cfg.batch // groups
+        sub = dataclasses.replace(cfg, batch=per,
                                   host_unique=max(1, cfg.host_unique // groups) if cfg.host_unique else 0)
+        if dialogues is None:
+            dialogues = list(range(seed, seed + cfg.batch))
         self.cfg = cfg
-        self.groups = [RoundDecodeEngine(sub, device=device, seed=seed + 97 * g) for g in range(groups)]
-        import os
+        self.dialogues = list(dialogues)
+        self.model = DecodeModel(cfg.shape, device, seed=cfg.model_seed, prefill_gemm=cfg.question_rows > 1)
+        self.groups = [RoundDecodeEngine(sub, device=device, model=self.model,
+                                         dialogues=self.dialogues[g * per:(g + 1) * per]) for g in range(groups)]
         self.stagger = os.environ.get("RK_STAGGER", "1") != "0"
 
     def prepare(self, e2e: bool = False):
@@ -758,7 +770,9 @@ class GroupedDecoder:
         if cur1 is not None:
             busy += cur1 - cur0
         self.last_decode_busy_ms = busy
-        self.last_decode_bytes = turns * sum(e.cfg.decode_steps * e.kv_bytes_per_token() for e in self.groups)
+        self.last_decode_bytes = turns * sum(e.cfg.decode_steps * (e.kv_bytes_per_token() + e.weight_bytes_per_token())
+                                             for e in self.groups)
+        self.last_decode_kv_bytes = turns * sum(e.cfg.decode_steps * e.kv_bytes_per_token() for e in self.groups)
         self.last_decode_launches = turns * sum(e.launches_per_token() * e.cfg.decode_steps for e in self.groups)
         for eng in self.groups:
             eng.window_log = None
@@ -769,8 +783,19 @@ class GroupedDecoder:
     def turn_tokens(self):
         return self.groups[0].turn_tokens
 
+    @property
+    def min_margin(self):
+        return min(e.min_margin for e in self.groups)
+
+    @property
+    def refined_turns(self):
+        return sum(e.refined_turns for e in self.groups)
+
     def kv_bytes_per_token(self):
         return sum(e.kv_bytes_per_token() for e in self.groups)
+
+    def weight_bytes_per_token(self):
+        return sum(e.weight_bytes_per_token() for e in self.groups)
 
     def gpu_kv_bytes(self):
         r = [e.gpu_kv_bytes() for e in self.groups]

@@ -195,3 +195,58 @@ def prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: 
               n_bins if raw is not None else 0, _lib.ptr(active), _lib.ptr(out), _lib.ptr(raw), _lib.ptr(bad_row),
               _lib.ptr(ws), ws.numel(), _lib.RK_PREFILL_SINGLE_PASS if single_pass else 0, _lib.stream_ptr(stream))
     return out, raw, bad_row
+
+
+# ---------------------------------------------------------------- layer body (proj.cu)
+def pack_weight(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """(k, n) weight of x @ W (fp32 or bf16, device) -> tensor-core fragment order (bf16)."""
+    k, n = w.shape
+    w = w.contiguous()
+    out = torch.empty(_lib.lib.rk_packed_weight_bytes(k, n) // 2, dtype=torch.bfloat16, device=w.device)
+    _lib.call("rk_pack_weight", _lib.ptr(w), kv_code(w), k, n, _lib.ptr(out), _lib.stream_ptr(stream))
+    return out
+
+
+def qkv_rope(x: torch.Tensor, w_qkv_packed: torch.Tensor, hq: int, hkv: int, d: int, pos: torch.Tensor,
+             freq: torch.Tensor, q_out: torch.Tensor, k_out: torch.Tensor, v_out: torch.Tensor,
+             kv_row_stride: int | None = None, stream=None) -> None:
+    """q, k, v = RoPE(x W_q), RoPE(x W_k), x W_v for m rows of x (m, d_model) f32."""
+    m, dm = x.shape
+    _lib.call("rk_qkv_rope", _lib.ptr(x), m, dm, _lib.ptr(w_qkv_packed), hq, hkv, d, _lib.ptr(pos), _lib.ptr(freq),
+              _lib.ptr(q_out), _lib.ptr(k_out), _lib.ptr(v_out),
+              int(hkv * d if kv_row_stride is None else kv_row_stride), _lib.stream_ptr(stream))
+
+
+def out_proj(a: torch.Tensor, w_o_packed: torch.Tensor, resid: torch.Tensor, stream=None) -> None:
+    """resid (m, d_model) += a (m, k) W_o."""
+    m, k = a.shape
+    _lib.call("rk_out_proj", _lib.ptr(a), m, k, _lib.ptr(w_o_packed), resid.shape[1], _lib.ptr(resid),
+              _lib.stream_ptr(stream))
+
+
+def lm_head(x: torch.Tensor, emb_packed: torch.Tensor, vocab: int, emb: torch.Tensor, x_next: torch.Tensor,
+            tokens: torch.Tensor | None, pos: torch.Tensor | None, tokens_log: torch.Tensor | None = None,
+            log_stride: int = 0, ws: torch.Tensor | None = None, stream=None) -> None:
+    """tokens = first argmax of x E^T; x_next = E[tokens]; pos += 1 (when given)."""
+    m, dm = x.shape
+    need = _lib.lib.rk_lm_head_workspace_bytes(m, vocab)
+    if ws is None or ws.numel() < need:
+        ws = scratch(need, x.device, "lm_head")
+    _lib.call("rk_lm_head", _lib.ptr(x), m, dm, _lib.ptr(emb_packed), vocab, _lib.ptr(emb), _lib.ptr(x_next),
+              _lib.ptr(tokens), _lib.ptr(pos), _lib.ptr(tokens_log), int(log_stride), _lib.ptr(ws), ws.numel(),
+              _lib.stream_ptr(stream))
+
+
+def embed(tokens: torch.Tensor, emb: torch.Tensor, x: torch.Tensor, stream=None) -> None:
+    """x (m, d_model) f32 = emb[tokens] (bf16 table)."""
+    _lib.call("rk_embed", _lib.ptr(tokens), tokens.numel(), _lib.ptr(emb), emb.shape[1], _lib.ptr(x),
+              _lib.stream_ptr(stream))
+
+
+def rope_rows(qkv: torch.Tensor, hq: int, hkv: int, d: int, pos: torch.Tensor, freq: torch.Tensor,
+              q_out: torch.Tensor, k_out: torch.Tensor, v_out: torch.Tensor, kv_row_stride: int,
+              rows_per_group: int, kv_group_stride: int, stream=None) -> None:
+    """RoPE + bf16 cache append of m projected rows (qkv (m, (hq+2hkv)d) f32)."""
+    _lib.call("rk_rope_rows", _lib.ptr(qkv), qkv.shape[0], hq, hkv, d, _lib.ptr(pos), _lib.ptr(freq),
+              _lib.ptr(q_out), _lib.ptr(k_out), _lib.ptr(v_out), int(kv_row_stride), int(rows_per_group),
+              int(kv_group_stride), _lib.stream_ptr(stream))

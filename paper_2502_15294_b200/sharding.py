@@ -33,3 +33,54 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], device=device or ("cuda" if dist.get_backend() == "nccl" else "cpu"))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gpu_for_rank(local_rank: int) -> tuple[int, bool]:
+    """(device index, shared) for this rank: one GPU per rank (local_rank);
+    RK_SHARE_GPU=1 maps ranks onto the visible GPUs round-robin
+    (local_rank % device_count) so the multi-rank path runs on a one-GPU box."""
+    import os
+
+    import torch
+    n = torch.cuda.device_count()
+    if os.environ.get("RK_SHARE_GPU", "0") == "1":
+        return local_rank % max(1, n), int(os.environ.get("WORLD_SIZE", "1")) > n
+    if local_rank >= n:
+        raise RuntimeError(f"local rank {local_rank} but only {n} visible GPUs (set RK_SHARE_GPU=1 to share)")
+    return local_rank, False
+
+
+def _cpulist(text: str) -> set:
+    cpus = set()
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        else:
+            cpus.add(int(part))
+    return cpus
+
+
+def bind_numa_local(device_index: int):
+    """Pin this process to the CPUs of its GPU's NUMA node, so the pinned host
+    pools it allocates next (the deep-layer round blocks, first touched by this
+    process) are NUMA-local to the GPU's PCIe root.  Returns the
+    node, or None when the topology is not exposed (no binding)."""
+    import os
+    from pathlib import Path
+
+    import torch
+    try:
+        props = torch.cuda.get_device_properties(device_index)
+        bus = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        node = int(Path(f"/sys/bus/pci/devices/{bus}/numa_node").read_text())
+        if node < 0:
+            return None
+        cpus = _cpulist(Path(f"/sys/devices/system/node/node{node}/cpulist").read_text())
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return node
+    except Exception:
+        return None

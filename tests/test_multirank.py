@@ -82,3 +82,41 @@ def test_two_ranks_gloo_independent_dialogues():
     for b in range(N_DIALOGUES):                     # identical to a single-process run
         assert merged[b] == _dialogue_selection(b)
     assert ms == 11.0                                # max over ranks
+
+
+def test_gpu_for_rank_sharing(monkeypatch):
+    """RK_SHARE_GPU=1 maps ranks onto the visible GPUs round-robin (the
+    multi-rank bench on a one-GPU box); without it a rank needs its own GPU."""
+    from paper_2502_15294_b200 import sharding
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 1)
+    monkeypatch.setenv("RK_SHARE_GPU", "1")
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert sharding.gpu_for_rank(0) == (0, True)
+    assert sharding.gpu_for_rank(1) == (0, True)
+    monkeypatch.setenv("RK_SHARE_GPU", "0")
+    assert sharding.gpu_for_rank(0) == (0, False)
+    with pytest.raises(RuntimeError):
+        sharding.gpu_for_rank(1)
+    # NUMA binding degrades to a no-op when the topology is not exposed
+    node = sharding.bind_numa_local(0)
+    assert node is None or node >= 0
+
+
+def test_bench_reference_arm_under_torchrun():
+    """The driver's N=2 launch of the reference arm: torchrun with two ranks,
+    rank 0 prints exactly one JSON line, rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    repo = Path(__file__).resolve().parents[1]
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), str(repo / "bench.py"), "--impl", "reference", "--gpus", "2",
+           "--steps", "1", "--warmup", "0"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=repo)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
