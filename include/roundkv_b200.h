@@ -258,9 +258,16 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d,
  *    q, k = RoPE(x W_q), RoPE(x W_k); v = x W_v; append; attention;
  *    x += out W_o; logits = x E^T; greedy argmax, pipeline.py:308), GQA
  *    (W_k, W_v: d_model x hkv*d) with bf16 weights and fp32 activations.
- *    Weights are packed once into the tensor-core fragment order:
- *    rk_pack_weight(W [k][n] row-major (x @ W), fp32 or bf16) -> packed
- *    (rk_packed_weight_bytes(k, n); n padded to 16, k % 64 == 0).
+ *    Weights are stored once for the tensor cores: rk_pack_weight(W [k][n]
+ *    row-major (x @ W), fp32 or bf16) -> 16 KB tiles [n_pad/128][k/64] of
+ *    W^T (128 features x 64 k, bf16, each in the 128-byte-swizzled K-major
+ *    shared-memory image of a tcgen05 A operand; rk_packed_weight_bytes(k, n),
+ *    n padded to 128 with zero rows, k % 64 == 0).  The projections are persistent tcgen05 kernels
+ *    (M = 128 features, N = the rows padded to 16/32/64) that split K across
+ *    the CTAs; `workspace` (rk_proj_workspace_bytes(m, k, n), ZEROED once at
+ *    allocation — the kernels leave their tickets at zero) holds the split-K
+ *    partials, added in a fixed order (deterministic).  One workspace per
+ *    stream: concurrent launches must not share it.
  *    rk_qkv_rope: x [m][d_model] f32 (m rows: one per dialogue in decode, the
  *    question rows in prefill) times the packed [W_q | W_k | W_v]; RoPE on q
  *    and k at pos [m] (int32) with rope_freq [d/2] (float64, the reference's
@@ -268,7 +275,7 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d,
  *    k_out / v_out + row * kv_row_stride elements.
  *    rk_out_proj: resid [m][d_model] += a [m][k] W_o.
  *    rk_lm_head: logits of x [m][d_model] against the packed embedding
- *    (vocab rows) into workspace, the first argmax per row -> tokens [m]
+ *    (vocab rows; m <= 64) into workspace, the first argmax per row -> tokens [m]
  *    (and tokens_log[row * log_stride] when given), x_next [m][d_model] =
  *    emb[token] (bf16 table [vocab][d_model]), pos[row] += 1 when given.
  *    rk_embed: x [m][d_model] = emb[tokens[row]].
@@ -277,12 +284,13 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d,
  * ---------------------------------------------------------------------- */
 size_t rk_packed_weight_bytes(int k, int n);
 int rk_pack_weight(const void* w, int w_dtype, int k, int n, void* packed, rk_stream_t stream);
+size_t rk_proj_workspace_bytes(int m, int k, int n);
 int rk_qkv_rope(const float* x, int m, int d_model, const void* w_qkv_packed, int hq, int hkv, int d,
                 const int32_t* pos, const double* rope_freq, float* q_out, void* k_out, void* v_out,
-                int64_t kv_row_stride, rk_stream_t stream);
+                int64_t kv_row_stride, void* workspace, size_t workspace_bytes, rk_stream_t stream);
 int rk_out_proj(const float* a, int m, int k, const void* w_o_packed, int d_model, float* resid,
-                rk_stream_t stream);
-size_t rk_lm_head_workspace_bytes(int m, int vocab);
+                void* workspace, size_t workspace_bytes, rk_stream_t stream);
+size_t rk_lm_head_workspace_bytes(int m, int vocab, int d_model);
 int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int vocab, const void* emb,
                float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                void* workspace, size_t workspace_bytes, rk_stream_t stream);

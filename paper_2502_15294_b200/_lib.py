@@ -54,9 +54,10 @@ _SIGS = {
                                   _sz, _i, _p]),
     "rk_packed_weight_bytes": (_sz, [_i, _i]),
     "rk_pack_weight": (_i, [_p, _i, _i, _i, _p, _p]),
-    "rk_qkv_rope": (_i, [_p, _i, _i, _p, _i, _i, _i, _p, _p, _p, _p, _p, _i64, _p]),
-    "rk_out_proj": (_i, [_p, _i, _i, _p, _i, _p, _p]),
-    "rk_lm_head_workspace_bytes": (_sz, [_i, _i]),
+    "rk_proj_workspace_bytes": (_sz, [_i, _i, _i]),
+    "rk_qkv_rope": (_i, [_p, _i, _i, _p, _i, _i, _i, _p, _p, _p, _p, _p, _i64, _p, _sz, _p]),
+    "rk_out_proj": (_i, [_p, _i, _i, _p, _i, _p, _p, _sz, _p]),
+    "rk_lm_head_workspace_bytes": (_sz, [_i, _i, _i]),
     "rk_lm_head": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _p, _p, _i, _p, _sz, _p]),
     "rk_embed": (_i, [_p, _i, _p, _i, _p, _p]),
     "rk_rope_rows": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i64, _i, _i64, _p]),

@@ -2,23 +2,38 @@
 // reference: q,k = RoPE(x W_q), RoPE(x W_k); v = x W_v; append; attention;
 // x += out W_o; logits = x E^T; argmax) for B dialogues at once.
 //
-// Every projection is a skinny GEMM (m = B tokens <= 32 per pass, K = 4096,
-// N = 6144 / 4096): the weights are read once per token step, so the kernels
-// are bound by HBM on the weight bytes (Llama-3-8B-shaped: 84 MB per layer).
+// Every projection is a skinny GEMM (m = B tokens <= 64 per launch, K = 4096,
+// N = 6144 / 4096): the weights are read once per token step, so the kernel is
+// bound by HBM on the weight bytes (Llama-3-8B-shaped: 84 MB per layer).
 //
-// Layout: weights are packed once (rk_pack_weight) into mma.m16n8k16 A-fragment
-// order — one 16 (output features) x 16 (inputs) tile = 512 contiguous bytes,
-// lane L's 8 bf16 at 16 L, so a warp fetches a whole A operand with one
-// coalesced 16-byte load per lane and no shared-memory staging.  The tiles of
-// one 16-row output strip are consecutive along K.
+// Layout: a weight W [K][N] (x @ W) is stored once (rk_pack_weight) as 16 KB
+// tiles [N_pad/128][K/64] of W^T — 128 features x 64 k, each tile already in
+// the 128-byte-swizzled K-major image a tcgen05.mma M=128 A operand reads from
+// shared memory (16-byte chunk c of feature row r at chunk c ^ (r & 7)); N is
+// padded to 128 with zero rows.  A tile is one contiguous bulk copy, and a
+// CTA's run of tiles is one contiguous stream (a TMA tensor box of W^T would
+// gather 128 separate 128-byte rows 8 KB apart: measured 2.9 TB/s).
 //
-// Kernel: a CTA of 8 warps owns RT = 2 output strips (32 features); the 8
-// warps are RT strips x KS = 4 K-quarters.  Each warp streams its weights with
-// 8 tiles (4 KB) in flight, converts the fp32 activations of its K range into
-// bf16 hi + lo fragments on the fly (x = hi + lo keeps ~16 mantissa bits, the
-// reference's projections are fp32 BLAS) and issues 2 MMAs per (tile, 8-token
-// block).  The K-quarter partials meet in shared memory and are added in a
-// fixed order (deterministic), then the fused epilogue runs:
+// Work: units (strip group sg = 128 features, k-chunk kc = 64 k) in sg-major
+// order; a persistent grid of min(#SMs, units) CTAs takes contiguous equal
+// runs of units, so every SM streams the same number of weight bytes whatever
+// the shape.  Per CTA (12 warps):
+//   warp 0   weight producer: bulk copy of each unit's 16 KB tile into a deep ring —
+//            issued BEFORE griddepcontrol.wait (weights do not depend on the
+//            previous kernel), so the ring fills while that kernel drains;
+//   warps 4-7 converters (after griddepcontrol.wait): the unit's fp32
+//            activation slice x[0:m][kc*64 : kc*64+64] straight from L2, several
+//            units ahead in registers, -> bf16 hi + lo (x = hi + lo keeps ~16
+//            mantissa bits; the reference's projections are fp32 BLAS) written
+//            as two swizzled K-major B operands [NP tokens][64 k];
+//   warp 2   MMA issuer (one elected lane): per unit 4 k16 steps x (hi, lo)
+//            tcgen05.mma m128 n=NP k16 into a TMEM accumulator (double
+//            buffered across the CTA's strip-group segments);
+//   warps 8-11 epilogue (TMEM lane quarter = warp % 4, thread = feature):
+//            a segment covering the whole K of its strip group runs the fused
+//            epilogue directly; otherwise the partial goes to the workspace and
+//            the last CTA to arrive on the group's ticket adds the partials in
+//            CTA order (deterministic) and runs it:
 //   qkv : RoPE on q and k (interleaved pairs, fp64 angles from the host-computed
 //         reference frequency table, engine.py:162-164,175-185), q -> fp32,
 //         k, v -> bf16 rows for the cache append;
@@ -27,177 +42,558 @@
 //         maximum (pipeline.py:308, np.argmax) and looks up the next input.
 #include "decode_common.cuh"
 #include "rk_common.cuh"
+#include "tc_common.cuh"
 
 namespace rk {
+namespace pj {
 
-constexpr int kPjWarps = 8;
-constexpr int kPjRT = 2;                  // output strips (16 features) per CTA
-constexpr int kPjKS = kPjWarps / kPjRT;   // K splits per strip
-constexpr int kPjU = 8;                   // weight tiles in flight per warp
-constexpr int kPjMaxNT = 4;               // 8-token blocks per pass (32 tokens)
+using namespace rk::tc;
+
+#ifdef PJ_TRACE   // timing experiments: per-CTA %globaltimer stamps of the last launch
+__device__ unsigned long long g_pj_trace[1024 * 16];
+__device__ unsigned long long g_pj_units[3 * 64];
+#define PJU(kind, i)                                                                     \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && (i) < 64) {                                                   \
+      unsigned long long _t;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                             \
+      g_pj_units[(kind) * 64 + (i)] = _t;                                                \
+    }                                                                                    \
+  } while (0)
+#define PJT(slot)                                                                        \
+  do {                                                                                   \
+    unsigned long long _t;                                                               \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                               \
+    g_pj_trace[blockIdx.x * 16 + (slot)] = _t;                                            \
+  } while (0)
+#else
+#define PJT(slot)
+#define PJU(kind, i)
+#endif
+
+constexpr int BM = 128;                    // features per strip group (MMA M)
+constexpr int BK = 64;                     // k per unit (one 128-byte swizzle row of bf16)
+constexpr int W_BYTES = BM * BK * 2;       // 16 KB weight box
+constexpr int kWarps = 12;
+constexpr int kThreads = kWarps * 32;
+constexpr int kWProducer = 0, kMma = 2, kConv0 = 4, kEpi0 = 8;
+#ifndef PJ_BUDGET_KB
+#define PJ_BUDGET_KB 110
+#endif
+constexpr int kSmemBudget = PJ_BUDGET_KB * 1024;
 
 enum { PJ_QKV = 0, PJ_OUT = 1, PJ_HEAD = 2 };
 
-struct ProjParams {
-  const float* x;          // [m][K] fp32 input rows
-  int m, K, N;
-  const uint4* w;          // packed [N/16][K/16][32 lanes] x 16 B
-  int mode;
+template <int NP>
+struct Cfg {
+  static constexpr int XHL = 2 * NP * 128;            // hi tile | lo tile
+  static constexpr int XH = NP >= 64 ? 2 : 3;
+  static constexpr int EPT = NP / 8;                  // float4 of a unit's x slice per converter thread
+  static constexpr int PD = NP >= 64 ? 2 : (NP >= 32 ? 4 : 8);   // units of x in flight (registers)
+  static constexpr int ROPE = NP <= 32 ? NP * (BM / 2) * 8 : 0;    // (cos, sin) table [t][pair]
+  static constexpr int WS = (kSmemBudget - 1024 - XH * XHL - ROPE - 1024) / W_BYTES;
+  static constexpr int SMEM = 1024 + WS * W_BYTES + XH * XHL + ROPE + 1024;
+  static constexpr int TMEM_COLS = 4 * NP < 32 ? 32 : 4 * NP;   // 2 buffers x [hi | lo] columns
+  static_assert(WS >= 3, "weight ring too shallow");
+};
+
+struct Params {
+  const void* w;                           // tiled, swizzled W^T (rk_pack_weight)
+  const float* x;                          // [m][K] activations
+  int m, K, N, Npad, mode;
+  int KC, n_units, maxc;                   // k-chunks per strip group, units, partial slots per group
   // qkv
   int hq, hkv, d;
-  const int32_t* pos;      // [m] absolute positions
-  const double* freq;      // [d/2] RoPE frequencies (host: theta ** (-2i/d))
-  float* q_out;            // [m][hq*d]
-  __nv_bfloat16* k_out;    // row j at k_out + j * kv_stride
+  const int32_t* pos;
+  const double* freq;
+  float* q_out;
+  __nv_bfloat16* k_out;
   __nv_bfloat16* v_out;
   int64_t kv_stride;
   // out
-  float* resid;            // [m][N] += result
+  float* resid;
   // head
-  float* logits;           // [m][N]
+  float* logits;
+  // split-K reduction
+  int* tickets;                            // [n_sg], zero between launches
+  float* part;                             // [n_sg][maxc][m][128]
 };
 
+__device__ __forceinline__ int owner(int u, int n_units, int G) {    // CTA whose run holds unit u
+  return (int)(((int64_t)(u + 1) * G - 1) / n_units);
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ bool elect() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void split_bf16(float2 p, uint32_t& hi, uint32_t& lo) {
   hi = pack_bf16(p.x, p.y);
   const float2 h = bf16x2_to_f2(hi);
   lo = pack_bf16(p.x - h.x, p.y - h.y);
 }
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 128;" ::: "memory"); }
 
-template <int NT>
-__global__ void __launch_bounds__(kPjWarps * 32, 2) proj_kernel(ProjParams p) {
-  __shared__ float red[kPjWarps][NT][32][4];
-  __shared__ float tile[kPjRT * 16][NT * 8 + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int strip = blockIdx.x * kPjRT + (warp % kPjRT);
-  const int ks = warp / kPjRT;
-  const int KT = p.K / 16;
-  const int n_strips = p.N / 16;
-  const int kt0 = ks * KT / kPjKS, kt1 = (ks + 1) * KT / kPjKS;
-  const bool active = strip < n_strips;
-  const uint4* wp = p.w + ((size_t)(active ? strip : 0) * KT) * 32 + lane;
-  // the weights do not depend on the previous kernel: the first batch is in
-  // flight before griddepcontrol.wait (programmatic dependent launch)
-  uint4 nxt[kPjU];
+// the fused epilogue of one strip group: thread `row` holds feature
+// n = sg * 128 + row for tokens 0..NP-1.  `rope` (QKV) is the CTA's table of
+// (cos, sin) of pos[t] * freq[pair] (angle and sincos in float64 as
+// engine.py:175-185, stored rounded to float32), [t][row / 2], filled while the
+// weights stream (nullptr: computed here); the rotation itself runs in float64.
+template <int NP>
+__device__ __forceinline__ void finish(const Params& p, int sg, int row, float (&v)[NP], const float2* rope) {
+  const int n = sg * BM + row;
+  if (p.mode == PJ_QKV) {
+    const int qd = p.hq * p.d, kd = p.hkv * p.d;
+    float other[NP];
 #pragma unroll
-  for (int u = 0; u < kPjU; ++u)
-    if (active && kt0 + u < kt1) nxt[u] = ld_stream(wp + (size_t)(kt0 + u) * 32);
-  pdl_wait();                              // the activations of the previous kernel are complete
-  for (int m0 = 0; m0 < p.m; m0 += NT * 8) {
-    float acc[NT][4];
+    for (int t = 0; t < NP; ++t) other[t] = __shfl_xor_sync(0xffffffffu, v[t], 1);
+    if (n >= p.N) return;
+    const bool even = (n & 1) == 0;
+    if (n < qd + kd) {
+      const double f = p.freq[(n % p.d) >> 1];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[nt][i] = 0.f;
-    if (active) {
-      const float* xr[NT];
-      bool tok_ok[NT];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int tok = m0 + nt * 8 + g;
-        tok_ok[nt] = tok < p.m;
-        xr[nt] = p.x + (size_t)(tok_ok[nt] ? tok : 0) * p.K + 2 * t;
-      }
-      if (m0 > 0) {                        // later passes (multi-row prefill): reload the first batch
-#pragma unroll
-        for (int u = 0; u < kPjU; ++u)
-          if (kt0 + u < kt1) nxt[u] = ld_stream(wp + (size_t)(kt0 + u) * 32);
-      }
-      for (int kt = kt0; kt < kt1; kt += kPjU) {
-        uint4 a[kPjU];
-#pragma unroll
-        for (int u = 0; u < kPjU; ++u) a[u] = nxt[u];
-#pragma unroll
-        for (int u = 0; u < kPjU; ++u)     // next batch in flight while this one computes
-          if (kt + kPjU + u < kt1) nxt[u] = ld_stream(wp + (size_t)(kt + kPjU + u) * 32);
-#pragma unroll
-        for (int u = 0; u < kPjU; ++u) {
-          if (kt + u >= kt1) break;
-          const uint32_t af[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            float2 x0 = make_float2(0.f, 0.f), x1 = make_float2(0.f, 0.f);
-            if (tok_ok[nt]) {
-              const float* xp = xr[nt] + (kt + u) * 16;
-              x0 = *reinterpret_cast<const float2*>(xp);
-              x1 = *reinterpret_cast<const float2*>(xp + 8);
-            }
-            uint32_t h0, l0, h1, l1;
-            split_bf16(x0, h0, l0);
-            split_bf16(x1, h1, l1);
-            mma_bf16_16816(acc[nt], af, h0, h1);
-            mma_bf16_16816(acc[nt], af, l0, l1);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) red[warp][nt][lane][i] = acc[nt][i];
-    __syncthreads();
-    if (warp < kPjRT) {                    // K-quarters in a fixed order
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        float s[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int q = 0; q < kPjKS; ++q)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) s[i] += red[q * kPjRT + warp][nt][lane][i];
-        // C fragment: c0,c1 = (row g, tokens 2t, 2t+1); c2,c3 = (row g + 8, ...)
-        const int r = warp * 16 + g, c = nt * 8 + 2 * t;
-        tile[r][c] = s[0];
-        tile[r][c + 1] = s[1];
-        tile[r + 8][c] = s[2];
-        tile[r + 8][c + 1] = s[3];
-      }
-    }
-    __syncthreads();
-    // ---- fused epilogue over this CTA's 32 features x the pass's tokens
-    const int n0 = blockIdx.x * kPjRT * 16;
-    const int mt = min(NT * 8, p.m - m0);
-    if (p.mode == PJ_QKV) {
-      const int qd = p.hq * p.d, kd = p.hkv * p.d;
-      for (int e = threadIdx.x; e < kPjRT * 8 * mt; e += blockDim.x) {
-        const int pr = e / mt, j = e - pr * mt;          // feature pair (2pr, 2pr+1), token j
-        const int n = n0 + 2 * pr;
-        if (n >= p.N) continue;
-        const int tok = m0 + j;
-        const float x0 = tile[2 * pr][j], x1 = tile[2 * pr + 1][j];
-        if (n < qd + kd) {
-          const int i = (n % p.d) >> 1;
-          const double ang = (double)p.pos[tok] * p.freq[i];
-          double sn, cs;
-          sincos(ang, &sn, &cs);
-          const float y0 = (float)((double)x0 * cs - (double)x1 * sn);
-          const float y1 = (float)((double)x0 * sn + (double)x1 * cs);
-          if (n < qd) {
-            float* qo = p.q_out + (size_t)tok * qd + n;
-            qo[0] = y0;
-            qo[1] = y1;
-          } else {
-            __nv_bfloat16* ko = p.k_out + (size_t)tok * p.kv_stride + (n - qd);
-            *reinterpret_cast<uint32_t*>(ko) = pack_bf16(y0, y1);
-          }
+      for (int t = 0; t < NP; ++t) {
+        if (t >= p.m) break;
+        double sn, cs;
+        if (rope) {
+          const float2 e = rope[t * (BM / 2) + (row >> 1)];
+          cs = e.x;
+          sn = e.y;
         } else {
-          __nv_bfloat16* vo = p.v_out + (size_t)tok * p.kv_stride + (n - qd - kd);
-          *reinterpret_cast<uint32_t*>(vo) = pack_bf16(x0, x1);
+          sincos((double)p.pos[t] * f, &sn, &cs);
         }
+        const double x0 = even ? v[t] : other[t], x1 = even ? other[t] : v[t];
+        const float y = even ? (float)(x0 * cs - x1 * sn) : (float)(x0 * sn + x1 * cs);
+        if (n < qd)
+          p.q_out[(size_t)t * qd + n] = y;
+        else
+          p.k_out[(size_t)t * p.kv_stride + (n - qd)] = __float2bfloat16_rn(y);
       }
     } else {
-      for (int e = threadIdx.x; e < kPjRT * 16 * mt; e += blockDim.x) {
-        const int r = e / mt, j = e - r * mt;
-        const int n = n0 + r;
-        if (n >= p.N) continue;
-        const int tok = m0 + j;
-        if (p.mode == PJ_OUT)
-          p.resid[(size_t)tok * p.N + n] += tile[r][j];
-        else
-          p.logits[(size_t)tok * p.N + n] = tile[r][j];
+#pragma unroll
+      for (int t = 0; t < NP; ++t) {
+        if (t >= p.m) break;
+        p.v_out[(size_t)t * p.kv_stride + (n - qd - kd)] = __float2bfloat16_rn(v[t]);
       }
     }
-    __syncthreads();
+  } else if (p.mode == PJ_OUT) {
+    if (n >= p.N) return;
+    float r[NP];
+#pragma unroll
+    for (int t = 0; t < NP; ++t) r[t] = t < p.m ? p.resid[(size_t)t * p.N + n] : 0.f;   // all loads in flight
+#pragma unroll
+    for (int t = 0; t < NP; ++t)
+      if (t < p.m) p.resid[(size_t)t * p.N + n] = r[t] + v[t];
+  } else {
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      if (t >= p.m) break;
+      p.logits[(size_t)t * p.Npad + n] = v[t];
+    }
   }
+}
+
+// v = the sum over the strip group's contributors (CTA order) of their
+// partials; every load of a chunk of 8 tokens is in flight at once
+template <int NP>
+__device__ __forceinline__ void reduce_partials(const Params& p, int sg, int row, int ncontrib, float (&v)[NP]) {
+  constexpr int TC = NP < 8 ? NP : 8;
+  const float* base = p.part + (size_t)sg * p.maxc * p.m * BM + row;
+#pragma unroll
+  for (int t0 = 0; t0 < NP; t0 += TC) {
+    if (t0 >= p.m) break;
+    float acc[TC];
+#pragma unroll
+    for (int tt = 0; tt < TC; ++tt) acc[tt] = 0.f;
+    for (int c0 = 0; c0 < ncontrib; c0 += 8) {
+      float x[8][TC];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+        for (int tt = 0; tt < TC; ++tt)
+          x[cc][tt] = (c0 + cc < ncontrib && t0 + tt < p.m)
+                          ? __ldcg(base + ((size_t)(c0 + cc) * p.m + t0 + tt) * BM) : 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+        for (int tt = 0; tt < TC; ++tt) acc[tt] += x[cc][tt];      // fixed order: deterministic
+    }
+#pragma unroll
+    for (int tt = 0; tt < TC; ++tt) v[t0 + tt] = acc[tt];
+  }
+}
+
+__device__ __forceinline__ int ticket_acq_rel(int* t) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+  return old;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kThreads, 1)
+proj_tc_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<NP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* wring = smem;                              // WS x 16 KB (SW128 K-major A tiles)
+  uint8_t* xhl = wring + C::WS * W_BYTES;             // XH x [hi NP x 128 B | lo NP x 128 B]
+  float2* rope_tab = reinterpret_cast<float2*>(xhl + C::XH * C::XHL);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xhl + C::XH * C::XHL + C::ROPE);
+  uint64_t* wfull = bars;
+  uint64_t* wempty = wfull + C::WS;
+  uint64_t* hfull = wempty + C::WS;
+  uint64_t* hempty = hfull + C::XH;
+  uint64_t* accfull = hempty + C::XH;
+  uint64_t* accempty = accfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int u0 = (int)((int64_t)c * p.n_units / G), u1 = (int)((int64_t)(c + 1) * p.n_units / G);
+  const int n = u1 - u0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::WS; ++s) { bar_init(&wfull[s], 1); bar_init(&wempty[s], 1); }
+    for (int s = 0; s < C::XH; ++s) { bar_init(&hfull[s], 128); bar_init(&hempty[s], 1); }
+    for (int b = 0; b < 2; ++b) { bar_init(&accfull[b], 1); bar_init(&accempty[b], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) PJT(0);
+  // every CTA of this grid is running: the next kernel on the stream may start
+  // its prologue (it reads nothing this kernel writes before its own
+  // griddepcontrol.wait, which waits for this whole grid)
   pdl_trigger();
+
+  if (warp == kWProducer) {
+    // ===== weights: independent of the previous kernel, streamed from launch
+    if (elect()) {
+      const uint64_t pol = evict_first_policy();     // read once per token step
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(p.w) + (size_t)u0 * W_BYTES;
+      for (int i = 0; i < n; ++i) {
+        const int s = i % C::WS;
+        if (i >= C::WS) bar_wait(&wempty[s], ((i / C::WS) - 1) & 1);
+#ifdef PJ_NO_W
+        bar_arrive(&wfull[s]);
+#else
+        bar_expect(&wfull[s], W_BYTES);
+        bulk_g2s(wring + s * W_BYTES, src + (size_t)i * W_BYTES, W_BYTES, &wfull[s], pol);
+#endif
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kConv0 && warp < kConv0 + 4) {
+    // ===== x -> bf16 hi + lo, swizzled K-major B operands.  The fp32 slice
+    // x[0:m][kc*64 : kc*64+64] of each unit is loaded straight from L2 (the
+    // previous kernel's output) PD units ahead in registers, so the activations
+    // never throttle the weight stream
+    pdl_wait();
+    const int tid = threadIdx.x - kConv0 * 32;
+    float4 pre[C::PD][C::EPT];
+    auto load = [&](int i, float4(&dst)[C::EPT]) {
+      const int kc = (u0 + i) % p.KC;
+#pragma unroll
+      for (int e = 0; e < C::EPT; ++e) {
+        const int idx = tid + 128 * e, r = idx >> 4, c4 = idx & 15;
+        dst[e] = (i < n && r < p.m) ? __ldcg(reinterpret_cast<const float4*>(p.x + (size_t)r * p.K + kc * BK) + c4)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < C::PD; ++d) load(d, pre[d]);
+    for (int i0 = 0; i0 < n; i0 += C::PD) {
+#pragma unroll
+      for (int d = 0; d < C::PD; ++d) {
+        const int i = i0 + d;
+        if (i >= n) break;
+        const int h = i % C::XH;
+        if (i >= C::XH) bar_wait(&hempty[h], ((i / C::XH) - 1) & 1);
+        uint8_t* hi = xhl + h * C::XHL;
+        uint8_t* lo = hi + NP * 128;
+#pragma unroll
+        for (int e = 0; e < C::EPT; ++e) {
+          const int idx = tid + 128 * e, r = idx >> 4, c4 = idx & 15;
+          uint2 vh, vl;
+          split_bf16(make_float2(pre[d][e].x, pre[d][e].y), vh.x, vl.x);
+          split_bf16(make_float2(pre[d][e].z, pre[d][e].w), vh.y, vl.y);
+          // 16-byte chunk c4 / 2 of row r holds k 8 (c4 / 2) .. +7; this float4 is its half c4 & 1
+          const int off = r * 128 + (((c4 >> 1) ^ (r & 7)) << 4) + ((c4 & 1) << 3);
+          *reinterpret_cast<uint2*>(hi + off) = vh;
+          *reinterpret_cast<uint2*>(lo + off) = vl;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core reads
+        bar_arrive(&hfull[h]);
+        if (tid == 0) PJU(2, i);
+        load(i + C::PD, pre[d]);
+      }
+    }
+  } else if (warp == kMma) {
+    // ===== MMA issuer
+    // B = [x_hi; x_lo] stacked (2 NP rows): one MMA per k16 step gives W x_hi in
+    // accumulator columns [0, NP) and W x_lo in [NP, 2 NP) — the weight tile is
+    // read once per k16 step, not once per half; the epilogue adds the halves
+    constexpr uint32_t idesc = idesc_f16(BM, 2 * NP);
+    const uint32_t w_a = sa(wring), h_a = sa(xhl);
+    int q = 0;                                        // segment counter (accumulator buffer q & 1)
+    bool fresh = true;
+    for (int i = 0; i < n; ++i) {
+      const int u = u0 + i, kc = u % p.KC, s = i % C::WS, h = i % C::XH;
+      const int b = q & 1;
+      if (fresh && q >= 2) bar_wait(&accempty[b], ((q / 2) - 1) & 1);
+      bar_wait(&wfull[s], (i / C::WS) & 1);
+      if (i == 0 && lane == 0) PJT(1);
+      if (lane == 0) PJU(0, i);
+#ifndef PJ_NO_X
+      bar_wait(&hfull[h], (i / C::XH) & 1);
+#endif
+      if (lane == 0) PJU(1, i);
+      if (i == 0 && lane == 0) PJT(3);
+      if (i == n - 1 && lane == 0) PJT(4);
+      fence_after();
+      if (elect()) {
+        const uint64_t da = umma_desc(wring + s * W_BYTES), db = umma_desc(xhl + h * C::XHL);
+        (void)w_a; (void)h_a;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma(tmem + b * 2 * NP, da + (uint64_t)((32 * k) >> 4), db + (uint64_t)((32 * k) >> 4), idesc,
+               (fresh && k == 0) ? 0u : 1u);
+        umma_commit(&wempty[s]);
+        umma_commit(&hempty[h]);
+        if (i == n - 1 || kc == p.KC - 1) umma_commit(&accfull[b]);
+      }
+      __syncwarp();
+      fresh = false;
+      if (i == n - 1 || kc == p.KC - 1) { ++q; fresh = true; }
+    }
+  } else if (warp >= kEpi0) {
+    // ===== epilogue: thread = feature row of the strip group
+    pdl_wait();
+    const int wq = warp & 3, row = wq * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    // RoPE table of this launch's rows (the pair index of row r is the same in
+    // every strip group when 128 % d == 0), built while the weights stream
+    const bool tab = C::ROPE > 0 && p.mode == PJ_QKV && BM % p.d == 0;
+    if (tab) {
+      const double f = p.freq[(row % p.d) >> 1];
+      for (int t = row & 1; t < p.m; t += 2) {
+        double sn, cs;
+        sincos((double)p.pos[t] * f, &sn, &cs);
+        rope_tab[t * (BM / 2) + (row >> 1)] = make_float2((float)cs, (float)sn);
+      }
+      epi_sync();
+    }
+    const float2* rope = tab ? rope_tab : nullptr;
+    int q = 0;
+    for (int i = 0; i < n;) {
+      const int u = u0 + i, sg = u / p.KC, kc_a = u - sg * p.KC;
+      const int len = min(n - i, p.KC - kc_a);
+      const int b = q & 1;
+      bar_wait(&accfull[b], (q / 2) & 1);
+      fence_after();
+      float v[NP];
+#pragma unroll
+      for (int c16 = 0; c16 < NP / 16; ++c16) {
+        float lo16[16];
+        tmem_ld16(tmem + lane_base + b * 2 * NP + 16 * c16, v + 16 * c16);
+        tmem_ld16(tmem + lane_base + b * 2 * NP + NP + 16 * c16, lo16);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[16 * c16 + e] += lo16[e];      // W x_hi + W x_lo
+      }
+      fence_before();
+      bar_arrive(&accempty[b]);
+      if (threadIdx.x == kEpi0 * 32) PJT(7);
+#ifdef PJ_NO_EPI
+      if (true) {
+#else
+      if (len == p.KC) {
+#endif
+        finish<NP>(p, sg, row, v, rope);
+      } else {
+        // split-K: publish the partial; the last of the group's contributors
+        // (ticket) adds them in CTA order and runs the epilogue
+        const int cf = owner(sg * p.KC, p.n_units, G), cl = owner(sg * p.KC + p.KC - 1, p.n_units, G);
+        float* slot = p.part + ((size_t)(sg * p.maxc + (c - cf)) * p.m) * BM + row;
+#pragma unroll
+        for (int t = 0; t < NP; ++t)
+          if (t < p.m) __stcg(slot + (size_t)t * BM, v[t]);
+        epi_sync();                                   // the group's stores precede the release below
+        if (threadIdx.x == kEpi0 * 32) PJT(8);
+        if (threadIdx.x == kEpi0 * 32) *flag = ticket_acq_rel(&p.tickets[sg]) == cl - cf;
+        epi_sync();
+        if (threadIdx.x == kEpi0 * 32) PJT(9);
+        if (*flag) {
+          reduce_partials<NP>(p, sg, row, cl - cf + 1, v);
+          if (threadIdx.x == kEpi0 * 32) PJT(10);
+          finish<NP>(p, sg, row, v, rope);
+          if (threadIdx.x == kEpi0 * 32) PJT(11);
+          if (threadIdx.x == kEpi0 * 32) p.tickets[sg] = 0;   // ready for the next launch
+        }
+        epi_sync();
+      }
+      i += len;
+      ++q;
+    }
+    if (threadIdx.x == kEpi0 * 32) PJT(5);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kMma) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+  }
+  if (threadIdx.x == 0) PJT(6);
+}
+
+}  // namespace pj
+
+// tiles[sg][kc] (16 KB, swizzled K-major image) <- W[k][n] (x @ W), rows n >= n_valid zero
+template <typename T>
+__global__ void pack_weight_kernel(const T* __restrict__ w, int K, int n_valid, int Npad,
+                                   __nv_bfloat16* __restrict__ out) {
+  // one thread per (feature row n, 16-byte chunk of 8 k)
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int kchunks = K / 8;
+  if (idx >= (size_t)Npad * kchunks) return;
+  const int n = (int)(idx % Npad), kq = (int)(idx / Npad);   // consecutive threads: consecutive n (coalesced reads)
+  const int k0 = kq * 8, sg = n / pj::BM, r = n % pj::BM, kc = k0 / pj::BK, c = (k0 % pj::BK) / 8;
+  __nv_bfloat16 v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    v[e] = __float2bfloat16_rn(n < n_valid ? (float)w[(size_t)(k0 + e) * n_valid + n] : 0.f);
+  const size_t tile = (size_t)sg * (K / pj::BK) + kc;
+  uint8_t* dst = reinterpret_cast<uint8_t*>(out) + tile * pj::W_BYTES + r * 128 + ((c ^ (r & 7)) << 4);
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+}
+
+constexpr int kMaxStripGroups = 1024;      // n_pad <= 131072 outputs
+
+struct ProjPlan {
+  int Npad, KC, n_sg, n_units, grid, maxc;
+  size_t part_off, part_bytes, logits_off, total;
+};
+
+static ProjPlan proj_plan(int m, int K, int N) {
+  ProjPlan pl{};
+  pl.Npad = (N + pj::BM - 1) / pj::BM * pj::BM;
+  pl.n_sg = pl.Npad / pj::BM;
+  pl.KC = K / pj::BK;
+  pl.n_units = pl.n_sg * pl.KC;
+#ifndef PJ_CTAS_PER_SM
+#define PJ_CTAS_PER_SM 1
+#endif
+  const int slots = PJ_CTAS_PER_SM * sm_count();
+  pl.grid = pl.n_units < slots ? pl.n_units : slots;
+  pl.maxc = 1;
+  for (int sg = 0; sg < pl.n_sg; ++sg) {
+    auto own = [&](int u) { return (int)(((int64_t)(u + 1) * pl.grid - 1) / pl.n_units); };
+    const int cnt = own(sg * pl.KC + pl.KC - 1) - own(sg * pl.KC) + 1;
+    pl.maxc = cnt > pl.maxc ? cnt : pl.maxc;
+  }
+  const int mm = m < 1 ? 1 : (m > 64 ? 64 : m);
+  // tickets live in a fixed leading region, so calls of any shape can share one
+  // workspace: no shape's partials ever land where another keeps its tickets
+  pl.part_off = sizeof(int) * kMaxStripGroups;
+  pl.part_bytes = sizeof(float) * (size_t)pl.n_sg * pl.maxc * mm * pj::BM;
+  pl.logits_off = align_up(pl.part_off + pl.part_bytes, 256);
+  pl.total = pl.logits_off + sizeof(float) * (size_t)mm * pl.Npad;
+  return pl;
+}
+
+template <int NP>
+static int launch_np(const pj::Params& p, int grid,
+                     cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    RK_CUDA(cudaFuncSetAttribute(pj::proj_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 pj::Cfg<NP>::SMEM), "proj smem attribute");
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(pj::kThreads);
+  cfg.dynamicSmemBytes = pj::Cfg<NP>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pj::proj_tc_kernel<NP>, p);
+  if (e != cudaSuccess) return cuda_status(e, "proj_tc_kernel launch");
+  return RK_OK;
+}
+
+// y = x W for rows [0, m) in launches of <= 64 rows
+static int launch_proj(pj::Params p, const float* x, const void* w_packed, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+  if (p.m <= 0) return RK_OK;
+  if (p.K % pj::BK != 0) return fail(RK_ERR_DOMAIN, "projection K=%d (multiple of %d)", p.K, pj::BK);
+  const ProjPlan pl = proj_plan(p.m, p.K, p.N);
+  if (pl.n_sg > kMaxStripGroups) return fail(RK_ERR_DOMAIN, "projection N=%d too large", p.N);
+  if (ws == nullptr || ws_bytes < pl.total)
+    return fail(RK_ERR_CAPACITY, "projection workspace %zu < %zu bytes", ws_bytes, pl.total);
+  int r = RK_OK;
+  p.w = w_packed;
+  p.Npad = pl.Npad;
+  p.KC = pl.KC;
+  p.n_units = pl.n_units;
+  p.maxc = pl.maxc;
+  p.tickets = reinterpret_cast<int*>(ws);
+  p.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pl.part_off);
+  if (p.mode == pj::PJ_HEAD) p.logits = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pl.logits_off);
+  const int m_all = p.m;
+  for (int m0 = 0; m0 < m_all; m0 += 64) {
+    pj::Params q = p;
+    q.m = m_all - m0 < 64 ? m_all - m0 : 64;
+    const int qd = p.hq * p.d;
+    if (p.mode == pj::PJ_QKV) {
+      q.pos = p.pos + m0;
+      q.q_out = p.q_out + (size_t)m0 * qd;
+      q.k_out = p.k_out + (size_t)m0 * p.kv_stride;
+      q.v_out = p.v_out + (size_t)m0 * p.kv_stride;
+    } else if (p.mode == pj::PJ_OUT) {
+      q.resid = p.resid + (size_t)m0 * p.N;
+    } else if (m0 > 0) {
+      return fail(RK_ERR_DOMAIN, "lm_head rows %d > 64 per call", m_all);
+    }
+    q.x = x + (size_t)m0 * p.K;
+    if (q.m <= 16)
+      r = launch_np<16>(q, pl.grid, st);
+    else if (q.m <= 32)
+      r = launch_np<32>(q, pl.grid, st);
+    else
+      r = launch_np<64>(q, pl.grid, st);
+    if (r != RK_OK) return r;
+  }
+  return RK_OK;
 }
 
 // tokens[b] = first argmax of logits[b][0:V) (np.argmax); x[b] = emb[token];
@@ -284,54 +680,6 @@ __global__ void rope_rows_kernel(const float* __restrict__ qkv, int m, int hq, i
   }
 }
 
-// packed[strip][kt][lane] <- W[k][n] (row-major [K][N], x @ W), fp32 or bf16 source
-template <typename T>
-__global__ void pack_weight_kernel(const T* __restrict__ w, int K, int N, int n_valid, __nv_bfloat16* __restrict__ out) {
-  const size_t tiles = (size_t)(N / 16) * (K / 16);
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;   // one (tile, lane)
-  if (idx >= tiles * 32) return;
-  const int lane = idx & 31;
-  const size_t tl = idx >> 5;
-  const int KT = K / 16;
-  const int strip = (int)(tl / KT), kt = (int)(tl % KT);
-  const int g = lane >> 2, t = lane & 3;
-  const int rows[8] = {g, g, g + 8, g + 8, g, g, g + 8, g + 8};
-  const int cols[8] = {2 * t, 2 * t + 1, 2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9, 2 * t + 8, 2 * t + 9};
-  __nv_bfloat16* o = out + idx * 8;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int n = strip * 16 + rows[e], k = kt * 16 + cols[e];
-    const float v = n < n_valid ? (float)w[(size_t)k * n_valid + n] : 0.f;
-    o[e] = __float2bfloat16_rn(v);
-  }
-}
-
-static int launch_proj(const ProjParams& p, cudaStream_t st) {
-  if (p.m <= 0) return RK_OK;
-  if (p.K % (16 * kPjKS) != 0 || p.N % 16 != 0)
-    return fail(RK_ERR_DOMAIN, "projection K=%d (multiple of %d), N=%d (multiple of 16)", p.K, 16 * kPjKS, p.N);
-  const int grid = (p.N / 16 + kPjRT - 1) / kPjRT;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kPjWarps * 32);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e;
-  const int nt = (p.m + 7) / 8;
-  if (nt <= 1)
-    e = cudaLaunchKernelEx(&cfg, proj_kernel<1>, p);
-  else if (nt <= 2)
-    e = cudaLaunchKernelEx(&cfg, proj_kernel<2>, p);
-  else
-    e = cudaLaunchKernelEx(&cfg, proj_kernel<4>, p);
-  if (e != cudaSuccess) return cuda_status(e, "proj_kernel launch");
-  return RK_OK;
-}
-
 }  // namespace rk
 
 using namespace rk;
@@ -339,19 +687,20 @@ using namespace rk;
 extern "C" {
 
 size_t rk_packed_weight_bytes(int k, int n) {
-  return (size_t)((n + 15) / 16 * 16) * (size_t)k * sizeof(__nv_bfloat16);
+  return (size_t)((n + pj::BM - 1) / pj::BM * pj::BM) * (size_t)k * sizeof(__nv_bfloat16);
 }
 
 int rk_pack_weight(const void* w, int w_dtype, int k, int n, void* packed, rk_stream_t stream) {
-  if (k <= 0 || n <= 0 || k % 16 != 0) return fail(RK_ERR_DOMAIN, "pack_weight k=%d (multiple of 16), n=%d", k, n);
-  const int np = (n + 15) / 16 * 16;
-  const size_t threads = (size_t)(np / 16) * (k / 16) * 32;
+  if (k <= 0 || n <= 0 || k % pj::BK != 0)
+    return fail(RK_ERR_DOMAIN, "pack_weight k=%d (multiple of %d), n=%d", k, pj::BK, n);
+  const int np = (n + pj::BM - 1) / pj::BM * pj::BM;
+  const size_t threads = (size_t)np * (k / 8);
   const int blocks = (int)((threads + 255) / 256);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (w_dtype == RK_F32)
-    pack_weight_kernel<float><<<blocks, 256, 0, st>>>((const float*)w, k, np, n, (__nv_bfloat16*)packed);
+    pack_weight_kernel<float><<<blocks, 256, 0, st>>>((const float*)w, k, n, np, (__nv_bfloat16*)packed);
   else if (w_dtype == RK_BF16)
-    pack_weight_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)w, k, np, n,
+    pack_weight_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)w, k, n, np,
                                                               (__nv_bfloat16*)packed);
   else
     return fail(RK_ERR_DOMAIN, "weight dtype %d", w_dtype);
@@ -359,17 +708,20 @@ int rk_pack_weight(const void* w, int w_dtype, int k, int n, void* packed, rk_st
   return RK_OK;
 }
 
+size_t rk_proj_workspace_bytes(int m, int k, int n) {
+  if (m <= 0 || k <= 0 || n <= 0) return 256;
+  return proj_plan(m, k, n).total;
+}
+
 int rk_qkv_rope(const float* x, int m, int d_model, const void* w_qkv_packed, int hq, int hkv, int d,
                 const int32_t* pos, const double* rope_freq, float* q_out, void* k_out, void* v_out,
-                int64_t kv_row_stride, rk_stream_t stream) {
+                int64_t kv_row_stride, void* workspace, size_t workspace_bytes, rk_stream_t stream) {
   if (hkv <= 0 || hq % hkv != 0 || d % 2 != 0) return fail(RK_ERR_DOMAIN, "qkv heads %d/%d, d %d", hq, hkv, d);
-  ProjParams p{};
-  p.x = x;
+  pj::Params p{};
   p.m = m;
   p.K = d_model;
   p.N = (hq + 2 * hkv) * d;
-  p.w = reinterpret_cast<const uint4*>(w_qkv_packed);
-  p.mode = PJ_QKV;
+  p.mode = pj::PJ_QKV;
   p.hq = hq;
   p.hkv = hkv;
   p.d = d;
@@ -379,45 +731,40 @@ int rk_qkv_rope(const float* x, int m, int d_model, const void* w_qkv_packed, in
   p.k_out = reinterpret_cast<__nv_bfloat16*>(k_out);
   p.v_out = reinterpret_cast<__nv_bfloat16*>(v_out);
   p.kv_stride = kv_row_stride;
-  if (p.N % 32 != 0) return fail(RK_ERR_DOMAIN, "qkv width %d (multiple of 32)", p.N);
-  return launch_proj(p, reinterpret_cast<cudaStream_t>(stream));
+  return launch_proj(p, x, w_qkv_packed, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rk_out_proj(const float* a, int m, int k, const void* w_o_packed, int d_model, float* resid,
-                rk_stream_t stream) {
-  ProjParams p{};
-  p.x = a;
+                void* workspace, size_t workspace_bytes, rk_stream_t stream) {
+  pj::Params p{};
   p.m = m;
   p.K = k;
   p.N = d_model;
-  p.w = reinterpret_cast<const uint4*>(w_o_packed);
-  p.mode = PJ_OUT;
+  p.mode = pj::PJ_OUT;
   p.resid = resid;
-  return launch_proj(p, reinterpret_cast<cudaStream_t>(stream));
+  return launch_proj(p, a, w_o_packed, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
-size_t rk_lm_head_workspace_bytes(int m, int vocab) {
-  return sizeof(float) * (size_t)m * ((vocab + 15) / 16 * 16);
+size_t rk_lm_head_workspace_bytes(int m, int vocab, int d_model) {
+  if (m <= 0 || vocab <= 0 || d_model <= 0) return 256;
+  return proj_plan(m, d_model, vocab).total;
 }
 
 int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int vocab, const void* emb,
                float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                void* workspace, size_t workspace_bytes, rk_stream_t stream) {
   if (m <= 0) return RK_OK;
-  const int vp = (vocab + 15) / 16 * 16;
-  if (workspace_bytes < rk_lm_head_workspace_bytes(m, vocab))
-    return fail(RK_ERR_CAPACITY, "lm_head workspace %zu", workspace_bytes);
-  ProjParams p{};
-  p.x = x;
+  if (m > 64) return fail(RK_ERR_DOMAIN, "lm_head rows %d > 64", m);
+  pj::Params p{};
   p.m = m;
   p.K = d_model;
-  p.N = vp;
-  p.w = reinterpret_cast<const uint4*>(emb_packed);
-  p.mode = PJ_HEAD;
-  p.logits = reinterpret_cast<float*>(workspace);
+  p.N = vocab;
+  p.mode = pj::PJ_HEAD;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int rc = launch_proj(p, st);
+  int rc = launch_proj(p, x, emb_packed, workspace, workspace_bytes, st);
   if (rc != RK_OK) return rc;
+  const ProjPlan pl = proj_plan(m, d_model, vocab);
+  const float* logits = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(workspace) + pl.logits_off);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(m);
   cfg.blockDim = dim3(256);
@@ -427,7 +774,7 @@ int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int v
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, argmax_embed_kernel, (const float*)p.logits, vp, vocab,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, argmax_embed_kernel, logits, pl.Npad, vocab,
                                      (const __nv_bfloat16*)emb, d_model, x_next, tokens, pos, tokens_log,
                                      log_stride);
   if (e != cudaSuccess) return cuda_status(e, "argmax_embed_kernel launch");
@@ -461,5 +808,14 @@ int rk_embed(const int32_t* tokens, int m, const void* emb, int d_model, float* 
   if (e != cudaSuccess) return cuda_status(e, "embed_kernel launch");
   return RK_OK;
 }
+
+#ifdef PJ_TRACE
+int rk_debug_proj_trace(unsigned long long* out, int n) {  // n <= 16384
+  return cudaMemcpyFromSymbol(out, pj::g_pj_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -1;
+}
+int rk_debug_proj_units(unsigned long long* out) {       // 3 x 64
+  return cudaMemcpyFromSymbol(out, pj::g_pj_units, sizeof(unsigned long long) * 192) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 }  // extern "C"

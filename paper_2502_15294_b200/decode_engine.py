@@ -177,8 +177,10 @@ class RoundDecodeEngine:
         # answer ids of the turn: [SEP, generated...] (the last entry is the argmax after the final forward)
         self.answer = torch.full((B, c.decode_steps + 1), SEP_TOKEN, dtype=torch.int32, device=self.dev)
         self.answer_host = torch.zeros((B, c.decode_steps + 1), dtype=torch.int32, pin_memory=True)
-        self.lm_ws = torch.zeros(max(256, _lib.lib.rk_lm_head_workspace_bytes(B, self.model.shape.vocab)),
+        # this engine's own split-K workspaces (groups run concurrently on their own streams)
+        self.lm_ws = torch.zeros(max(256, _lib.lib.rk_lm_head_workspace_bytes(B, self.model.shape.vocab, D)),
                                  dtype=torch.uint8, device=self.dev)
+        self.proj_ws = kernels.proj_workspace(B, D, max(self.model.shape.qkv_width, D), self.dev)
         if nq > 1:
             self.xq = torch.zeros((B * nq, D), dtype=torch.float32, device=self.dev)
             self.qq = torch.zeros((B * nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
@@ -282,11 +284,11 @@ class RoundDecodeEngine:
         c, m = self.cfg, self.model
         kc, vc, ln, cap = self._caches(l)
         kernels.qkv_rope(self.x, m.w_qkv_packed[l], c.hq, c.hkv, c.head_dim, self.pos, m.freq, self.q_buf,
-                         self.k_new, self.v_new)
+                         self.k_new, self.v_new, ws=self.proj_ws)
         kernels.decode_attention(self.q_buf, kc, vc, ln, cap, k_new=self.k_new, v_new=self.v_new,
                                  out=self.attn.view(c.batch, c.hq, c.head_dim), ws=self.ws,
                                  advance=ln if advance else None)
-        kernels.out_proj(self.attn, m.w_o_packed[l], self.x)
+        kernels.out_proj(self.attn, m.w_o_packed[l], self.x, ws=self.proj_ws)
 
     def _attn_launches(self, l: int, advance: bool = False) -> int:
         c = self.cfg

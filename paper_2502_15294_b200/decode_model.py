@@ -89,9 +89,11 @@ class DecodeModel:
         torch.cuda.synchronize(dev)
 
     def weight_bytes_per_token(self) -> int:
-        """Bytes of weights one decode token step reads (all layers + logits)."""
-        return (sum(w.numel() * 2 for w in self.w_qkv_packed) + sum(w.numel() * 2 for w in self.w_o_packed)
-                + self.emb_packed.numel() * 2)
+        """Algorithmic weight bytes of one decode token step (bf16 W_q|W_k|W_v
+        and W_o of every layer + the tied embedding; the 128-row padding of the
+        stored logits operand is not counted)."""
+        s = self.shape
+        return 2 * (s.num_layers * (s.d_model * s.qkv_width + s.d_model * s.d_model) + s.vocab * s.d_model)
 
     def host_weights(self) -> dict:
         """The bf16 weights as float32 NumPy (for the oracle)."""

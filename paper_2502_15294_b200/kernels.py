@@ -199,7 +199,8 @@ def prefill_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: 
 
 # ---------------------------------------------------------------- layer body (proj.cu)
 def pack_weight(w: torch.Tensor, stream=None) -> torch.Tensor:
-    """(k, n) weight of x @ W (fp32 or bf16, device) -> tensor-core fragment order (bf16)."""
+    """(k, n) weight of x @ W (fp32 or bf16, device) -> W^T [n_pad][k] bf16
+    (n padded to 128 with zero rows), the K-major tcgen05 A operand."""
     k, n = w.shape
     w = w.contiguous()
     out = torch.empty(_lib.lib.rk_packed_weight_bytes(k, n) // 2, dtype=torch.bfloat16, device=w.device)
@@ -207,21 +208,38 @@ def pack_weight(w: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
+def proj_workspace(m: int, k: int, n: int, device) -> torch.Tensor:
+    """A zeroed split-K workspace for one stream's projections of m rows
+    (k inputs, n outputs); the kernels leave it zeroed."""
+    return torch.zeros(max(256, int(_lib.lib.rk_proj_workspace_bytes(m, k, n))), dtype=torch.uint8, device=device)
+
+
+def _proj_ws(ws, m, k, n, device, tag):
+    need = _lib.lib.rk_proj_workspace_bytes(m, k, n)
+    if ws is None or ws.numel() < need:
+        ws = scratch(need, device, tag)
+    return ws
+
+
 def qkv_rope(x: torch.Tensor, w_qkv_packed: torch.Tensor, hq: int, hkv: int, d: int, pos: torch.Tensor,
              freq: torch.Tensor, q_out: torch.Tensor, k_out: torch.Tensor, v_out: torch.Tensor,
-             kv_row_stride: int | None = None, stream=None) -> None:
+             kv_row_stride: int | None = None, ws: torch.Tensor | None = None, stream=None) -> None:
     """q, k, v = RoPE(x W_q), RoPE(x W_k), x W_v for m rows of x (m, d_model) f32."""
     m, dm = x.shape
+    ws = _proj_ws(ws, m, dm, (hq + 2 * hkv) * d, x.device, "proj")
     _lib.call("rk_qkv_rope", _lib.ptr(x), m, dm, _lib.ptr(w_qkv_packed), hq, hkv, d, _lib.ptr(pos), _lib.ptr(freq),
               _lib.ptr(q_out), _lib.ptr(k_out), _lib.ptr(v_out),
-              int(hkv * d if kv_row_stride is None else kv_row_stride), _lib.stream_ptr(stream))
+              int(hkv * d if kv_row_stride is None else kv_row_stride), _lib.ptr(ws), ws.numel(),
+              _lib.stream_ptr(stream))
 
 
-def out_proj(a: torch.Tensor, w_o_packed: torch.Tensor, resid: torch.Tensor, stream=None) -> None:
+def out_proj(a: torch.Tensor, w_o_packed: torch.Tensor, resid: torch.Tensor, ws: torch.Tensor | None = None,
+             stream=None) -> None:
     """resid (m, d_model) += a (m, k) W_o."""
     m, k = a.shape
+    ws = _proj_ws(ws, m, k, resid.shape[1], a.device, "proj")
     _lib.call("rk_out_proj", _lib.ptr(a), m, k, _lib.ptr(w_o_packed), resid.shape[1], _lib.ptr(resid),
-              _lib.stream_ptr(stream))
+              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
 
 
 def lm_head(x: torch.Tensor, emb_packed: torch.Tensor, vocab: int, emb: torch.Tensor, x_next: torch.Tensor,
@@ -229,7 +247,7 @@ def lm_head(x: torch.Tensor, emb_packed: torch.Tensor, vocab: int, emb: torch.Te
             log_stride: int = 0, ws: torch.Tensor | None = None, stream=None) -> None:
     """tokens = first argmax of x E^T; x_next = E[tokens]; pos += 1 (when given)."""
     m, dm = x.shape
-    need = _lib.lib.rk_lm_head_workspace_bytes(m, vocab)
+    need = _lib.lib.rk_lm_head_workspace_bytes(m, vocab, dm)
     if ws is None or ws.numel() < need:
         ws = scratch(need, x.device, "lm_head")
     _lib.call("rk_lm_head", _lib.ptr(x), m, dm, _lib.ptr(emb_packed), vocab, _lib.ptr(emb), _lib.ptr(x_next),

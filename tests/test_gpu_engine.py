@@ -268,9 +268,9 @@ def test_engine_accounting():
     resident, full = eng.gpu_kv_bytes()
     assert 1 - resident / full > 0.54                      # >= 54 % GPU KV saved (north star)
     assert eng.K == 4
-    # Llama-3-8B-shaped projections: 41.9 M parameters per layer (bf16), + the tied logits (vocab padded to 272)
+    # Llama-3-8B-shaped projections: 41.9 M parameters per layer (bf16), + the tied logits (vocab 258)
     per_layer = (4096 * (32 + 16) * 128 + 4096 * 4096) * 2
-    assert eng.weight_bytes_per_token() == 32 * per_layer + 4096 * 272 * 2
+    assert eng.weight_bytes_per_token() == 32 * per_layer + 4096 * 258 * 2
 
 
 def test_engine_c2_full_shapes_turn_matches_oracle():
