@@ -44,7 +44,10 @@ namespace {
 // next layer's CTAs prefetch under PDL, measured slower at every batch.)
 constexpr int kCW = 8;                       // consumer warps
 constexpr int kThreads = (kCW + 1) * 32;
-constexpr int kStg = 3;
+#ifndef RK_CL_STAGES
+#define RK_CL_STAGES 3
+#endif
+constexpr int kStg = RK_CL_STAGES;
 constexpr int kBoxRows = 16;                 // keys per box (one consumer warp's group)
 constexpr int kTK = kBoxRows * kCW;          // keys per stage
 constexpr int kBoxBytes = kBoxRows * 128;    // 16 keys x 64 bf16 dims

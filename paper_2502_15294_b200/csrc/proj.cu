@@ -40,6 +40,9 @@
 //   out : x += attention_out W_o (the residual, engine.py:267);
 //   head: logits (engine.py:270-271), then rk_argmax_embed picks the first
 //         maximum (pipeline.py:308, np.argmax) and looks up the next input.
+#include <cstdlib>
+#include <type_traits>
+
 #include "decode_common.cuh"
 #include "rk_common.cuh"
 #include "tc_common.cuh"
@@ -78,7 +81,7 @@ constexpr int kWarps = 12;
 constexpr int kThreads = kWarps * 32;
 constexpr int kWProducer = 0, kMma = 2, kConv0 = 4, kEpi0 = 8;
 #ifndef PJ_BUDGET_KB
-#define PJ_BUDGET_KB 110
+#define PJ_BUDGET_KB 200
 #endif
 constexpr int kSmemBudget = PJ_BUDGET_KB * 1024;
 
@@ -89,15 +92,17 @@ struct Cfg {
   static constexpr int XHL = 2 * NP * 128;            // hi tile | lo tile
   static constexpr int XH = NP >= 64 ? 2 : 3;
   static constexpr int EPT = NP / 8;                  // float4 of a unit's x slice per converter thread
-  static constexpr int PD = NP >= 64 ? 2 : (NP >= 32 ? 4 : 8);   // units of x in flight (registers)
+  static constexpr int PD = 16 / EPT < 1 ? 1 : 16 / EPT;   // units of x in flight (registers)
   static constexpr int ROPE = NP <= 32 ? NP * (BM / 2) * 8 : 0;    // (cos, sin) table [t][pair]
-  static constexpr int WS = (kSmemBudget - 1024 - XH * XHL - ROPE - 1024) / W_BYTES;
-  static constexpr int SMEM = 1024 + WS * W_BYTES + XH * XHL + ROPE + 1024;
+  static constexpr int RED = NP * BM * 4;             // cluster mode: this CTA's partial [NP][128] f32
+  static constexpr int WS = (kSmemBudget - 1024 - XH * XHL - ROPE - RED - 1024) / W_BYTES;
+  static constexpr int SMEM = 1024 + WS * W_BYTES + XH * XHL + ROPE + RED + 1024;
   static constexpr int TMEM_COLS = 4 * NP < 32 ? 32 : 4 * NP;   // 2 buffers x [hi | lo] columns
   static_assert(WS >= 3, "weight ring too shallow");
 };
 
 struct Params {
+  int cs;                                  // cluster mode: CTAs per strip group (the cluster size)
   const void* w;                           // tiled, swizzled W^T (rk_pack_weight)
   const float* x;                          // [m][K] activations
   int m, K, N, Npad, mode;
@@ -163,16 +168,14 @@ __device__ __forceinline__ void finish(const Params& p, int sg, int row, float (
   const int n = sg * BM + row;
   if (p.mode == PJ_QKV) {
     const int qd = p.hq * p.d, kd = p.hkv * p.d;
-    float other[NP];
+    const bool even = (n & 1) == 0, valid = n < p.N, rot = n < qd + kd;
+    const double f = rot ? p.freq[(n % p.d) >> 1] : 0.0;
 #pragma unroll
-    for (int t = 0; t < NP; ++t) other[t] = __shfl_xor_sync(0xffffffffu, v[t], 1);
-    if (n >= p.N) return;
-    const bool even = (n & 1) == 0;
-    if (n < qd + kd) {
-      const double f = p.freq[(n % p.d) >> 1];
-#pragma unroll
-      for (int t = 0; t < NP; ++t) {
-        if (t >= p.m) break;
+    for (int t = 0; t < NP; ++t) {
+      if (t >= p.m) break;                                          // uniform: every lane has the same m
+      const float other = __shfl_xor_sync(0xffffffffu, v[t], 1);   // the pair partner (all lanes take part)
+      if (!valid) continue;
+      if (rot) {
         double sn, cs;
         if (rope) {
           const float2 e = rope[t * (BM / 2) + (row >> 1)];
@@ -181,17 +184,13 @@ __device__ __forceinline__ void finish(const Params& p, int sg, int row, float (
         } else {
           sincos((double)p.pos[t] * f, &sn, &cs);
         }
-        const double x0 = even ? v[t] : other[t], x1 = even ? other[t] : v[t];
+        const double x0 = even ? v[t] : other, x1 = even ? other : v[t];
         const float y = even ? (float)(x0 * cs - x1 * sn) : (float)(x0 * sn + x1 * cs);
         if (n < qd)
           p.q_out[(size_t)t * qd + n] = y;
         else
           p.k_out[(size_t)t * p.kv_stride + (n - qd)] = __float2bfloat16_rn(y);
-      }
-    } else {
-#pragma unroll
-      for (int t = 0; t < NP; ++t) {
-        if (t >= p.m) break;
+      } else {
         p.v_out[(size_t)t * p.kv_stride + (n - qd - kd)] = __float2bfloat16_rn(v[t]);
       }
     }
@@ -212,11 +211,59 @@ __device__ __forceinline__ void finish(const Params& p, int sg, int row, float (
   }
 }
 
+// the fused epilogue for one feature pair (n, n + 1), n = sg * 128 + 2 pr, of
+// token t (cluster mode): same arithmetic as finish()
+__device__ __forceinline__ void finish_pair(const Params& p, int sg, int pr, int t, float y0, float y1,
+                                            const float2* rope) {
+  const int n = sg * BM + 2 * pr;
+  if (n >= p.N) return;
+  if (p.mode == PJ_QKV) {
+    const int qd = p.hq * p.d, kd = p.hkv * p.d;
+    if (n < qd + kd) {
+      double sn, cs;
+      if (rope) {
+        const float2 e = rope[t * (BM / 2) + pr];
+        cs = e.x;
+        sn = e.y;
+      } else {
+        sincos((double)p.pos[t] * p.freq[(n % p.d) >> 1], &sn, &cs);
+      }
+      const float a = (float)((double)y0 * cs - (double)y1 * sn), b = (float)((double)y0 * sn + (double)y1 * cs);
+      if (n < qd)
+        *reinterpret_cast<float2*>(p.q_out + (size_t)t * qd + n) = make_float2(a, b);
+      else
+        *reinterpret_cast<uint32_t*>(p.k_out + (size_t)t * p.kv_stride + (n - qd)) = pack_bf16(a, b);
+    } else {
+      *reinterpret_cast<uint32_t*>(p.v_out + (size_t)t * p.kv_stride + (n - qd - kd)) = pack_bf16(y0, y1);
+    }
+  } else if (p.mode == PJ_OUT) {
+    float2* r = reinterpret_cast<float2*>(p.resid + (size_t)t * p.N + n);
+    const float2 o = *r;
+    *r = make_float2(o.x + y0, o.y + y1);
+  } else {
+    *reinterpret_cast<float2*>(p.logits + (size_t)t * p.Npad + n) = make_float2(y0, y1);
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
 // v = the sum over the strip group's contributors (CTA order) of their
-// partials; every load of a chunk of 8 tokens is in flight at once
+// partials: the loads of 4 contributors x 16 tokens are in flight at once
 template <int NP>
 __device__ __forceinline__ void reduce_partials(const Params& p, int sg, int row, int ncontrib, float (&v)[NP]) {
-  constexpr int TC = NP < 8 ? NP : 8;
+  constexpr int TC = NP < 16 ? NP : 16, CC = 4;
   const float* base = p.part + (size_t)sg * p.maxc * p.m * BM + row;
 #pragma unroll
   for (int t0 = 0; t0 < NP; t0 += TC) {
@@ -224,16 +271,16 @@ __device__ __forceinline__ void reduce_partials(const Params& p, int sg, int row
     float acc[TC];
 #pragma unroll
     for (int tt = 0; tt < TC; ++tt) acc[tt] = 0.f;
-    for (int c0 = 0; c0 < ncontrib; c0 += 8) {
-      float x[8][TC];
+    for (int c0 = 0; c0 < ncontrib; c0 += CC) {
+      float x[CC][TC];
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
+      for (int cc = 0; cc < CC; ++cc)
 #pragma unroll
         for (int tt = 0; tt < TC; ++tt)
           x[cc][tt] = (c0 + cc < ncontrib && t0 + tt < p.m)
                           ? __ldcg(base + ((size_t)(c0 + cc) * p.m + t0 + tt) * BM) : 0.f;
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc)
+      for (int cc = 0; cc < CC; ++cc)
 #pragma unroll
         for (int tt = 0; tt < TC; ++tt) acc[tt] += x[cc][tt];      // fixed order: deterministic
     }
@@ -248,7 +295,11 @@ __device__ __forceinline__ int ticket_acq_rel(int* t) {
   return old;
 }
 
-template <int NP>
+// CL = cluster mode: a cluster of p.cs CTAs per strip group, each a contiguous
+// k range, partials added through distributed shared memory (no global round
+// trips in the kernel's tail); otherwise the ticketed split-K over a flat run
+// of units per CTA.
+template <int NP, bool CL>
 __global__ void __launch_bounds__(kThreads, 1)
 proj_tc_kernel(const __grid_constant__ Params p) {
   using C = Cfg<NP>;
@@ -257,7 +308,8 @@ proj_tc_kernel(const __grid_constant__ Params p) {
   uint8_t* wring = smem;                              // WS x 16 KB (SW128 K-major A tiles)
   uint8_t* xhl = wring + C::WS * W_BYTES;             // XH x [hi NP x 128 B | lo NP x 128 B]
   float2* rope_tab = reinterpret_cast<float2*>(xhl + C::XH * C::XHL);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xhl + C::XH * C::XHL + C::ROPE);
+  float* red = reinterpret_cast<float*>(xhl + C::XH * C::XHL + C::ROPE);     // [NP][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xhl + C::XH * C::XHL + C::ROPE + C::RED);
   uint64_t* wfull = bars;
   uint64_t* wempty = wfull + C::WS;
   uint64_t* hfull = wempty + C::WS;
@@ -269,7 +321,15 @@ proj_tc_kernel(const __grid_constant__ Params p) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, c = blockIdx.x;
-  const int u0 = (int)((int64_t)c * p.n_units / G), u1 = (int)((int64_t)(c + 1) * p.n_units / G);
+  int u0, u1;
+  if constexpr (CL) {               // strip group c / cs, k chunks [r KC / cs, (r + 1) KC / cs)
+    const int sg = c / p.cs, r = c - sg * p.cs;
+    u0 = sg * p.KC + r * p.KC / p.cs;
+    u1 = sg * p.KC + (r + 1) * p.KC / p.cs;
+  } else {
+    u0 = (int)((int64_t)c * p.n_units / G);
+    u1 = (int)((int64_t)(c + 1) * p.n_units / G);
+  }
   const int n = u1 - u0;
 
   if (threadIdx.x == 0) {
@@ -430,11 +490,10 @@ proj_tc_kernel(const __grid_constant__ Params p) {
       fence_before();
       bar_arrive(&accempty[b]);
       if (threadIdx.x == kEpi0 * 32) PJT(7);
-#ifdef PJ_NO_EPI
-      if (true) {
-#else
-      if (len == p.KC) {
-#endif
+      if constexpr (CL) {             // this CTA's partial -> smem; the cluster adds them below
+#pragma unroll
+        for (int t = 0; t < NP; ++t) red[t * BM + row] = v[t];
+      } else if (len == p.KC) {
         finish<NP>(p, sg, row, v, rope);
       } else {
         // split-K: publish the partial; the last of the group's contributors
@@ -462,6 +521,30 @@ proj_tc_kernel(const __grid_constant__ Params p) {
       ++q;
     }
     if (threadIdx.x == kEpi0 * 32) PJT(5);
+  }
+  if constexpr (CL) {
+    cluster_sync_all();               // every CTA's partial is in its shared memory
+    if (warp >= kEpi0) {
+      // rank r finishes feature pairs [r 64 / cs, (r + 1) 64 / cs) of the strip
+      // group: the cluster's partials added in rank order (deterministic)
+      const int sg = c / p.cs, r = c - sg * p.cs, tid = threadIdx.x - kEpi0 * 32;
+      const int p0 = r * (BM / 2) / p.cs, np_ = (r + 1) * (BM / 2) / p.cs - p0;
+      const bool tab = C::ROPE > 0 && p.mode == PJ_QKV && BM % p.d == 0;
+      const float2* rope = tab ? rope_tab : nullptr;
+      const uint32_t red_a = sa(red);
+      for (int e = tid; e < np_ * p.m; e += 128) {
+        const int t = e / np_, pr = p0 + (e - t * np_);
+        const uint32_t off = (uint32_t)(t * BM + 2 * pr) * 4;
+        float2 y = make_float2(0.f, 0.f);
+        for (int q = 0; q < p.cs; ++q) {
+          const float2 z = ld_dsmem_f2(mapa_u32(red_a + off, (uint32_t)q));
+          y.x += z.x;
+          y.y += z.y;
+        }
+        finish_pair(p, sg, pr, t, y.x, y.y, rope);
+      }
+    }
+    cluster_sync_all();               // the peers are done reading this CTA's partial
   }
   fence_before();
   __syncthreads();
@@ -527,12 +610,11 @@ static ProjPlan proj_plan(int m, int K, int N) {
   return pl;
 }
 
-template <int NP>
-static int launch_np(const pj::Params& p, int grid,
-                     cudaStream_t st) {
+template <int NP, bool CL>
+static int launch_np(const pj::Params& p, int grid, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    RK_CUDA(cudaFuncSetAttribute(pj::proj_tc_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RK_CUDA(cudaFuncSetAttribute(pj::proj_tc_kernel<NP, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  pj::Cfg<NP>::SMEM), "proj smem attribute");
     attr_set = true;
   }
@@ -541,14 +623,59 @@ static int launch_np(const pj::Params& p, int grid,
   cfg.blockDim = dim3(pj::kThreads);
   cfg.dynamicSmemBytes = pj::Cfg<NP>::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CL ? p.cs : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, pj::proj_tc_kernel<NP>, p);
+  cfg.numAttrs = CL ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pj::proj_tc_kernel<NP, CL>, p);
   if (e != cudaSuccess) return cuda_status(e, "proj_tc_kernel launch");
   return RK_OK;
+}
+
+// clusters of `cs` CTAs of the NP kernel that can be co-resident on this GPU (0 = unknown)
+template <int NP>
+static int max_clusters(int cs) {
+  static int cache[17] = {0};
+  if (cs < 1 || cs > 16) return 0;
+  if (cache[cs] == 0) {
+    if (cudaFuncSetAttribute(pj::proj_tc_kernel<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pj::Cfg<NP>::SMEM) != cudaSuccess)
+      return 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs * 64);
+    cfg.blockDim = dim3(pj::kThreads);
+    cfg.dynamicSmemBytes = pj::Cfg<NP>::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, pj::proj_tc_kernel<NP, true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      nc = -1;
+    }
+    cache[cs] = nc;
+  }
+  return cache[cs] > 0 ? cache[cs] : 0;
+}
+
+// the cluster size for a launch: the largest cs <= 8 with n_sg clusters of cs
+// co-resident on the GPU (one wave), or 0 = ticketed split-K
+template <int NP>
+static int pick_cs(int n_sg, int KC) {
+  if (getenv("RK_PROJ_NO_CLUSTER")) return 0;
+  int best = 0;
+  for (int cs = 2; cs <= 8 && cs <= KC; ++cs)
+    if (n_sg * cs <= sm_count() && max_clusters<NP>(cs) >= n_sg) best = cs;
+  return best;
 }
 
 // y = x W for rows [0, m) in launches of <= 64 rows
@@ -585,12 +712,22 @@ static int launch_proj(pj::Params p, const float* x, const void* w_packed, void*
       return fail(RK_ERR_DOMAIN, "lm_head rows %d > 64 per call", m_all);
     }
     q.x = x + (size_t)m0 * p.K;
+    auto run = [&](auto np_tag) -> int {
+      constexpr int NP = decltype(np_tag)::value;
+      const int cs = pick_cs<NP>(pl.n_sg, pl.KC);
+      if (cs > 1) {
+        q.cs = cs;
+        return launch_np<NP, true>(q, pl.n_sg * cs, st);
+      }
+      q.cs = 0;
+      return launch_np<NP, false>(q, pl.grid, st);
+    };
     if (q.m <= 16)
-      r = launch_np<16>(q, pl.grid, st);
+      r = run(std::integral_constant<int, 16>{});
     else if (q.m <= 32)
-      r = launch_np<32>(q, pl.grid, st);
+      r = run(std::integral_constant<int, 32>{});
     else
-      r = launch_np<64>(q, pl.grid, st);
+      r = run(std::integral_constant<int, 64>{});
     if (r != RK_OK) return r;
   }
   return RK_OK;

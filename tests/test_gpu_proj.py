@@ -36,9 +36,12 @@ def _rope64(y, pos, d, freq):
 SHAPES = [(32, 8, 128), (28, 4, 128), (8, 8, 64), (8, 2, 128)]
 
 
+@pytest.mark.parametrize("mode", ["cluster", "ticket"])
 @pytest.mark.parametrize("hq,hkv,d", SHAPES)
 @pytest.mark.parametrize("m", [1, 3, 16, 17, 32, 40, 64, 100])
-def test_qkv_rope_matches_float64(hq, hkv, d, m):
+def test_qkv_rope_matches_float64(hq, hkv, d, m, mode, monkeypatch):
+    if mode == "ticket":
+        monkeypatch.setenv("RK_PROJ_NO_CLUSTER", "1")
     g = torch.Generator(device="cuda").manual_seed(1000 * m + hq)
     D = hq * d
     qd, kd = hq * d, hkv * d
@@ -68,9 +71,15 @@ def test_qkv_rope_matches_float64(hq, hkv, d, m):
     assert torch.all(kbuf[:, kd:] == 0) and torch.all(vbuf[:, kd:] == 0)
 
 
+@pytest.mark.parametrize("mode", ["cluster", "ticket"])
 @pytest.mark.parametrize("k,n", [(4096, 4096), (3584, 3584), (512, 512), (4096, 384)])
 @pytest.mark.parametrize("m", [1, 16, 33, 64, 70])
-def test_out_proj_accumulates_residual(k, n, m):
+def test_out_proj_accumulates_residual(k, n, m, mode, monkeypatch):
+    """Both split-K reductions: partials added through distributed shared memory
+    inside a cluster per strip group, or published and added by the last CTA
+    of a ticket (RK_PROJ_NO_CLUSTER)."""
+    if mode == "ticket":
+        monkeypatch.setenv("RK_PROJ_NO_CLUSTER", "1")
     g = torch.Generator(device="cuda").manual_seed(7 * m + k)
     w = (torch.randn((k, n), generator=g, device="cuda") / np.sqrt(k)).to(torch.bfloat16)
     a = torch.randn((m, k), generator=g, device="cuda")
@@ -83,8 +92,11 @@ def test_out_proj_accumulates_residual(k, n, m):
     assert err < 1e-5, err
 
 
-def test_projection_deterministic():
+@pytest.mark.parametrize("mode", ["cluster", "ticket"])
+def test_projection_deterministic(mode, monkeypatch):
     """Split-K partials are added in CTA order: repeated launches are bitwise equal."""
+    if mode == "ticket":
+        monkeypatch.setenv("RK_PROJ_NO_CLUSTER", "1")
     g = torch.Generator(device="cuda").manual_seed(3)
     w = (torch.randn((4096, 4096), generator=g, device="cuda") / 64).to(torch.bfloat16)
     wp = kernels.pack_weight(w)

@@ -56,6 +56,7 @@ print(f"graph of {sh.num_layers}: {e0.elapsed_time(e1) * 1000 / sh.num_layers:.2
 buf = (C.c_ulonglong * (148 * 16))()
 assert _lib.lib.rk_debug_proj_trace(buf, 148 * 16) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 16).astype(np.int64)
+t = t[t[:, 0] > 0]                               # CTAs of this launch (cluster grids use fewer than 148)
 t0 = t[:, 0].min()
 names = ["start", "1st W", "pdl done", "1st X", "last MMA", "epi done", "end", "last acc ld", "partial st",
          "ticket", "red loads", "finish"]
