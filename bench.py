@@ -180,9 +180,10 @@ def reference_arm(args, world, rank):
         if i >= args.warmup:
             samples.append(r)
     tps = sum(s["tokens_per_s"] for s in samples) / len(samples)
-    sample = (f"{cores} dialogues x 1 decode token per step ({args.workload} shapes, GQA expanded to MHA, "
-              f"fp32 KV = 2x the GPU arm's bf16 bytes), one process per core, inputs generated before the "
-              f"timed region; {args.steps} steps")
+    sample = (f"{cores} dialogues x 1 decode token per step ({args.workload} shapes: every layer's projections "
+              f"(float32 BLAS) + RoPE + attention (GQA expanded to MHA, fp32 KV = 2x the GPU arm's bf16 bytes) + "
+              f"residual, Lw-1 scoring + selection, tied logits + argmax), one process per core, inputs generated "
+              f"before the timed region; {args.steps} steps")
     line = {
         "metric": "decode tokens/s", "value": tps, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * samples[-1]["timed_s"], "higher_is_better": True,
@@ -250,6 +251,13 @@ def main():
         return ms, clk.summary(), brk, h2d, kept
 
     ms, clocks, brk, h2d_bytes, kept0 = timed(False, args.steps)
+    # kept rounds of the last timed turn of every dialogue, keyed by its global id (gathered on rank 0):
+    # a dialogue's data and questions are seeded by its global id, so this is independent of the sharding
+    kept_by_dialogue = {int(gid): [int(x) for x in k] for e in eng.groups for gid, k in zip(e.dialogues, e.last_kept)}
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, kept_by_dialogue)
+        kept_by_dialogue = {k: v for part in parts for k, v in part.items()}
     # decode-loop statistics of THIS (device-resident) timed run, before the next runs overwrite them
     dec_busy_ms, dec_bytes, dec_kv_bytes = eng.last_decode_busy_ms, eng.last_decode_bytes, eng.last_decode_kv_bytes
     dec_launches = eng.last_decode_launches
@@ -352,6 +360,8 @@ def main():
         "breakdown_ms_group0": brk,
         "clocks": clocks,
         "kept_dialogue0": [int(x) for x in kept0[0]],
+        "kept_by_dialogue": ({str(k): kept_by_dialogue[k] for k in sorted(kept_by_dialogue)}
+                             if len(kept_by_dialogue) <= 64 else None),
         "host": {"numa_node": numa, "pinned_round_bytes": sum(e.host_sets * e.cfg.rounds for e in eng.groups)
                  * g0.host_blocks[0][0].numel() * 2},
     }
@@ -370,8 +380,9 @@ def main():
                                                  hkv=cfg.hkv, d=cfg.head_dim, rounds=cfg.rounds,
                                                  T=cfg.round_tokens, K=g0.K, processes=cores)
             line["cpu_baseline"] = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": cores, "kind": kind,
-                                    "sample": f"{cores} dialogues x 1 decode token ({args.workload} shapes, fp32 KV, "
-                                              f"attention path only: no projections), one process per core, timed "
+                                    "sample": f"{cores} dialogues x 1 decode token ({args.workload} shapes: projections "
+                                              f"(float32 BLAS) + RoPE + attention (fp32 KV) + residual per layer, "
+                                              f"scoring + selection, tied logits), one process per core, timed "
                                               f"{r['timed_s']:.1f}s after input generation"}
         except Exception as exc:  # the GPU number stands on its own
             line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}

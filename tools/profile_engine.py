@@ -18,19 +18,27 @@ ap.add_argument("--decode-steps", type=int, default=4)
 ap.add_argument("--turns", type=int, default=2)
 ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--eager", action="store_true")
+ap.add_argument("--profile-turns", action="store_true",
+                help="cudaProfilerStart/Stop around the turns (ncu --profile-from-start off)")
 a = ap.parse_args()
 w = dict(WORKLOADS[a.workload])
 w["decode_steps"] = a.decode_steps
 if a.batch:
     w["batch"] = a.batch
 eng = RoundDecodeEngine(EngineConfig(**w))
+if not a.eager:
+    eng.prepare(e2e=False)
+torch.cuda.synchronize()
+if a.profile_turns:
+    torch.cuda.profiler.start()
 if a.eager:
     with torch.cuda.stream(eng.compute_stream):
         for _ in range(a.turns):
             eng.run_turn_eager()
 else:
-    eng.prepare(e2e=False)
     for _ in range(a.turns):
         eng.run_turn()
 torch.cuda.synchronize()
+if a.profile_turns:
+    torch.cuda.profiler.stop()
 print("turns done", eng.turn_breakdown_ms() if not a.eager else "")
