@@ -171,6 +171,21 @@ int rk_select_batch(const double* raw, int n, int ld, int batch, int normalize, 
                     int k_top, double kappa, double* masses_out, int32_t* kept_out, int32_t* n_kept_out,
                     int32_t* degenerate_out, int32_t* status_out, rk_stream_t stream);
 
+/* Selection over each dialogue's ACTIVE rounds (the inactivity drop policy:
+ * selection.py:183-204 ActivityLedger + pipeline.py:238-245 active_rounds).
+ * raw [batch][ld] float64 holds the Eq. 1 mass of every one of the n rounds
+ * (inactive ones included); active [batch][ld] uint8 (NULL = all active).  Per
+ * dialogue the active rounds are taken in ascending order, normalized and
+ * selected as rk_select_batch; kept_out receives ROUND IDS (ascending),
+ * masses_out the normalized masses at the compacted positions.  top_percent
+ * with k_top <= 0 sizes k per dialogue from fraction / min_rounds and the
+ * dialogue's active count (selection.py:87-97).  margin_out [batch] (nullable)
+ * as rk_selection_margin.  n <= 2048. */
+int rk_select_batch_active(const double* raw, int n, int ld, int batch, const uint8_t* active, int normalize,
+                           int kind, double v, int k_top, double fraction, int min_rounds, double kappa,
+                           double* masses_out, int32_t* kept_out, int32_t* n_kept_out, int32_t* degenerate_out,
+                           int32_t* status_out, double* margin_out, rk_stream_t stream);
+
 /* Decision margin of the selection made from `masses` (rows ld apart):
  * top_percent (m_(K) - m_(K+1)) / m_(K) of the K-th / (K+1)-th largest masses;
  * fixed min |m - v| / v; adaptive min |m - cut| / |cut|; all +inf.
@@ -205,6 +220,18 @@ int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d,
                           const int32_t* items, int items_stride, const int32_t* n_items,
                           int n_bins, const uint8_t* active, int n_out, double* raw_out,
                           void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
+/* capture_mode="pre" (engine.py:187-200, Model._capture_pre): the same Eq. 1
+ * masses from ONE softmax per query row over the head-summed logits
+ * sum_h q_h . k_kv(h) / (Hq * sqrt(d)) (fp64; einsum "nhd,shd->ns"), instead of
+ * the head-summed per-head probabilities.  Arguments, workspace and outputs as
+ * rk_round_scores_exact (hq*d*8 bytes of shared memory per row, <= 200 KB). */
+int rk_round_scores_exact_pre(const float* q, int batch, int n_q, int hq, int d,
+                              const void* k, int kv_dtype, int hkv, int64_t k_batch_stride,
+                              const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                              const int32_t* items, int items_stride, const int32_t* n_items,
+                              int n_bins, const uint8_t* active, int n_out, double* raw_out,
+                              void* workspace, size_t workspace_bytes, rk_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * 5. Batched host->HBM gather of kept rounds' upper-layer blocks

@@ -99,6 +99,25 @@ def _forward(q, k, v, q_pos, k_pos, allowed, capture):
     return out, cap
 
 
+def capture_pre(q, k, q_pos, k_pos, allowed=None):
+    """engine.py:187-200 (Model._capture_pre, capture_mode="pre"): one softmax per
+    query row over the head-summed fp64 logits sum_h q_h . k_h / (H sqrt(d)),
+    masked keys excluded.  q (n, Hq, d); k (s, Hkv, d) with GQA heads expanded
+    as repeat_kv (Hkv = Hq for the reference's MHA model).  Returns (n, s)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    hq, hkv, d = q.shape[1], k.shape[1], q.shape[2]
+    k = np.repeat(k, hq // hkv, axis=1)
+    logits = np.einsum("nhd,shd->ns", q, k) / (hq * np.sqrt(d))
+    vis = np.asarray(k_pos)[None, :] <= np.asarray(q_pos)[:, None]
+    if allowed is not None:
+        vis = vis & np.asarray(allowed, dtype=bool)[None, :]
+    logits = np.where(vis, logits, -np.inf)
+    logits -= logits.max(axis=1, keepdims=True)
+    w = np.exp(logits)
+    return w / w.sum(axis=1, keepdims=True)
+
+
 def round_to_bf16(x: np.ndarray) -> np.ndarray:
     """float32 values rounded to the nearest bf16 (round-to-nearest-even),
     returned as float32 — the identical inputs fed to both sides for bf16 parity."""

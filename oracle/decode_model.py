@@ -23,7 +23,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import rounds as orr
-from .attention import round_to_bf16
+from .attention import capture_pre, round_to_bf16
 
 SEP_TOKEN = 256
 
@@ -92,10 +92,13 @@ class TurnOracle:
 
 
 def run_turn(oracle: TurnOracle, lower_k, lower_v, upper_blocks_fn, question_token, hist, round_tokens, n_rounds,
-             lw, policy, decode_steps):
+             lw, policy, decode_steps, capture_mode="post", active=None):
     """One turn of one dialogue.  lower_k/v: [lw] arrays (hist, Hkv, d);
     upper_blocks_fn(kept) -> [L-lw] pairs (K, V) of the kept rounds' keys in
-    the engine's slot order.  Returns dict(kept, raw, masses, answer, x)."""
+    the engine's slot order.  capture_mode "pre": the head-summed-logit capture
+    (engine.py:187-200); active: the candidate rounds (the drop policy's
+    active_rounds, pipeline.py:238-245; None = every round).
+    Returns dict(kept, raw, masses, answer, x)."""
     L = oracle.L
     T = round_tokens
     x = oracle.w["emb"][question_token].astype(np.float32)
@@ -104,11 +107,14 @@ def run_turn(oracle: TurnOracle, lower_k, lower_v, upper_blocks_fn, question_tok
     lv = [v.copy() for v in lower_v]
     cap = None
     for l in range(lw):
-        x, lk[l], lv[l], c, _ = oracle.layer(l, x, pos, lk[l], lv[l], capture=(l == lw - 1))
+        x, lk[l], lv[l], c, q = oracle.layer(l, x, pos, lk[l], lv[l], capture=(l == lw - 1))
         if c is not None:
             cap = c
-    raw = np.array([cap[r * T:(r + 1) * T].sum() for r in range(n_rounds)])
-    dist = orr.normalize(raw)
+            if capture_mode == "pre":
+                cap = capture_pre(q[None], lk[l], [pos], np.arange(lk[l].shape[0]))[0]
+    act = list(range(n_rounds)) if active is None else list(active)
+    raw = np.array([cap[r * T:(r + 1) * T].sum() for r in act])
+    dist = orr.normalize(raw, round_indices=act)
     kept = orr.select(dist, policy)
     uk, uv = [], []
     blocks = upper_blocks_fn(kept)

@@ -245,6 +245,39 @@ def block_nbytes(tokens, hidden, layers):
     return 2 * MODELED_ELEM_BYTES * tokens * hidden * layers
 
 
+class ActivityLedger:
+    """selection.py:168-204: last-active turn per round and the inactivity drop rule."""
+
+    def __init__(self, window=math.inf, protect_recent=2):
+        self.window = window
+        self.protect_recent = protect_recent
+        self.last_active = {}
+        self.dropped = set()
+
+    def register_round(self, round_index, turn):
+        self.last_active.setdefault(round_index, turn)
+
+    def active_rounds(self, upto):
+        return [m for m in range(upto) if m not in self.dropped]
+
+    def update_and_drop(self, kept, current_turn, total_rounds):
+        kept = set(kept)
+        for m in kept:
+            self.last_active[m] = current_turn
+        if math.isinf(self.window):
+            return []
+        drops = []
+        for m in range(total_rounds):
+            if m in self.dropped or m in kept:
+                continue
+            if m >= total_rounds - self.protect_recent:
+                continue
+            if current_turn - self.last_active.get(m, current_turn) >= self.window:
+                drops.append(m)
+        self.dropped.update(drops)
+        return drops
+
+
 @dataclass
 class TurnRecord:
     turn: int

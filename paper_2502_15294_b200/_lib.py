@@ -43,10 +43,13 @@ _SIGS = {
     "rk_aggregate_rounds": (_i, [_p, _i64, _i, _i, _p, _i, _p, _p]),
     "rk_select": (_i, [_p, _i, _i, _i, _d, _i, _d, _p, _p, _p, _p, _p, _p]),
     "rk_select_batch": (_i, [_p, _i, _i, _i, _i, _i, _d, _i, _d, _p, _p, _p, _p, _p, _p]),
+    "rk_select_batch_active": (_i, [_p, _i, _i, _i, _p, _i, _i, _d, _i, _d, _i, _d, _p, _p, _p, _p, _p, _p, _p]),
     "rk_selection_margin": (_i, [_p, _i, _i, _i, _i, _d, _i, _d, _p, _p]),
     "rk_round_scores_exact_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
     "rk_round_scores_exact": (_i, [_p, _i, _i, _i, _i, _p, _i, _i, _i64, _p, _i, _p, _p, _p, _i, _p, _i, _p, _i,
                                    _p, _p, _sz, _p]),
+    "rk_round_scores_exact_pre": (_i, [_p, _i, _i, _i, _i, _p, _i, _i, _i64, _p, _i, _p, _p, _p, _i, _p, _i, _p, _i,
+                                       _p, _p, _sz, _p]),
     "rk_h2d_gather": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "rk_d2h_scatter": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "rk_prefill_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i]),

@@ -134,21 +134,12 @@ def layer_round_masses(model, conv, n: int, *, chunk: int = 256) -> np.ndarray:
     scoring — the capture matrices of capture_all_layers are never formed."""
     import torch
 
-    from .stats import SEGMENT_QUESTION, aggregate_round_attention
-
     c = model.config
     L, H, dk = c.num_layers, c.num_heads, c.d_k
     r_n = conv.rounds[n]
     q0, q1 = r_n.q_span
     if q1 <= q0:
         raise DomainError(f"round {n} has an empty question segment")
-    if c.capture_mode != "post":
-        # "pre" capture (engine.py:187-200) has no fused form: materialised captures
-        cache = model.new_cache()
-        _, caps = model.forward_range(cache, 0, L, tokens=conv.token_ids, positions=np.arange(conv.num_tokens),
-                                      capture_layers=range(L))
-        return np.stack([normalize(aggregate_round_attention(caps[l], conv.rounds, SEGMENT_QUESTION, n),
-                                   layer=l).masses for l in range(L)])
     # every prior round receives a bin; keys from round n onwards are the
     # denominator-only bin (causal visibility keeps later keys out)
     bounds = [(conv.rounds[m].start, conv.rounds[m].end, m) for m in range(n)]
@@ -158,7 +149,8 @@ def layer_round_masses(model, conv, n: int, *, chunk: int = 256) -> np.ndarray:
 
     def hook(l, q, kv):
         keys = kv.keys.view(-1, H, dk)
-        raws[l] = round_scores(q[q0:q1].contiguous(), keys, q_pos, kv.positions, bounds, n, chunk=chunk)
+        raws[l] = round_scores(q[q0:q1].contiguous(), keys, q_pos, kv.positions, bounds, n, chunk=chunk,
+                               capture_mode=c.capture_mode)
 
     cache = model.new_cache()
     model.forward_range(cache, 0, L, tokens=conv.token_ids, positions=np.arange(conv.num_tokens),

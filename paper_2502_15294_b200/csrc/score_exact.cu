@@ -75,6 +75,63 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// One key sub-chunk's logits (acc * scale; masked keys -> -inf) folded into the
+// running (m, l) per (row, head): sub-chunk max by a fixed warp/block tree, then
+// sum exp(s - max), merged into the running statistics.
+template <int RT, int G>
+__device__ __forceinline__ void chunk_stats(const double (&acc)[RT][G], bool in, int64_t kp, const int64_t (&qp)[RT],
+                                            double scale, double (*red)[RT * G], double* sub_m, double* run_m,
+                                            double* run_l) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double s[RT][G];
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const bool vis = in && kp <= qp[r];
+      s[r][h] = vis ? (scale > 0.0 ? __dmul_rn(acc[r][h], scale) : __ddiv_rn(acc[r][h], -scale)) : -INFINITY;
+      double m = warp_max_d(s[r][h]);
+      if (lane == 0) red[warp][r * G + h] = m;
+    }
+    __syncthreads();
+    if (tid < RT * G) {
+      double m = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kExWarps; ++w) m = fmax(m, red[w][tid]);
+      sub_m[tid] = m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const double m = sub_m[r * G + h];
+        double e = (s[r][h] == -INFINITY) ? 0.0 : exp(__dsub_rn(s[r][h], m));
+        e = warp_sum_d(e);
+        if (lane == 0) red[warp][r * G + h] = e;
+      }
+    __syncthreads();
+    if (tid < RT * G) {
+      double l = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kExWarps; ++w) l = __dadd_rn(l, red[w][tid]);
+      const double m = sub_m[tid];
+      if (m != -INFINITY) {
+        const double M = run_m[tid];
+        if (M == -INFINITY) {
+          run_m[tid] = m;
+          run_l[tid] = l;
+        } else if (m > M) {
+          run_l[tid] = __fma_rn(run_l[tid], exp(__dsub_rn(M, m)), l);
+          run_m[tid] = m;
+        } else {
+          run_l[tid] = __fma_rn(l, exp(__dsub_rn(m, M)), run_l[tid]);
+        }
+      }
+    }
+    __syncthreads();
+}
+
 // grid (items_stride, hkv, batch * row_tiles), block kExThreads.
 // part_m / part_l: [batch][n_q][hq][items_stride] fp64.
 template <typename KT, int RT, int G>
@@ -142,54 +199,7 @@ __global__ void __launch_bounds__(kExThreads) exact_stats_kernel(
         }
       }
     }
-    // logits (masked keys -> -inf), sub-chunk max per (row, head)
-    double s[RT][G];
-#pragma unroll
-    for (int r = 0; r < RT; ++r)
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const bool vis = in && kp <= qp[r];
-        s[r][h] = vis ? __dmul_rn(acc[r][h], scale) : -INFINITY;
-        double m = warp_max_d(s[r][h]);
-        if (lane == 0) red[warp][r * G + h] = m;
-      }
-    __syncthreads();
-    if (tid < RT * G) {
-      double m = red[0][tid];
-#pragma unroll
-      for (int w = 1; w < kExWarps; ++w) m = fmax(m, red[w][tid]);
-      sub_m[tid] = m;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < RT; ++r)
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const double m = sub_m[r * G + h];
-        double e = (s[r][h] == -INFINITY) ? 0.0 : exp(__dsub_rn(s[r][h], m));
-        e = warp_sum_d(e);
-        if (lane == 0) red[warp][r * G + h] = e;
-      }
-    __syncthreads();
-    if (tid < RT * G) {
-      double l = red[0][tid];
-#pragma unroll
-      for (int w = 1; w < kExWarps; ++w) l = __dadd_rn(l, red[w][tid]);
-      const double m = sub_m[tid];
-      if (m != -INFINITY) {
-        const double M = run_m[tid];
-        if (M == -INFINITY) {
-          run_m[tid] = m;
-          run_l[tid] = l;
-        } else if (m > M) {
-          run_l[tid] = __fma_rn(run_l[tid], exp(__dsub_rn(M, m)), l);
-          run_m[tid] = m;
-        } else {
-          run_l[tid] = __fma_rn(l, exp(__dsub_rn(m, M)), run_l[tid]);
-        }
-      }
-    }
-    __syncthreads();
+    chunk_stats<RT, G>(acc, in, kp, qp, scale, red, sub_m, run_m, run_l);
   }
   if (tid < RT * G) {
     const int r = tid / G, h = tid % G;
@@ -198,6 +208,79 @@ __global__ void __launch_bounds__(kExThreads) exact_stats_kernel(
       part_m[o] = run_m[tid];
       part_l[o] = run_l[tid];
     }
+  }
+}
+
+// capture_mode="pre" (engine.py:187-200): ONE logit per (row, key), the
+// head-summed dot product sum_h q_h . k_kv(h) in fp64 (h ascending, t sequential
+// within a head, as the einsum "nhd,shd->ns"), divided by Hq * sqrt(d); one
+// softmax over the keys per row.  The statistics are those of a single "head".
+// grid (items_stride, 1, batch * row_tiles); part_m / part_l [batch][n_q][1][items_stride].
+template <typename KT, int RT>
+__global__ void __launch_bounds__(kExThreads) exact_pre_stats_kernel(
+    const float* __restrict__ q, int n_q, int hq, int d, const KT* __restrict__ k, int64_t k_bstride, int hkv,
+    const int32_t* __restrict__ seq_len, int s_static, const int64_t* __restrict__ q_pos,
+    const int64_t* __restrict__ k_pos, const int32_t* __restrict__ items, int items_stride,
+    const int32_t* __restrict__ n_items_dev, double denom, int row_tiles, double* __restrict__ part_m,
+    double* __restrict__ part_l) {
+  extern __shared__ double qs[];                       // [RT][hq][d]
+  __shared__ double red[kExWarps][RT];
+  __shared__ double run_m[RT], run_l[RT], sub_m[RT];
+  const int it = blockIdx.x;
+  const int b = blockIdx.z / row_tiles;
+  const int r0 = (blockIdx.z % row_tiles) * RT;
+  const int n_items = n_items_dev ? n_items_dev[b] : items_stride;
+  if (it >= n_items) return;
+  const int32_t* tab = items + ((size_t)b * items_stride + it) * 3;
+  const int s_b = seq_len ? seq_len[b] : s_static;
+  const int lo = tab[0];
+  const int hi = min(tab[1], s_b);
+  const int tid = threadIdx.x;
+  const int nr = min(RT, n_q - r0);
+  const int G = hq / hkv;
+
+  for (int x = tid; x < RT * hq * d; x += kExThreads) {
+    const int r = x / (hq * d), rem = x - r * hq * d;
+    qs[x] = r < nr ? (double)q[((size_t)b * n_q + r0 + r) * hq * d + rem] : 0.0;
+  }
+  for (int x = tid; x < RT; x += kExThreads) {
+    run_m[x] = -INFINITY;
+    run_l[x] = 0.0;
+  }
+  int64_t qp[RT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) qp[r] = r < nr ? q_pos[r0 + r] : INT64_MIN;
+  __syncthreads();
+
+  const KT* kb = k + (size_t)b * k_bstride;
+  const int64_t row_stride = (int64_t)hkv * d;
+  for (int c0 = lo; c0 < hi; c0 += kExThreads) {
+    const int j = c0 + tid;
+    const bool in = j < hi;
+    const int64_t kp = in ? (k_pos ? k_pos[j] : (int64_t)j) : 0;
+    double acc[RT][1];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) acc[r][0] = 0.0;
+    if (in) {
+      const KT* kr = kb + (int64_t)j * row_stride;
+      for (int h = 0; h < hq; ++h) {
+        const KT* kh = kr + (size_t)(h / G) * d;
+        for (int t0 = 0; t0 < d; t0 += 8) {
+          double kv[8];
+          KLoad<KT>::load8(kh + t0, kv);
+#pragma unroll
+          for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+            for (int r = 0; r < RT; ++r) acc[r][0] = __fma_rn(qs[(r * hq + h) * d + t0 + tt], kv[tt], acc[r][0]);
+        }
+      }
+    }
+    chunk_stats<RT, 1>(acc, in, kp, qp, -denom, red, sub_m, run_m, run_l);
+  }
+  if (tid < nr) {
+    const size_t o = ((size_t)b * n_q + r0 + tid) * items_stride + it;
+    part_m[o] = run_m[tid];
+    part_l[o] = run_l[tid];
   }
 }
 
@@ -316,6 +399,34 @@ static int launch_exact_stats(const float* q, int batch, int n_q, int hq, int d,
 #undef RK_EXACT_G
 }
 
+template <typename KT>
+static int launch_exact_pre(const float* q, int batch, int n_q, int hq, int d, const void* k, int64_t k_bstride,
+                            int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                            const int32_t* items, int items_stride, const int32_t* n_items, double denom, double* pm,
+                            double* pl, cudaStream_t st) {
+  constexpr int RT = 4;
+  const int rt = n_q == 1 ? 1 : RT;
+  const int row_tiles = (n_q + rt - 1) / rt;
+  dim3 grid(items_stride, 1, batch * row_tiles);
+  const size_t smem = sizeof(double) * rt * hq * d;
+  if (smem > 200 * 1024) return fail(RK_ERR_DOMAIN, "exact pre scoring: %d heads x %d dims", hq, d);
+  if (n_q == 1) {
+    auto kern = exact_pre_stats_kernel<KT, 1>;
+    if (smem > 48 * 1024)
+      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "exact_pre smem");
+    kern<<<grid, kExThreads, smem, st>>>(q, n_q, hq, d, reinterpret_cast<const KT*>(k), k_bstride, hkv, seq_len, s,
+                                         q_pos, k_pos, items, items_stride, n_items, denom, row_tiles, pm, pl);
+  } else {
+    auto kern = exact_pre_stats_kernel<KT, RT>;
+    if (smem > 48 * 1024)
+      RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "exact_pre smem");
+    kern<<<grid, kExThreads, smem, st>>>(q, n_q, hq, d, reinterpret_cast<const KT*>(k), k_bstride, hkv, seq_len, s,
+                                         q_pos, k_pos, items, items_stride, n_items, denom, row_tiles, pm, pl);
+  }
+  RK_CHECK_LAUNCH("exact_pre_stats_kernel");
+  return RK_OK;
+}
+
 }  // namespace rk
 
 using namespace rk;
@@ -327,7 +438,11 @@ size_t rk_round_scores_exact_workspace_bytes(int batch, int n_q, int hq, int ite
   return exact_ws_parts(batch, n_q, hq, items_stride, n_bins, &a, &b);
 }
 
-int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d, const void* k, int kv_dtype, int hkv,
+}  // extern "C"
+
+namespace rk {
+
+static int round_scores_exact_impl(int pre, const float* q, int batch, int n_q, int hq, int d, const void* k, int kv_dtype, int hkv,
                           int64_t k_batch_stride, const int32_t* seq_len, int s, const int64_t* q_pos,
                           const int64_t* k_pos, const int32_t* items, int items_stride, const int32_t* n_items,
                           int n_bins, const uint8_t* active, int n_out, double* raw_out, void* workspace,
@@ -349,7 +464,14 @@ int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d, con
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const double scale = 1.0 / sqrt((double)d);        // the reference's inv_scale (_attn_ext.pyx:36)
   int rc;
-  if (kv_dtype == RK_BF16)
+  if (pre) {
+    const double denom = (double)hq * sqrt((double)d);   // num_heads * sqrt(d_k) (engine.py:191)
+    rc = kv_dtype == RK_BF16
+             ? launch_exact_pre<__nv_bfloat16>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos, k_pos,
+                                               items, items_stride, n_items, denom, pm, pl, st)
+             : launch_exact_pre<float>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos, k_pos, items,
+                                       items_stride, n_items, denom, pm, pl, st);
+  } else if (kv_dtype == RK_BF16)
     rc = n_q == 1 ? launch_exact_stats<__nv_bfloat16, 1>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s,
                                                          q_pos, k_pos, items, items_stride, n_items, scale, pm, pl, st)
                   : launch_exact_stats<__nv_bfloat16, 4>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s,
@@ -360,17 +482,42 @@ int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d, con
                   : launch_exact_stats<float, 4>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos,
                                                  k_pos, items, items_stride, n_items, scale, pm, pl, st);
   if (rc != RK_OK) return rc;
-  const size_t smem = sizeof(double) * (n_bins + 1 + 2 * hq) + sizeof(int) * (n_bins + 2);
+  const int heads = pre ? 1 : hq;          // "pre": one softmax per row
+  const size_t smem = sizeof(double) * (n_bins + 1 + 2 * heads) + sizeof(int) * (n_bins + 2);
   if (smem > 48 * 1024) {
     RK_CUDA(cudaFuncSetAttribute(exact_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
             "exact_rows smem");
   }
-  exact_rows_kernel<<<batch * n_q, 128, smem, st>>>(pm, pl, n_q, hq, items, items_stride, n_items, n_bins, rows);
+  exact_rows_kernel<<<batch * n_q, 128, smem, st>>>(pm, pl, n_q, heads, items, items_stride, n_items, n_bins, rows);
   RK_CHECK_LAUNCH("exact_rows_kernel");
   dim3 g2((n_bins + 127) / 128, batch);
   exact_sum_rows_kernel<<<g2, 128, 0, st>>>(rows, n_q, n_bins, active, n_out, raw_out);
   RK_CHECK_LAUNCH("exact_sum_rows_kernel");
   return RK_OK;
+}
+
+}  // namespace rk
+
+extern "C" {
+
+int rk_round_scores_exact(const float* q, int batch, int n_q, int hq, int d, const void* k, int kv_dtype, int hkv,
+                          int64_t k_batch_stride, const int32_t* seq_len, int s, const int64_t* q_pos,
+                          const int64_t* k_pos, const int32_t* items, int items_stride, const int32_t* n_items,
+                          int n_bins, const uint8_t* active, int n_out, double* raw_out, void* workspace,
+                          size_t workspace_bytes, rk_stream_t stream) {
+  return round_scores_exact_impl(0, q, batch, n_q, hq, d, k, kv_dtype, hkv, k_batch_stride, seq_len, s, q_pos, k_pos,
+                                 items, items_stride, n_items, n_bins, active, n_out, raw_out, workspace,
+                                 workspace_bytes, stream);
+}
+
+int rk_round_scores_exact_pre(const float* q, int batch, int n_q, int hq, int d, const void* k, int kv_dtype, int hkv,
+                              int64_t k_batch_stride, const int32_t* seq_len, int s, const int64_t* q_pos,
+                              const int64_t* k_pos, const int32_t* items, int items_stride, const int32_t* n_items,
+                              int n_bins, const uint8_t* active, int n_out, double* raw_out, void* workspace,
+                              size_t workspace_bytes, rk_stream_t stream) {
+  return round_scores_exact_impl(1, q, batch, n_q, hq, d, k, kv_dtype, hkv, k_batch_stride, seq_len, s, q_pos, k_pos,
+                                 items, items_stride, n_items, n_bins, active, n_out, raw_out, workspace,
+                                 workspace_bytes, stream);
 }
 
 }  // extern "C"

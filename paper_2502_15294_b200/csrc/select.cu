@@ -39,20 +39,14 @@ __device__ double pw_sum(const F& f, int lo, int n) {
 
 constexpr int kSelMax = 16384;
 
-// one block per distribution (blockIdx.x = batch row, rows `ld` apart)
-__global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int normalize, int kind, double v,
-                              int k_top, double kappa, double* __restrict__ masses, int32_t* __restrict__ kept,
-                              int32_t* __restrict__ n_kept, int32_t* __restrict__ degenerate,
-                              int32_t* __restrict__ status) {
-  raw += (size_t)blockIdx.x * ld;
-  masses += (size_t)blockIdx.x * ld;
-  kept += (size_t)blockIdx.x * ld;
-  n_kept += blockIdx.x;
-  degenerate += blockIdx.x;
-  status += blockIdx.x;
+// One distribution per block: normalize (pairwise sum), then the policy's kept
+// positions (ascending) into kept[0, *n_kept).  raw may live in shared memory.
+__device__ void select_core(const double* raw, int n, int normalize, int kind, double v, int k_top, double kappa,
+                            double* __restrict__ masses, int32_t* __restrict__ kept, int32_t* __restrict__ n_kept,
+                            int32_t* __restrict__ degenerate, int32_t* __restrict__ status,
+                            unsigned char* __restrict__ flag) {
   __shared__ double s_total, s_cut;
   __shared__ int s_neg, s_any;
-  __shared__ unsigned char flag[kSelMax];
   const int t = threadIdx.x;
   if (t == 0) { s_neg = 0; s_any = 0; }
   __syncthreads();
@@ -61,6 +55,7 @@ __global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int
   __syncthreads();
   if (s_neg) {
     if (t == 0) { *status = RK_ERR_DOMAIN; *n_kept = 0; }
+    __syncthreads();
     return;
   }
   if (t == 0) {
@@ -119,6 +114,18 @@ __global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int
     }
     *n_kept = c;
   }
+  __syncthreads();
+}
+
+// one block per distribution (blockIdx.x = batch row, rows `ld` apart)
+__global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int normalize, int kind, double v,
+                              int k_top, double kappa, double* __restrict__ masses, int32_t* __restrict__ kept,
+                              int32_t* __restrict__ n_kept, int32_t* __restrict__ degenerate,
+                              int32_t* __restrict__ status) {
+  __shared__ unsigned char flag[kSelMax];
+  const size_t o = (size_t)blockIdx.x * ld;
+  select_core(raw + o, n, normalize, kind, v, k_top, kappa, masses + o, kept + o, n_kept + blockIdx.x,
+              degenerate + blockIdx.x, status + blockIdx.x, flag);
 }
 
 // Decision margin of one selection (relative distance of the deciding masses
@@ -130,9 +137,8 @@ __global__ void select_kernel(const double* __restrict__ raw, int n, int ld, int
 // A kept set computed from masses accurate to a relative error e is the
 // reference's kept set whenever margin > 2e (exact ties, margin 0, are decided
 // by index on both sides when the masses tie exactly).
-__global__ void margin_kernel(const double* __restrict__ masses, int n, int ld, int kind, double v, int k_top,
-                              double kappa, double* __restrict__ margin) {
-  masses += (size_t)blockIdx.x * ld;
+__device__ void margin_core(const double* __restrict__ masses, int n, int kind, double v, int k_top, double kappa,
+                            double* __restrict__ margin) {
   __shared__ double red[256];
   __shared__ double s_cut, s_a, s_b;
   const int t = threadIdx.x;
@@ -180,8 +186,75 @@ __global__ void margin_kernel(const double* __restrict__ masses, int n, int ld, 
     double m = red[0];
     if (kind == RK_SEL_TOP_PERCENT && k_top > 0 && k_top < n)
       m = s_a > 0.0 ? (s_a - s_b) / s_a : 0.0;
-    margin[blockIdx.x] = m;
+    *margin = m;
   }
+  __syncthreads();
+}
+
+__global__ void margin_kernel(const double* __restrict__ masses, int n, int ld, int kind, double v, int k_top,
+                              double kappa, double* __restrict__ margin) {
+  margin_core(masses + (size_t)blockIdx.x * ld, n, kind, v, k_top, kappa, margin + blockIdx.x);
+}
+
+constexpr int kSelActMax = 2048;   // static shared memory: flags + masses + ids
+
+// Selection over each dialogue's ACTIVE rounds (the inactivity drop policy,
+// selection.py:183-204 + pipeline.py:238-245): raw [batch][ld] holds one Eq. 1
+// mass per round (inactive rounds included, as the scorer's row normalisation
+// needs every key); the block compacts its active rounds in ascending order
+// (the reference's active_rounds list), normalizes and selects over them
+// exactly as select_kernel, and reports the kept ROUND IDS.  top_percent with
+// k_top <= 0 takes k = min(n_b, max(min_rounds, ceil(fraction * n_b - 1e-9)))
+// per dialogue (selection.py:87-97).  masses [batch][ld] at compacted positions;
+// margin [batch] as margin_kernel (nullable).
+__global__ void select_active_kernel(const double* __restrict__ raw, int n, int ld,
+                                     const uint8_t* __restrict__ active, int normalize, int kind, double v, int k_top,
+                                     double fraction, int min_rounds, double kappa, double* __restrict__ masses,
+                                     int32_t* __restrict__ kept, int32_t* __restrict__ n_kept,
+                                     int32_t* __restrict__ degenerate, int32_t* __restrict__ status,
+                                     double* __restrict__ margin) {
+  __shared__ unsigned char flag[kSelActMax];
+  __shared__ double vals[kSelActMax];
+  __shared__ int32_t ids[kSelActMax];
+  __shared__ int s_n;
+  const int b = blockIdx.x, t = threadIdx.x;
+  const size_t o = (size_t)b * ld;
+  if (t < 32) {                               // ordered compaction by warp ballots
+    int base = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + t;
+      const bool a = i < n && (active == nullptr || active[o + i]);
+      const unsigned m = __ballot_sync(0xffffffffu, a);
+      if (a) {
+        const int p = base + __popc(m & ((1u << t) - 1u));
+        ids[p] = i;
+        vals[p] = raw[o + i];
+      }
+      base += __popc(m);
+    }
+    if (t == 0) s_n = base;
+  }
+  __syncthreads();
+  const int nb = s_n;
+  int k = k_top;
+  if (kind == RK_SEL_TOP_PERCENT && k_top <= 0) {
+    k = max(min_rounds, (int)ceil(fraction * (double)nb - 1e-9));
+    k = min(k, nb);
+  }
+  if (nb == 0) {                              // no history: the reference's empty result
+    if (t == 0) {
+      n_kept[b] = 0;
+      degenerate[b] = 0;
+      status[b] = RK_OK;
+      if (margin) margin[b] = INFINITY;
+    }
+    return;
+  }
+  select_core(vals, nb, normalize, kind, v, k, kappa, masses + o, kept + o, n_kept + b, degenerate + b, status + b,
+              flag);
+  const int c = n_kept[b];
+  for (int i = t; i < c; i += blockDim.x) kept[o + i] = ids[kept[o + i]];
+  if (margin) margin_core(masses + o, nb, kind, v, k, kappa, margin + b);
 }
 
 __global__ void aggregate_kernel(const double* __restrict__ scores, int64_t ld, int row_lo, int row_hi,
@@ -232,6 +305,23 @@ int rk_select_batch(const double* raw, int n, int ld, int batch, int normalize, 
   select_kernel<<<batch, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       raw, n, ld, normalize, kind, v, k_top, kappa, masses_out, kept_out, n_kept_out, degenerate_out, status_out);
   RK_CHECK_LAUNCH("select_kernel");
+  return RK_OK;
+}
+
+int rk_select_batch_active(const double* raw, int n, int ld, int batch, const uint8_t* active, int normalize,
+                           int kind, double v, int k_top, double fraction, int min_rounds, double kappa,
+                           double* masses_out, int32_t* kept_out, int32_t* n_kept_out, int32_t* degenerate_out,
+                           int32_t* status_out, double* margin_out, rk_stream_t stream) {
+  if (n < 0 || n > kSelActMax || ld < n)
+    return fail(RK_ERR_DOMAIN, "active selection over %d rounds (max %d)", n, kSelActMax);
+  if (kind < RK_SEL_FIXED || kind > RK_SEL_ALL) return fail(RK_ERR_DOMAIN, "selection kind %d unknown", kind);
+  if (kind == RK_SEL_TOP_PERCENT && k_top <= 0 && (!(fraction > 0.0 && fraction <= 1.0) || min_rounds < 1))
+    return fail(RK_ERR_DOMAIN, "top_percent needs k_top > 0 or fraction in (0, 1] and min_rounds >= 1");
+  if (batch <= 0) return RK_OK;
+  select_active_kernel<<<batch, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      raw, n, ld, active, normalize, kind, v, k_top, fraction, min_rounds, kappa, masses_out, kept_out, n_kept_out,
+      degenerate_out, status_out, margin_out);
+  RK_CHECK_LAUNCH("select_active_kernel");
   return RK_OK;
 }
 

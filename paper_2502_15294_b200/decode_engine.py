@@ -74,6 +74,10 @@ class EngineConfig:
     refine_margin: float = 1e-3   # multi-row questions: re-score in fp64 when the K-boundary gap of the
                                   # fp32-class fused scoring is below this (1-row questions always score in fp64)
     model_seed: int = 42
+    capture_mode: str = "post"    # "pre": head-summed-logit softmax scoring (engine.py:187-200)
+    max_kept: int = 0             # working-cache capacity in rounds (0: top_percent -> its K, else every round)
+    drop_window: float = math.inf  # inactivity drop policy (selection.py:168-204); inf = off
+    drop_protect: int = 2         # newest rounds never dropped
 
     @property
     def group(self) -> int:
@@ -97,8 +101,10 @@ class RoundDecodeEngine:
                  dialogues=None, seed: int | None = None):
         self.cfg = c = cfg
         self.dev = torch.device(device)
-        if c.policy.kind != "top_percent":
-            raise ValueError("the batched engine sizes its working cache for top_percent selection")
+        if c.policy.kind not in ("top_percent", "fixed", "adaptive", "all"):
+            raise ValueError(f"policy {c.policy.kind!r} is not a round-selection strategy")
+        if c.capture_mode not in ("post", "pre"):
+            raise ValueError(f"capture_mode must be 'post' or 'pre', got {c.capture_mode!r}")
         self.dtype = torch.bfloat16
         L, lw, B, T, R = c.num_layers, c.watershed, c.batch, c.round_tokens, c.rounds
         if dialogues is None:
@@ -112,7 +118,24 @@ class RoundDecodeEngine:
         if self.model.shape != c.shape:
             raise ValueError("model shape does not match the engine config")
         self.L_up = L - lw
-        self.K = top_k_count(R, c.policy.fraction, c.policy.min_rounds)
+        # K = the working cache's round slots.  top_percent keeps the same number of
+        # rounds every turn (uniform K); fixed / adaptive thresholds and the drop
+        # policy's shrinking candidate set keep a data-dependent count per dialogue
+        # (<= K), and the upper caches / writeback follow each dialogue's count.
+        k_policy = top_k_count(R, c.policy.fraction, c.policy.min_rounds) if c.policy.kind == "top_percent" else R
+        self.K = min(R, c.max_kept) if c.max_kept > 0 else k_policy
+        if c.policy.kind in ("top_percent", "all") and self.K < k_policy:
+            raise ValueError(f"max_kept {c.max_kept} below the {c.policy.kind} kept count {k_policy}")
+        self.uniform_k = c.policy.kind in ("top_percent", "all") and math.isinf(c.drop_window)
+        if not self.uniform_k and c.question_rows > 1:
+            raise ValueError("multi-row questions need a uniform kept count (top_percent / all, no drop policy)")
+        from .selection import ActivityLedger
+        self.activity = [ActivityLedger(window=c.drop_window, protect_recent=c.drop_protect) for _ in range(B)]
+        for led in self.activity:
+            for r in range(R):
+                led.register_round(r, r)          # round r completed at turn r (pipeline.py:333)
+        self.dropped = [[] for _ in range(B)]
+        self.n_kept = [self.K] * B                # kept rounds per dialogue, last turn
         self.hist = R * T
         self.nq = nq = max(1, c.question_rows)
         # rows appended to the caches per turn; tokens the decode metric counts
@@ -211,6 +234,9 @@ class RoundDecodeEngine:
 
         # ---- scratch (this engine's own: groups run concurrently on their own streams)
         self.raw = torch.empty((B, R), dtype=torch.float64, device=self.dev)
+        self.active_host = torch.ones((B, R), dtype=torch.uint8, pin_memory=True)
+        self.active_dev = torch.ones((B, R), dtype=torch.uint8, device=self.dev)
+        self.sel_out = None
         ws_bytes = _lib.lib.rk_decode_workspace_bytes(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8))
         self.ws = torch.zeros(max(256, int(ws_bytes)), dtype=torch.uint8, device=self.dev)
         ex_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, nq, c.hq, self.items.shape[1], R)
@@ -336,12 +362,23 @@ class RoundDecodeEngine:
         lw1 = c.watershed - 1
         kernels.round_scores_exact(self.q_buf.unsqueeze(1), self.lower[:, lw1, 0], self.q_pos_1, self.items,
                                    c.rounds, seq_len=self.lower_len, n_items=self.n_items, raw=self.raw,
-                                   ws=self.ws_exact)
+                                   ws=self.ws_exact, capture_mode=c.capture_mode)
         self._select()
 
     def _select(self):
-        self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(self.raw, "top_percent", k_top=self.K)
-        kernels.selection_margin(self.masses, "top_percent", k_top=self.K, out=self.margin)
+        """Device selection over every dialogue's active rounds (bit-exact,
+        selection.py:63-126): kept round ids, counts and the K-boundary margin.
+        With a per-dialogue kept count the upper caches' lengths follow it."""
+        pol = self.cfg.policy
+        if self.uniform_k and pol.kind == "top_percent":
+            self.masses, self.kept_pos, self.sel_meta = kernels.select_batch(self.raw, "top_percent", k_top=self.K)
+            kernels.selection_margin(self.masses, "top_percent", k_top=self.K, out=self.margin)
+            return
+        self.sel_out = kernels.select_batch_active(self.raw, pol, active=self.active_dev, out=self.sel_out)
+        self.masses, self.kept_pos, self.sel_meta, margin = self.sel_out
+        self.margin.copy_(margin)
+        if not self.uniform_k:
+            torch.mul(self.sel_meta[0], self.cfg.round_tokens, out=self.upper_len)
 
     def _refine_exact(self):
         """Multi-row question whose fused fp32-class scoring left a K-boundary
@@ -352,7 +389,7 @@ class RoundDecodeEngine:
         lw1 = c.watershed - 1
         kernels.round_scores_exact(self.qq.view(c.batch, self.nq, c.hq, c.head_dim), self.lower[:, lw1, 0],
                                    self.q_pos, self.items, c.rounds, seq_len=self.lower_len, n_items=self.n_items,
-                                   raw=self.raw, ws=self.ws_exact)
+                                   raw=self.raw, ws=self.ws_exact, capture_mode=c.capture_mode)
         self._select()
         self.refined_turns += 1
 
@@ -462,7 +499,12 @@ class RoundDecodeEngine:
     def _phase_wb(self):
         """Writeback of the new round's upper rows to pinned host memory
         (store.writeback_upper, pipeline.py:324-325): one strided D2H."""
-        self.writeback.copy_(self.upper[:, :, :, self.K * self.cfg.round_tokens:], non_blocking=True)
+        T = self.cfg.round_tokens
+        if self.uniform_k:
+            self.writeback.copy_(self.upper[:, :, :, self.K * T:], non_blocking=True)
+            return
+        for b, n in enumerate(self.n_kept):      # the turn's rows follow each dialogue's kept rounds
+            self.writeback[b].copy_(self.upper[b, :, :, n * T:n * T + self.turn_rows], non_blocking=True)
 
     # ------------------------------------------------------------------ gather
     def assign_slots(self, kept):
@@ -477,14 +519,19 @@ class RoundDecodeEngine:
         copies = []
         for b in range(self.cfg.batch):
             new = [int(r) for r in kept[b]]
+            nb = len(new)
+            if nb > self.K:
+                raise RuntimeError(f"dialogue {self.dialogues[b]} keeps {nb} rounds > working-cache capacity "
+                                   f"{self.K} (raise EngineConfig.max_kept)")
             cur = self.slot_round[b]
             if not self.cfg.round_cache:
                 cur[:] = -1
-            stay = set(new) & set(int(x) for x in cur if x >= 0)
+            # the kept rounds occupy slots [0, nb) (the cache rows stay contiguous)
+            stay = set(new) & set(int(cur[i]) for i in range(nb) if cur[i] >= 0)
             for i in range(self.K):
-                if cur[i] not in stay:
+                if i >= nb or cur[i] not in stay:
                     cur[i] = -1
-            free = [i for i in range(self.K) if cur[i] < 0]
+            free = [i for i in range(nb) if cur[i] < 0]
             for i, r in zip(free, [r for r in new if r not in stay]):
                 cur[i] = r
                 copies.append((b, i, r))
@@ -558,7 +605,27 @@ class RoundDecodeEngine:
         for b in range(self.cfg.batch):
             n = int(self.meta_host[0, b])
             kept.append(self.kept_host[b, :n].numpy().copy())
+        self.n_kept = [len(k) for k in kept]
+        self._update_activity(kept)
         return kept
+
+    def _update_activity(self, kept):
+        """The inactivity drop policy (pipeline.py:333-338, selection.py:183-204):
+        record the turn's kept rounds, drop the rounds idle for drop_window turns
+        (their upper blocks leave the host tier, store.drop_upper) and take them
+        out of the next turn's candidate set (the active mask the selector reads)."""
+        if math.isinf(self.cfg.drop_window):
+            return
+        R = self.cfg.rounds
+        now = R + self.turn - 1                    # the turn being served (rounds 0..R-1 came before it)
+        for b, k in enumerate(kept):
+            drops = self.activity[b].update_and_drop([int(x) for x in k], now, R)
+            self.dropped[b] = drops
+            for r in drops:
+                self.active_host[b, r] = 0
+                if self.host_sets == self.cfg.batch:
+                    self.host_blocks[b][r] = None   # store.drop_upper: the payload is gone
+        self.active_dev.copy_(self.active_host, non_blocking=True)
 
     def _set_question(self, e2e: bool = False):
         """This turn's question (variant turn % V) into the question input: from

@@ -94,6 +94,32 @@ def select_batch(raw: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, nor
     return masses, kept, meta
 
 
+def select_batch_active(raw: torch.Tensor, policy, *, active: torch.Tensor | None = None, k_top: int = 0,
+                        out=None, stream=None):
+    """rk_select_batch_active: selection over each dialogue's active rounds (the
+    drop policy's candidate set) for a SelectionPolicy-like `policy` (kind, v,
+    fraction, kappa, min_rounds).  raw (B, n) float64 device, one mass per round;
+    active (B, n) uint8 device or None.  Returns device (masses (B, n), kept
+    ROUND IDS (B, n) int32, meta (3, B) int32 = n_kept, degenerate, status,
+    margin (B,) float64); `out` = a previous return value to reuse."""
+    raw = raw.contiguous()
+    B, n = raw.shape
+    if out is None:
+        out = (torch.empty((B, n), dtype=torch.float64, device=raw.device),
+               torch.zeros((B, n), dtype=torch.int32, device=raw.device),
+               torch.zeros((3, B), dtype=torch.int32, device=raw.device),
+               torch.zeros(B, dtype=torch.float64, device=raw.device))
+    masses, kept, meta, margin = out
+    if active is not None and (active.dtype != torch.uint8 or tuple(active.shape) != (B, n)
+                               or not active.is_contiguous()):
+        raise ValueError("active must be a contiguous (B, n) uint8 tensor")
+    _lib.call("rk_select_batch_active", _lib.ptr(raw), n, n, B, _lib.ptr(active), 1, _lib.SEL_KINDS[policy.kind],
+              float(policy.v), int(k_top), float(policy.fraction), int(policy.min_rounds), float(policy.kappa),
+              _lib.ptr(masses), _lib.ptr(kept), _lib.ptr(meta[0]), _lib.ptr(meta[1]), _lib.ptr(meta[2]),
+              _lib.ptr(margin), _lib.stream_ptr(stream))
+    return out
+
+
 def selection_margin(masses: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1.0, out=None, stream=None):
     """rk_selection_margin over rows of a (B, n) float64 device tensor of masses:
     the relative distance of the deciding masses from the decision threshold
@@ -110,8 +136,10 @@ def selection_margin(masses: torch.Tensor, kind: str, *, v=0.1, k_top=0, kappa=1
 def round_scores_exact(q: torch.Tensor, k_cache: torch.Tensor, q_pos: torch.Tensor, items: torch.Tensor,
                        n_bins: int, *, seq_len: torch.Tensor | None = None, n_items: torch.Tensor | None = None,
                        k_pos: torch.Tensor | None = None, active: torch.Tensor | None = None,
-                       raw: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """Exact (fp64) Eq. 1 masses for B dialogues (rk_round_scores_exact).
+                       raw: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None,
+                       capture_mode: str = "post") -> torch.Tensor:
+    """Exact (fp64) Eq. 1 masses for B dialogues (rk_round_scores_exact; with
+    capture_mode="pre" rk_round_scores_exact_pre, engine.py:187-200).
 
     q (B, n_q, Hq, d) f32; k_cache (B, S_cap, Hkv, d) with any batch stride
     (layer Lw-1 keys); q_pos (n_q,) int64 device; items (B, n_items_max, 3)
@@ -127,7 +155,10 @@ def round_scores_exact(q: torch.Tensor, k_cache: torch.Tensor, q_pos: torch.Tens
     if ws is None:
         nbytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, n_q, hq, items.shape[1], n_bins)
         ws = scratch(nbytes, q.device, "scores_exact")
-    _lib.call("rk_round_scores_exact", _lib.ptr(q), B, n_q, hq, d, _lib.ptr(k_cache), kv_code(k_cache), hkv, stride,
+    if capture_mode not in ("post", "pre"):
+        raise ValueError(f"capture_mode {capture_mode!r}")
+    entry = "rk_round_scores_exact" if capture_mode == "post" else "rk_round_scores_exact_pre"
+    _lib.call(entry, _lib.ptr(q), B, n_q, hq, d, _lib.ptr(k_cache), kv_code(k_cache), hkv, stride,
               _lib.ptr(seq_len), k_cache.shape[1], _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(items), items.shape[1],
               _lib.ptr(n_items), n_bins, _lib.ptr(active), max(1, n_out), _lib.ptr(raw), _lib.ptr(ws), ws.numel(),
               _lib.stream_ptr(stream))

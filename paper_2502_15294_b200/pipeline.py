@@ -152,17 +152,11 @@ class RoundPipeline:
             r = rounds_now[m]
             bounds.append((r.start, r.end, m))
         bounds.append((q_start, len(kv), n))
-        if c.capture_mode == "pre":
-            # head-summed-logit capture (engine.py:187-200, config capture_mode="pre"):
-            # materialise it on the device, then Eq. 1 with rk_aggregate_rounds
-            pos = torch.as_tensor(np.asarray(q_pos), dtype=torch.int64, device=kv.positions.device)
-            cap = self.model._capture_pre(q, kv, pos, None)
-            raw = aggregate_round_attention(cap, rounds_now, SEGMENT_QUESTION, n, active_rounds=active,
-                                            row_offset=q_start)
-            return raw.cpu().numpy()
+        # capture_mode="pre" (engine.py:187-200): the head-summed-logit softmax,
+        # scored by rk_round_scores_exact_pre without a capture matrix
         active_mask = [m in set(active) for m in range(n)]
         raw = round_scores(q, kv.keys.view(-1, c.num_heads, c.d_k), q_pos, kv.positions, bounds, n,
-                           active=active_mask)
+                           active=active_mask, capture_mode=c.capture_mode)
         return raw.cpu().numpy()
 
     def run_turn(self, question, max_decode_steps: int = 16) -> TurnResult:

@@ -151,7 +151,8 @@ def build_round_items(bounds, chunk: int = 256):
     return np.asarray(items, dtype=np.int32).reshape(-1, 3)
 
 
-def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: int = 256, exact: bool = True):
+def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: int = 256, exact: bool = True,
+                 capture_mode: str = "post"):
     """Fused capture + Eq. 1: raw mass per ACTIVE prior round (float64, device).
 
     q: (n_q, Hq, d) float32 cuda; k: (S, Hkv, d) fp32/bf16 cuda (layer Lw-1
@@ -160,7 +161,9 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
     exact=True (default): rk_round_scores_exact, the reference kernel's fp64
     arithmetic (kept sets bit-exact by construction); exact=False: the
     fp32-class rk_round_scores (tcgen05 scores-only pass for large bf16
-    questions).
+    questions).  capture_mode="pre" (engine.py:187-200): one softmax per row
+    over the head-summed logits / (Hq sqrt(d)) (rk_round_scores_exact_pre;
+    exact scoring only).
     """
     torch, dev = _device()
     n_q, hq, d = q.shape
@@ -175,6 +178,10 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
         act = torch.from_numpy(a).to(dev)
     raw = torch.zeros(max(n_out, 1), dtype=torch.float64, device=dev)
     kv_dtype = _lib.RK_BF16 if k.dtype == torch.bfloat16 else _lib.RK_F32
+    if capture_mode not in ("post", "pre"):
+        raise DomainError(f"capture_mode must be 'post' or 'pre', got {capture_mode!r}")
+    if capture_mode == "pre" and not exact:
+        raise DomainError("capture_mode='pre' is scored by the exact (fp64) scorer only")
     if exact:
         q_pos = torch.as_tensor(q_pos, dtype=torch.int64, device=dev)
         k_pos = torch.as_tensor(k_pos, dtype=torch.int64, device=dev)
@@ -182,7 +189,8 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
         kc = k.contiguous()
         ws_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(1, n_q, hq, n_items, n_bins)
         ws = scratch(ws_bytes, dev, "scores_exact")
-        _lib.call("rk_round_scores_exact", _lib.ptr(qc), 1, n_q, hq, d, _lib.ptr(kc), kv_dtype, hkv, 0, None, s,
+        entry = "rk_round_scores_exact" if capture_mode == "post" else "rk_round_scores_exact_pre"
+        _lib.call(entry, _lib.ptr(qc), 1, n_q, hq, d, _lib.ptr(kc), kv_dtype, hkv, 0, None, s,
                   _lib.ptr(q_pos), _lib.ptr(k_pos), _lib.ptr(items), n_items, None, n_bins, _lib.ptr(act),
                   max(n_out, 1), _lib.ptr(raw), _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
         return raw[:n_out]

@@ -1,0 +1,118 @@
+"""The batched serving engine beyond top_percent (VERDICT r1 missing #5/#6):
+fixed / adaptive / all selection (a data-dependent kept count per dialogue:
+the upper caches, the gather slots and the writeback follow each dialogue's
+count), the inactivity drop policy (selection.py:168-204 + pipeline.py:238-245,
+333-338: dropped rounds leave the candidate set the device selector reads) and
+capture_mode="pre" scoring (engine.py:187-200 on rk_round_scores_exact_pre) —
+every turn against the oracle's float64 turn (kept rounds exact, answer ids)."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import decode_model as odm
+from oracle import rounds as orr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2502_15294_b200.decode_engine import EngineConfig, RoundDecodeEngine  # noqa: E402
+from paper_2502_15294_b200.decode_model import DecodeModel  # noqa: E402
+from paper_2502_15294_b200.selection import SelectionPolicy  # noqa: E402
+
+
+def _f(t):
+    return t.float().cpu().numpy()
+
+
+CASES = {
+    "fixed": dict(policy=SelectionPolicy("fixed", v=0.15)),
+    "adaptive": dict(policy=SelectionPolicy("adaptive", kappa=0.5)),
+    "all": dict(policy=SelectionPolicy("all")),
+    "top_percent_drop": dict(policy=SelectionPolicy("top_percent", fraction=0.3), drop_window=1, drop_protect=1),
+    "adaptive_drop": dict(policy=SelectionPolicy("adaptive", kappa=0.25), drop_window=2, drop_protect=2),
+    "pre": dict(policy=SelectionPolicy("top_percent", fraction=0.3), capture_mode="pre"),
+    "pre_fixed": dict(policy=SelectionPolicy("fixed", v=0.12), capture_mode="pre"),
+}
+
+
+def _oracle_policy(p: SelectionPolicy):
+    return orr.SelectionPolicy(p.kind, v=p.v, fraction=p.fraction, kappa=p.kappa, min_rounds=p.min_rounds)
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_engine_policies_match_oracle(name, graphs):
+    kw = CASES[name]
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=8, hkv=2, head_dim=128, rounds=7, round_tokens=64, batch=3,
+                       decode_steps=4, item_chunk=32, plant=2, plant_beta=0.3, question_variants=2, **kw)
+    model = DecodeModel(cfg.shape, "cuda", seed=5, prefill_gemm=True)
+    eng = RoundDecodeEngine(cfg, model=model, dialogues=[2, 7, 11])
+    lower0 = _f(eng.lower[:, :, :, : eng.hist])
+    w = model.host_weights()
+    orc = odm.TurnOracle(w, cfg.hq, cfg.hkv, cfg.head_dim, model.freq.cpu().numpy())
+    pol = _oracle_policy(cfg.policy)
+    R, T, lw = cfg.rounds, cfg.round_tokens, cfg.watershed
+    ledgers = [orr.ActivityLedger(window=cfg.drop_window, protect_recent=cfg.drop_protect) for _ in range(cfg.batch)]
+    for led in ledgers:
+        for r in range(R):
+            led.register_round(r, r)
+    turns = 3
+    if graphs:
+        eng.prepare()                      # turn 0 runs eagerly (warm-up), the rest replay the graphs
+    saw_drop = False
+    for t in range(turns):
+        if graphs and t > 0:
+            kept, _ = eng.run_turn()
+        elif not graphs or t > 0:
+            with torch.cuda.stream(eng.compute_stream):
+                kept = eng.run_turn_eager()
+        else:
+            kept = eng.last_kept
+        torch.cuda.synchronize()
+        answers = eng.answers()
+        for b in range(cfg.batch):
+            active = ledgers[b].active_rounds(R)
+            slots = [int(r) for r in eng.slot_round[b][: len(kept[b])]]
+
+            def blocks(kk, b=b, slots=slots):
+                assert sorted(slots) == list(kk), (slots, kk)
+                hs = b % eng.host_sets
+                return [(np.concatenate([_f(eng.host_blocks[hs][r][u][0]) for r in slots]),
+                         np.concatenate([_f(eng.host_blocks[hs][r][u][1]) for r in slots])) for u in range(eng.L_up)]
+
+            ref = odm.run_turn(orc, [lower0[b, l, 0] for l in range(lw)], [lower0[b, l, 1] for l in range(lw)],
+                               blocks, int(eng.q_tok_all[t % 2, b, 0]), eng.hist, T, R, lw, pol, cfg.decode_steps,
+                               capture_mode=cfg.capture_mode, active=active)
+            assert tuple(int(x) for x in kept[b]) == ref["kept"], (name, t, b, active)
+            assert list(answers[b]) == ref["answer"][:cfg.decode_steps], (name, t, b, ref["logit_gaps"])
+            drops = ledgers[b].update_and_drop(ref["kept"], R + t, R)
+            assert sorted(eng.dropped[b]) == sorted(drops), (name, t, b)
+            saw_drop |= bool(drops)
+            # the writeback holds this dialogue's turn rows, placed after its own kept rounds
+            n = len(kept[b])
+            np.testing.assert_array_equal(_f(eng.writeback[b]),
+                                          _f(eng.upper[b, :, :, n * T:n * T + eng.turn_rows]))
+    if not math.isinf(cfg.drop_window):
+        assert saw_drop, "the drop policy never fired"
+
+
+def test_engine_rejects_overflowing_kept_count():
+    """A data-dependent kept count above the working-cache capacity fails loudly."""
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=8, hkv=2, head_dim=128, rounds=7, round_tokens=64, batch=1,
+                       decode_steps=2, item_chunk=32, plant=0, question_variants=1,
+                       policy=SelectionPolicy("all"), max_kept=3)
+    with pytest.raises(ValueError, match="max_kept"):
+        RoundDecodeEngine(cfg, dialogues=[0])
+    cfg2 = EngineConfig(num_layers=4, watershed=2, hq=8, hkv=2, head_dim=128, rounds=7, round_tokens=64, batch=1,
+                        decode_steps=2, item_chunk=32, plant=0, question_variants=1,
+                        policy=SelectionPolicy("fixed", v=0.01), max_kept=3)
+    eng = RoundDecodeEngine(cfg2, dialogues=[0])
+    with pytest.raises(RuntimeError, match="capacity"):
+        with torch.cuda.stream(eng.compute_stream):
+            eng.run_turn_eager()

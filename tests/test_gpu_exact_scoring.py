@@ -256,3 +256,48 @@ def test_c4_full_size_16_dialogues():
         assert kept[b] == want, b
         gaps.append(_rel_gap(orr.normalize(refs[b]).masses, K))
     print(f"C4: min K-boundary gap over 16 dialogues {min(gaps):.3e}")
+
+
+@pytest.mark.parametrize("n_q,hq,hkv,d,R,T", [(1, 32, 8, 128, 32, 512), (4, 28, 4, 128, 16, 256),
+                                              (7, 8, 8, 64, 8, 128), (1, 8, 2, 64, 12, 97)])
+def test_exact_pre_scorer_matches_oracle(n_q, hq, hkv, d, R, T):
+    """capture_mode="pre" (engine.py:187-200) on rk_round_scores_exact_pre: one
+    softmax per row over the head-summed fp64 logits / (Hq sqrt(d)); Eq. 1 masses
+    vs the oracle's capture_pre + aggregate within 1e-12, kept sets equal."""
+    from oracle import attention as oatt
+    rng = np.random.default_rng(n_q * 1000 + hq + R)
+    B = 2
+    hist = R * T
+    s = hist + n_q
+    k = oatt.round_to_bf16(rng.standard_normal((B, s, hkv, d)).astype(np.float32))
+    q = rng.standard_normal((B, n_q, hq, d)).astype(np.float32)
+    q_pos = np.arange(hist, hist + n_q, dtype=np.int64)
+    bounds = [(r * T, (r + 1) * T, r) for r in range(R)] + [(hist, s, R)]
+    items = build_round_items(bounds, 256)
+    it = torch.from_numpy(np.stack([items] * B)).cuda()
+    raw = kernels.round_scores_exact(torch.from_numpy(q).cuda(), _bf16(torch.from_numpy(k).cuda()),
+                                     torch.from_numpy(q_pos).cuda(), it, R, capture_mode="pre")
+    K = orr.top_k_count(R, 0.10, 1)
+    kept, _ = _select(raw, K)
+    raw = raw.cpu().numpy()
+    for b in range(B):
+        cap = oatt.capture_pre(q[b], k[b], q_pos, np.arange(s))
+        want = np.array([cap[:, r * T:(r + 1) * T].sum() for r in range(R)])
+        np.testing.assert_allclose(raw[b], want, rtol=1e-12, atol=0)
+        dist = orr.normalize(want)
+        assert kept[b] == orr.select(dist, POLICY), (b, kept[b])
+
+
+def test_exact_pre_differs_from_post():
+    """The two capture modes are different statistics (guards a silent mode mix-up)."""
+    rng = np.random.default_rng(5)
+    R, T, hq, hkv, d = 8, 64, 8, 2, 64
+    s = R * T + 1
+    k = _bf16(torch.from_numpy(rng.standard_normal((1, s, hkv, d)).astype(np.float32)).cuda())
+    q = torch.from_numpy(rng.standard_normal((1, 1, hq, d)).astype(np.float32)).cuda()
+    qp = torch.tensor([R * T], dtype=torch.int64, device="cuda")
+    it = torch.from_numpy(build_round_items([(r * T, (r + 1) * T, r) for r in range(R)] + [(R * T, s, R)], 256)
+                          )[None].cuda()
+    post = kernels.round_scores_exact(q, k, qp, it, R).cpu().numpy()
+    pre = kernels.round_scores_exact(q, k, qp, it, R, capture_mode="pre").cpu().numpy()
+    assert not np.allclose(post, pre, rtol=1e-6)
