@@ -75,6 +75,8 @@ def parse():
                     help="skip the reference transfer pattern pass (every kept round fetched every turn)")
     ap.add_argument("--no-round-cache", action="store_true",
                     help="fetch every kept round every turn (the reference's transfer pattern)")
+    ap.add_argument("--kv-dtype", default="bf16", choices=["bf16", "f32"],
+                    help="KV caches / host blocks: bf16 (BASELINE configs[1]) or f32 (the reference's precision)")
     ap.add_argument("--groups", type=int, default=None,
                     help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
@@ -228,6 +230,7 @@ def main():
         w["round_cache"] = False
     if args.host_unique is not None:
         w["host_unique"] = args.host_unique
+    w["kv_dtype"] = args.kv_dtype
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
@@ -271,7 +274,7 @@ def main():
         # the public turn API's own transfers: question ids in; answer ids, kept ids + selection
         # metadata and the new round's upper KV (writeback) out; plus the kept rounds' KV gathers
         step_in = sum(e.q_tok.numel() * 4 for e in eng.groups)
-        step_out = sum(e.answer_host.numel() * 4 + e.writeback.numel() * 2 + e.kept_host.numel() * 4
+        step_out = sum(e.answer_host.numel() * 4 + e.writeback.numel() * e.es + e.kept_host.numel() * 4
                        + e.meta_host.numel() * 4 + e.margin_host.numel() * 8 for e in eng.groups)
         e2e = {"value": world * tokens_per_turn * args.steps / (ms_e / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d_e + step_in), "d2h_bytes_per_step": int(step_out),
@@ -299,7 +302,7 @@ def main():
     resident, full = eng.gpu_kv_bytes()
     traffic = None      # DRAM bytes per token-step from the committed ncu capture (same shapes)
     tp = REPO / "profiles" / "r02_traffic_c2_tokenstep.json"
-    if tp.exists() and args.workload == "c2":
+    if tp.exists() and args.workload == "c2" and args.kv_dtype == "bf16":
         t = json.loads(tp.read_text())
         if t.get("batch_per_group") == g0.cfg.batch:
             traffic = t["per_token_step_bytes_per_group"] * len(eng.groups)
@@ -319,7 +322,8 @@ def main():
     line = {
         "metric": "decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16 weights + KV, fp32 activations / accumulate",
+        "vs_baseline": None,
+        "dtype": f"bf16 weights, {args.kv_dtype} KV, fp32 activations / accumulate",
         "data": "synthetic (random-init weights of the config's shape, random KV history, random question ids)",
         "config": {"workload": f"{args.workload}: L={cfg.num_layers} Lw={cfg.watershed} Hq={cfg.hq} "
                                f"Hkv={cfg.hkv} d={cfg.head_dim} rounds={cfg.rounds}x{cfg.round_tokens} "
@@ -327,7 +331,7 @@ def main():
                                f"decode tokens/turn={eng.turn_tokens} (fixed; EOT ignored) "
                                f"host_round_sets/group={g0.host_sets} (unique per dialogue: "
                                f"{g0.host_sets == g0.cfg.batch}) round_cache={cfg.round_cache} "
-                               f"question_variants={cfg.question_variants}",
+                               f"question_variants={cfg.question_variants} kv_dtype={args.kv_dtype}",
                    "model": "reference toy transformer (attention + residual, RoPE, tied logits) at "
                             f"{'Llama-3-8B' if cfg.hq == 32 else 'Qwen2-7B'} shapes, GQA, bf16 weights",
                    "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
@@ -363,7 +367,7 @@ def main():
         "kept_by_dialogue": ({str(k): kept_by_dialogue[k] for k in sorted(kept_by_dialogue)}
                              if len(kept_by_dialogue) <= 64 else None),
         "host": {"numa_node": numa, "pinned_round_bytes": sum(e.host_sets * e.cfg.rounds for e in eng.groups)
-                 * g0.host_blocks[0][0].numel() * 2},
+                 * g0.host_blocks[0][0].numel() * g0.es},
     }
     if fetch_all:
         line["fetch_all"] = fetch_all

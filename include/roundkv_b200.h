@@ -315,6 +315,13 @@ size_t rk_proj_workspace_bytes(int m, int k, int n);
 int rk_qkv_rope(const float* x, int m, int d_model, const void* w_qkv_packed, int hq, int hkv, int d,
                 const int32_t* pos, const double* rope_freq, float* q_out, void* k_out, void* v_out,
                 int64_t kv_row_stride, void* workspace, size_t workspace_bytes, rk_stream_t stream);
+
+/* rk_qkv_rope with the cache's dtype: kv_dtype RK_BF16 (rk_qkv_rope) or RK_F32
+ * (the reference's float32 KV, _attn_np.py:26-28); kv_row_stride in elements. */
+int rk_qkv_rope_kv(const float* x, int m, int d_model, const void* w_qkv_packed, int hq, int hkv, int d,
+                   const int32_t* pos, const double* rope_freq, float* q_out, void* k_out, void* v_out,
+                   int kv_dtype, int64_t kv_row_stride, void* workspace, size_t workspace_bytes,
+                   rk_stream_t stream);
 int rk_out_proj(const float* a, int m, int k, const void* w_o_packed, int d_model, float* resid,
                 void* workspace, size_t workspace_bytes, rk_stream_t stream);
 size_t rk_lm_head_workspace_bytes(int m, int vocab, int d_model);

@@ -64,11 +64,12 @@ class TurnOracle:
     """State of one dialogue for one turn: lower caches (history), the kept
     rounds' upper blocks are given after selection."""
 
-    def __init__(self, weights, hq, hkv, d, freq):
+    def __init__(self, weights, hq, hkv, d, freq, kv_bf16=True):
         self.w = weights
         self.hq, self.hkv, self.d = hq, hkv, d
         self.freq = freq
         self.L = len(weights["wq"])
+        self.kv_round = round_to_bf16 if kv_bf16 else (lambda a: np.asarray(a, dtype=np.float32))
 
     def layer(self, l, x, pos, K, V, capture=False):
         """x (D,) fp32; K/V caches (S, Hkv, d) of layer l BEFORE the append.
@@ -79,8 +80,8 @@ class TurnOracle:
         k = (x64 @ w["wk"][l]).astype(np.float32).reshape(1, self.hkv, self.d)
         v = (x64 @ w["wv"][l]).astype(np.float32).reshape(1, self.hkv, self.d)
         q = rope(q, [pos], self.freq)[0]
-        k = round_to_bf16(rope(k, [pos], self.freq))
-        v = round_to_bf16(v)
+        k = self.kv_round(rope(k, [pos], self.freq))      # the cache's dtype (bf16 or the reference's fp32)
+        v = self.kv_round(v)
         K = np.concatenate([K, k])
         V = np.concatenate([V, v])
         out, cap = attend(q, K, V, capture)

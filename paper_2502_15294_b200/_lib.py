@@ -59,6 +59,7 @@ _SIGS = {
     "rk_pack_weight": (_i, [_p, _i, _i, _i, _p, _p]),
     "rk_proj_workspace_bytes": (_sz, [_i, _i, _i]),
     "rk_qkv_rope": (_i, [_p, _i, _i, _p, _i, _i, _i, _p, _p, _p, _p, _p, _i64, _p, _sz, _p]),
+    "rk_qkv_rope_kv": (_i, [_p, _i, _i, _p, _i, _i, _i, _p, _p, _p, _p, _p, _i, _i64, _p, _sz, _p]),
     "rk_out_proj": (_i, [_p, _i, _i, _p, _i, _p, _p, _sz, _p]),
     "rk_lm_head_workspace_bytes": (_sz, [_i, _i, _i]),
     "rk_lm_head": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _p, _p, _i, _p, _sz, _p]),

@@ -360,8 +360,8 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
   if (!items) {   // small batches: one cluster per (dialogue, kv-head), merge in DSMEM (decode_cluster.cu)
     const int C = cluster_decode_size(kv_dtype, d, hkv, G, batch, max_seq_len, cache_stride);
     if (C) {
-      st = launch_decode_cluster(C, q, batch, hq, d, k_cache, v_cache, hkv, cache_stride, seq_len, max_seq_len,
-                                 k_new, v_new, out, cs);
+      st = launch_decode_cluster(C, kv_dtype, q, batch, hq, d, k_cache, v_cache, hkv, cache_stride, seq_len,
+                                 max_seq_len, k_new, v_new, out, cs);
       if (st) return st;
       if (advance_len) return advance_after(advance_len, batch, cs);
       return RK_OK;

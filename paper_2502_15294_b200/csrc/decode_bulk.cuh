@@ -32,8 +32,8 @@ int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const Bu
 
 // small-batch cluster decode (decode_cluster.cu): cluster size, 0 = not applicable
 int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride);
-int launch_decode_cluster(int C, const float* q, int batch, int hq, int d, void* k_cache, void* v_cache, int hkv,
-                          int64_t batch_stride, const int32_t* seq_len, int max_len, const void* k_new,
-                          const void* v_new, float* out, cudaStream_t st);
+int launch_decode_cluster(int C, int kv_dtype, const float* q, int batch, int hq, int d, void* k_cache,
+                          void* v_cache, int hkv, int64_t batch_stride, const int32_t* seq_len, int max_len,
+                          const void* k_new, const void* v_new, float* out, cudaStream_t st);
 
 }  // namespace rk

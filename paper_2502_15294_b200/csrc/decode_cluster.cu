@@ -49,20 +49,38 @@ constexpr int kThreads = (kCW + 1) * 32;
 #endif
 constexpr int kStg = RK_CL_STAGES;
 constexpr int kBoxRows = 16;                 // keys per box (one consumer warp's group)
-constexpr int kTK = kBoxRows * kCW;          // keys per stage
-constexpr int kBoxBytes = kBoxRows * 128;    // 16 keys x 64 bf16 dims
+constexpr int kBoxBytes = kBoxRows * 128;    // 16 keys x 128 bytes (64 bf16 / 32 fp32 dims)
 
-template <int D>
+// KV element type: bf16 stages hold 128 keys (8 groups of 16, one per consumer
+// warp); fp32 rows are twice as wide, so a stage holds 64 keys (4 groups) and
+// the consumer warps form two sets that take alternate stages (warp w: group
+// w % 4 of the stages t with t % 2 == w / 4) — same ring bytes, same warps.
+template <typename KT>
+struct KV;
+template <>
+struct KV<__nv_bfloat16> {
+  static constexpr int ES = 2, GROUPS = 8, SETS = 1;
+};
+template <>
+struct KV<float> {
+  static constexpr int ES = 4, GROUPS = 4, SETS = 2;
+};
+
+template <typename KT, int D>
 struct CTile {
-  static constexpr int NH = D / 64;                      // 64-dim halves (boxes per key group)
-  static constexpr int HALF = kTK * 128;                 // one 64-dim half of a stage: [kTK rows][128 B]
+  static constexpr int ES = KV<KT>::ES;
+  static constexpr int TK = kBoxRows * KV<KT>::GROUPS;   // keys per stage
+  static constexpr int BOXE = 128 / ES;                  // elements per 128-byte box row
+  static constexpr int NH = D / BOXE;                    // boxes per key row (128-byte column slabs)
+  static constexpr int HALF = TK * 128;                  // one slab of a stage: [TK rows][128 B]
   static constexpr int OP = NH * HALF;                   // bytes of K (or V) per stage
+  static constexpr int C16 = D * ES / 16;                // 16-byte chunks per key row
   static constexpr size_t smem = 1024 + 2 * (size_t)kStg * OP + 2 * kStg * sizeof(uint64_t);
-  // byte offset of (key row r of group w, dims [8*c8, 8*c8+8)) in one operand
-  // stage; rows of a half are contiguous, so a full stage is one {64, kTK} box
-  // per half and a partial one is {64, 16} boxes per group (same layout)
-  __device__ static __forceinline__ uint32_t off(int w, int r, int c8) {
-    const int hf = c8 >> 3, c = c8 & 7;
+  // byte offset of (key row r of group w, 16-byte chunk c16 of the row) in one
+  // operand stage; rows of a slab are contiguous, so a full stage is one
+  // {BOXE, TK} box per slab and a partial one is {BOXE, 16} boxes per group
+  __device__ static __forceinline__ uint32_t off(int w, int r, int c16) {
+    const int hf = c16 >> 3, c = c16 & 7;
     return (uint32_t)(hf * HALF + (16 * w + r) * 128 + ((c ^ (r & 7)) << 4));
   }
 };
@@ -105,27 +123,37 @@ __device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* map, in
 
 struct ClusterParams {
   const float* q;          // [B][Hq][D]
-  __nv_bfloat16* k;        // cache base (k_map / v_map describe the same memory)
-  __nv_bfloat16* v;
+  void* k;                 // cache base (k_map / v_map describe the same memory), bf16 or fp32
+  void* v;
   int64_t rows_per_b;      // cache rows (keys) per dialogue = batch_stride / (HKV*D)
   const int32_t* seq_len;  // [B]
-  const __nv_bfloat16* k_new;   // [B][HKV][D] or null
-  const __nv_bfloat16* v_new;
+  const void* k_new;       // [B][HKV][D] or null
+  const void* v_new;
   int hq, hkv;
   float scale_log2;
   float* out;              // [B][Hq][D]
 };
 
-// kmap/vmap: {64, kTK}-key boxes (whole stages); kmap16/vmap16: {64, 16} (the
+// fp32 K / V rows r, r+1 at 16-byte chunk c16 (+ byte offset) of one stage -> bf16 hi / lo pairs
+__device__ __forceinline__ float2 lds_f2(const uint8_t* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const float ha = bf16_round(a), hb = bf16_round(b);
+  hi = pack_bf16(ha, hb);
+  lo = pack_bf16(a - ha, b - hb);
+}
+
+// kmap/vmap: {BOXE, TK}-key boxes (whole stages); kmap16/vmap16: {BOXE, 16} (the
 // last, partial stage of a slice, so a slice reads at most 15 keys past its end)
-template <int D, int G>
+template <typename KT, int D, int G>
 __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __grid_constant__ CUtensorMap kmap,
                                                                      const __grid_constant__ CUtensorMap vmap,
                                                                      const __grid_constant__ CUtensorMap kmap16,
                                                                      const __grid_constant__ CUtensorMap vmap16,
                                                                      const __grid_constant__ ClusterParams p) {
-  using T = CTile<D>;
-  constexpr int NH = T::NH, OP = T::OP;
+  using T = CTile<KT, D>;
+  constexpr int NH = T::NH, OP = T::OP, TK = T::TK, BOXE = T::BOXE;
+  constexpr int GROUPS = KV<KT>::GROUPS, SETS = KV<KT>::SETS;
+  constexpr bool F32 = sizeof(KT) == 4;
   constexpr int KC = D / 16, NT = D / 8;
   static_assert(G <= 8, "at most 8 query heads per kv-head");
   extern __shared__ uint8_t smem_raw[];
@@ -150,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStg; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCW);
+      mbar_init(&empty[s], GROUPS);
     }
     mbar_init(&in_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -170,15 +198,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
     const bool owns_new = append && hi == len && hi > lo;
     const uint64_t pol = evict_first_policy();
     int t = 0;
-    for (int j0 = lo; j0 < hi; j0 += kTK, ++t) {
-      const int nk = min(kTK, hi - j0);
+    for (int j0 = lo; j0 < hi; j0 += TK, ++t) {
+      const int nk = min(TK, hi - j0);
       if (owns_new && j0 + nk == hi) {
         pdl_wait();
         const int64_t dst = (row0 + len - 1) * p.hkv * D + (int64_t)h * D;
         const int64_t src = ((int64_t)b * p.hkv + h) * D;
-        for (int e = lane; e < D / 8; e += 32) {
-          reinterpret_cast<uint4*>(p.k + dst)[e] = reinterpret_cast<const uint4*>(p.k_new + src)[e];
-          reinterpret_cast<uint4*>(p.v + dst)[e] = reinterpret_cast<const uint4*>(p.v_new + src)[e];
+        for (int e = lane; e < T::C16; e += 32) {
+          reinterpret_cast<uint4*>(static_cast<KT*>(p.k) + dst)[e] =
+              reinterpret_cast<const uint4*>(static_cast<const KT*>(p.k_new) + src)[e];
+          reinterpret_cast<uint4*>(static_cast<KT*>(p.v) + dst)[e] =
+              reinterpret_cast<const uint4*>(static_cast<const KT*>(p.v_new) + src)[e];
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
@@ -191,13 +221,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
         const int r = (int)(row0 + j0);
         for (int hf = 0; hf < NH; ++hf) {
           const uint32_t kd = smem_u32(kst + s * OP) + hf * T::HALF, vd = smem_u32(vst + s * OP) + hf * T::HALF;
-          if (nk == kTK) {
-            tma_box(kd, &kmap, h * D + hf * 64, r, &full[s], pol);
-            tma_box(vd, &vmap, h * D + hf * 64, r, &full[s], pol);
+          if (nk == TK) {
+            tma_box(kd, &kmap, h * D + hf * BOXE, r, &full[s], pol);
+            tma_box(vd, &vmap, h * D + hf * BOXE, r, &full[s], pol);
           } else {
             for (int w = 0; w < ng; ++w) {
-              tma_box(kd + w * kBoxBytes, &kmap16, h * D + hf * 64, r + w * kBoxRows, &full[s], pol);
-              tma_box(vd + w * kBoxBytes, &vmap16, h * D + hf * 64, r + w * kBoxRows, &full[s], pol);
+              tma_box(kd + w * kBoxBytes, &kmap16, h * D + hf * BOXE, r + w * kBoxRows, &full[s], pol);
+              tma_box(vd + w * kBoxBytes, &vmap16, h * D + hf * BOXE, r + w * kBoxRows, &full[s], pol);
             }
           }
         }
@@ -232,33 +262,54 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
     float m = -INFINITY, lsum = 0.f;
-    int t = 0;
-    for (int j0 = lo; j0 < hi; j0 += kTK, ++t) {
+    const int grp = warp % GROUPS, set = warp / GROUPS;
+    for (int j0 = lo + set * TK, t = set; j0 < hi; j0 += SETS * TK, t += SETS) {
       const int s = t % kStg;
-      const int nkw = min(kBoxRows, max(0, min(kTK, hi - j0) - kBoxRows * warp));
+      const int nkw = min(kBoxRows, max(0, min(TK, hi - j0) - kBoxRows * grp));
       mbar_wait(&full[s], (t / kStg) & 1);
       if (nkw > 0) {
         const uint8_t* kb = kst + s * OP;
         uint8_t* vb = vst + s * OP;
         if (nkw < kBoxRows) {   // rows past the slice are other keys (or unwritten rows): zero their V
-          for (int e = lane; e < (kBoxRows - nkw) * (D / 8); e += 32) {
-            const int r = nkw + e / (D / 8), c8 = e % (D / 8);
-            *reinterpret_cast<uint4*>(vb + T::off(warp, r, c8)) = make_uint4(0, 0, 0, 0);
+          for (int e = lane; e < (kBoxRows - nkw) * T::C16; e += 32) {
+            const int r = nkw + e / T::C16, c16 = e % T::C16;
+            *reinterpret_cast<uint4*>(vb + T::off(grp, r, c16)) = make_uint4(0, 0, 0, 0);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
         }
         float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (F32) {
+          // fp32 K rows split into bf16 hi + lo on the fly: S = [q_hi; q_lo] (K_hi + K_lo),
+          // ~16 mantissa bits per operand (the bf16 cache's products keep the same class)
 #pragma unroll
-        for (int kk = 0; kk < KC / 2; ++kk) {
-          uint32_t r[4];
-          const int c8 = 4 * kk + (lane >> 3);
-          ldmatrix_x4(r, kb + T::off(warp, lane & 7, c8));
-          mma_bf16_16816(s0, qa[2 * kk], r[0], r[1]);
-          mma_bf16_16816(s0, qa[2 * kk + 1], r[2], r[3]);
-          ldmatrix_x4(r, kb + T::off(warp, 8 + (lane & 7), c8));
-          mma_bf16_16816(s1, qa[2 * kk], r[0], r[1]);
-          mma_bf16_16816(s1, qa[2 * kk + 1], r[2], r[3]);
+          for (int kc = 0; kc < KC; ++kc) {
+            const int cb = 4 * kc + (c >> 1), ob = (c & 1) * 8;     // dims 16kc + 2c (+8): chunks cb, cb + 2
+            uint32_t bh0, bl0, bh1, bl1;
+            float2 x0 = lds_f2(kb + T::off(grp, g, cb) + ob), x1 = lds_f2(kb + T::off(grp, g, cb + 2) + ob);
+            split_pair(x0.x, x0.y, bh0, bl0);
+            split_pair(x1.x, x1.y, bh1, bl1);
+            mma_bf16_16816(s0, qa[kc], bh0, bh1);
+            mma_bf16_16816(s0, qa[kc], bl0, bl1);
+            x0 = lds_f2(kb + T::off(grp, 8 + g, cb) + ob);
+            x1 = lds_f2(kb + T::off(grp, 8 + g, cb + 2) + ob);
+            split_pair(x0.x, x0.y, bh0, bl0);
+            split_pair(x1.x, x1.y, bh1, bl1);
+            mma_bf16_16816(s1, qa[kc], bh0, bh1);
+            mma_bf16_16816(s1, qa[kc], bl0, bl1);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < KC / 2; ++kk) {
+            uint32_t r[4];
+            const int c8 = 4 * kk + (lane >> 3);
+            ldmatrix_x4(r, kb + T::off(grp, lane & 7, c8));
+            mma_bf16_16816(s0, qa[2 * kk], r[0], r[1]);
+            mma_bf16_16816(s0, qa[2 * kk + 1], r[2], r[3]);
+            ldmatrix_x4(r, kb + T::off(grp, 8 + (lane & 7), c8));
+            mma_bf16_16816(s1, qa[2 * kk], r[0], r[1]);
+            mma_bf16_16816(s1, qa[2 * kk + 1], r[2], r[3]);
+          }
         }
         float sc[4];
         sc[0] = (2 * c < nkw) ? s0[0] + s0[2] : -INFINITY;
@@ -292,12 +343,35 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
           pa[2] = pack_bf16(h2, h3);
           pa[3] = pack_bf16(pr[2] - h2, pr[3] - h3);
         }
+        if constexpr (F32) {
+          // V rows (keys 2c, 2c+1, 2c+8, 2c+9) x dims 16jj + 2g, +1: tile 2jj holds the even
+          // dims, tile 2jj+1 the odd ones, so one 8-byte load feeds both tiles (the
+          // epilogue writes dims 16jj + 4c .. +3 from o[2jj][*], o[2jj+1][*])
 #pragma unroll
-        for (int jj = 0; jj < NT / 2; ++jj) {
-          uint32_t r[4];
-          ldmatrix_x4_trans(r, vb + T::off(warp, (lane & 7) + 8 * ((lane >> 3) & 1), 2 * jj + (lane >> 4)));
-          mma_bf16_16816(o[2 * jj], pa, r[0], r[1]);
-          mma_bf16_16816(o[2 * jj + 1], pa, r[2], r[3]);
+          for (int jj = 0; jj < NT / 2; ++jj) {
+            const int cb = 4 * jj + (g >> 1), ob = (g & 1) * 8;
+            const float2 v0 = lds_f2(vb + T::off(grp, 2 * c, cb) + ob);
+            const float2 v1 = lds_f2(vb + T::off(grp, 2 * c + 1, cb) + ob);
+            const float2 v8 = lds_f2(vb + T::off(grp, 2 * c + 8, cb) + ob);
+            const float2 v9 = lds_f2(vb + T::off(grp, 2 * c + 9, cb) + ob);
+            uint32_t eh0, el0, eh1, el1, oh0, ol0, oh1, ol1;
+            split_pair(v0.x, v1.x, eh0, el0);
+            split_pair(v8.x, v9.x, eh1, el1);
+            split_pair(v0.y, v1.y, oh0, ol0);
+            split_pair(v8.y, v9.y, oh1, ol1);
+            mma_bf16_16816(o[2 * jj], pa, eh0, eh1);
+            mma_bf16_16816(o[2 * jj], pa, el0, el1);
+            mma_bf16_16816(o[2 * jj + 1], pa, oh0, oh1);
+            mma_bf16_16816(o[2 * jj + 1], pa, ol0, ol1);
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < NT / 2; ++jj) {
+            uint32_t r[4];
+            ldmatrix_x4_trans(r, vb + T::off(grp, (lane & 7) + 8 * ((lane >> 3) & 1), 2 * jj + (lane >> 4)));
+            mma_bf16_16816(o[2 * jj], pa, r[0], r[1]);
+            mma_bf16_16816(o[2 * jj + 1], pa, r[2], r[3]);
+          }
         }
       }
       __syncwarp();
@@ -312,10 +386,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
     float* wl = wm + kCW * 8;                              // [kCW][8]
     float* wacc = wl + kCW * 8;                            // [kCW][8][D]
     if (g < G) {
+      if constexpr (F32) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        *reinterpret_cast<float2*>(wacc + (warp * 8 + g) * D + 8 * nt + 2 * c) =
-            make_float2(o[nt][0] + o[nt][2], o[nt][1] + o[nt][3]);
+        for (int jj = 0; jj < NT / 2; ++jj)
+          *reinterpret_cast<float4*>(wacc + (warp * 8 + g) * D + 16 * jj + 4 * c) =
+              make_float4(o[2 * jj][0] + o[2 * jj][2], o[2 * jj + 1][0] + o[2 * jj + 1][2],
+                          o[2 * jj][1] + o[2 * jj][3], o[2 * jj + 1][1] + o[2 * jj + 1][3]);
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          *reinterpret_cast<float2*>(wacc + (warp * 8 + g) * D + 8 * nt + 2 * c) =
+              make_float2(o[nt][0] + o[nt][2], o[nt][1] + o[nt][3]);
+      }
       if (c == 0) {
         wm[warp * 8 + g] = m;
         wl[warp * 8 + g] = lsum;
@@ -404,12 +486,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
 
 int g_max_clusters[17] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};   // by cluster size
 
-template <int D, int G>
+template <typename KT, int D, int G>
 cudaError_t configure(int C) {
-  auto kern = decode_cluster_kernel<D, G>;
+  auto kern = decode_cluster_kernel<KT, D, G>;
   static bool done = false;
   if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTile<D>::smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CTile<KT, D>::smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
@@ -419,14 +502,14 @@ cudaError_t configure(int C) {
   return cudaSuccess;
 }
 
-template <int D, int G>
+template <typename KT, int D, int G>
 cudaError_t launch(int C, int B, int hkv, const CUtensorMap* m, const ClusterParams& p, cudaStream_t st) {
-  cudaError_t e = configure<D, G>(C);
+  cudaError_t e = configure<KT, D, G>(C);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(C, hkv, B);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = CTile<D>::smem;
+  cfg.dynamicSmemBytes = CTile<KT, D>::smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -437,18 +520,18 @@ cudaError_t launch(int C, int B, int hkv, const CUtensorMap* m, const ClusterPar
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, decode_cluster_kernel<D, G>, m[0], m[1], m[2], m[3], p);
+  return cudaLaunchKernelEx(&cfg, decode_cluster_kernel<KT, D, G>, m[0], m[1], m[2], m[3], p);
 }
 
-template <int D>
+template <typename KT, int D>
 cudaError_t launch_by_g(int G, int C, int B, int hkv, const CUtensorMap* m, const ClusterParams& p,
                         cudaStream_t st) {
   switch (G) {
-    case 1: return launch<D, 1>(C, B, hkv, m, p, st);
-    case 2: return launch<D, 2>(C, B, hkv, m, p, st);
-    case 4: return launch<D, 4>(C, B, hkv, m, p, st);
-    case 7: return launch<D, 7>(C, B, hkv, m, p, st);
-    case 8: return launch<D, 8>(C, B, hkv, m, p, st);
+    case 1: return launch<KT, D, 1>(C, B, hkv, m, p, st);
+    case 2: return launch<KT, D, 2>(C, B, hkv, m, p, st);
+    case 4: return launch<KT, D, 4>(C, B, hkv, m, p, st);
+    case 7: return launch<KT, D, 7>(C, B, hkv, m, p, st);
+    case 8: return launch<KT, D, 8>(C, B, hkv, m, p, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -456,11 +539,11 @@ cudaError_t launch_by_g(int G, int C, int B, int hkv, const CUtensorMap* m, cons
 int max_clusters(int C) {
   const int i = C;
   if (g_max_clusters[i] < 0) {
-    if (configure<128, 4>(C) != cudaSuccess) return g_max_clusters[i] = 0;
+    if (configure<__nv_bfloat16, 128, 4>(C) != cudaSuccess) return g_max_clusters[i] = 0;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(C, 1, 1);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = CTile<128>::smem;
+    cfg.dynamicSmemBytes = CTile<__nv_bfloat16, 128>::smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = C;
@@ -469,7 +552,7 @@ int max_clusters(int C) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel<128, 4>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, decode_cluster_kernel<__nv_bfloat16, 128, 4>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       n = 0;
     }
@@ -496,7 +579,8 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
     const char* e = std::getenv("RK_DECODE_CLUSTER");
     mode = e ? std::atoi(e) : 1;
   }
-  if (mode == 0 || kv_dtype != RK_BF16 || (d != 128 && d != 64)) return 0;
+  // fp32 and bf16 stages have the same bytes and warps (CTile), so the same co-residency
+  if (mode == 0 || (kv_dtype != RK_BF16 && kv_dtype != RK_F32) || (d != 128 && d != 64)) return 0;
   if (!(G == 1 || G == 2 || G == 4 || G == 7 || G == 8)) return 0;
   const int64_t row = (int64_t)hkv * d;
   if (batch > 1 && (batch_stride % row != 0 || batch_stride <= 0)) return 0;
@@ -526,9 +610,12 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
   return 0;
 }
 
-int launch_decode_cluster(int C, const float* q, int batch, int hq, int d, void* k_cache, void* v_cache, int hkv,
-                          int64_t batch_stride, const int32_t* seq_len, int max_len, const void* k_new,
-                          const void* v_new, float* out, cudaStream_t st) {
+int launch_decode_cluster(int C, int kv_dtype, const float* q, int batch, int hq, int d, void* k_cache,
+                          void* v_cache, int hkv, int64_t batch_stride, const int32_t* seq_len, int max_len,
+                          const void* k_new, const void* v_new, float* out, cudaStream_t st) {
+  const bool f32 = kv_dtype == RK_F32;
+  const int es = f32 ? 4 : 2;
+  const uint32_t tk = f32 ? (uint32_t)CTile<float, 128>::TK : (uint32_t)CTile<__nv_bfloat16, 128>::TK;
   const int64_t row = (int64_t)hkv * d;
   const int64_t rows_per_b = batch > 1 ? batch_stride / row : (int64_t)max_len;
   // the map ends at the last dialogue's max_len-th row (max_len bounds seq_len+1
@@ -539,23 +626,28 @@ int launch_decode_cluster(int C, const float* q, int batch, int hq, int d, void*
   CUtensorMap m[4];   // K, V whole-stage boxes; K, V 16-key boxes
   int r = 0;
   for (int i = 0; i < 4 && !r; ++i)
-    r = tc::make_map(&m[i], (i & 1) ? v_cache : k_cache, (uint64_t)row, rows, (uint64_t)row * 2,
-                     i < 2 ? kTK : kBoxRows);
+    r = tc::make_map(&m[i], (i & 1) ? v_cache : k_cache, (uint64_t)row, rows, (uint64_t)row * es,
+                     i < 2 ? tk : (uint32_t)kBoxRows, es);
   if (r) return r;
   ClusterParams p{};
   p.q = q;
-  p.k = static_cast<__nv_bfloat16*>(k_cache);
-  p.v = static_cast<__nv_bfloat16*>(v_cache);
+  p.k = k_cache;
+  p.v = v_cache;
   p.rows_per_b = rows_per_b;
   p.seq_len = seq_len;
-  p.k_new = static_cast<const __nv_bfloat16*>(k_new);
-  p.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  p.k_new = k_new;
+  p.v_new = v_new;
   p.hq = hq;
   p.hkv = hkv;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.out = out;
   const int G = hq / hkv;
-  cudaError_t e = d == 128 ? launch_by_g<128>(G, C, batch, hkv, m, p, st) : launch_by_g<64>(G, C, batch, hkv, m, p, st);
+  cudaError_t e;
+  if (f32)
+    e = d == 128 ? launch_by_g<float, 128>(G, C, batch, hkv, m, p, st) : launch_by_g<float, 64>(G, C, batch, hkv, m, p, st);
+  else
+    e = d == 128 ? launch_by_g<__nv_bfloat16, 128>(G, C, batch, hkv, m, p, st)
+                 : launch_by_g<__nv_bfloat16, 64>(G, C, batch, hkv, m, p, st);
   if (e != cudaSuccess) return cuda_status(e, "decode_cluster_kernel launch");
   return RK_OK;
 }

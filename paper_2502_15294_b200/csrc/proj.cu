@@ -112,9 +112,10 @@ struct Params {
   const int32_t* pos;
   const double* freq;
   float* q_out;
-  __nv_bfloat16* k_out;
-  __nv_bfloat16* v_out;
+  void* k_out;                             // bf16 or (kv_f32) fp32 cache rows
+  void* v_out;
   int64_t kv_stride;
+  int kv_f32;
   // out
   float* resid;
   // head
@@ -163,6 +164,20 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 128;" :::
 // (cos, sin) of pos[t] * freq[pair] (angle and sincos in float64 as
 // engine.py:175-185, stored rounded to float32), [t][row / 2], filled while the
 // weights stream (nullptr: computed here); the rotation itself runs in float64.
+// one k / v cache element (or an adjacent pair) in the cache's dtype
+__device__ __forceinline__ void store_kv(const Params& p, void* base, size_t i, float y) {
+  if (p.kv_f32)
+    static_cast<float*>(base)[i] = y;
+  else
+    static_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(y);
+}
+__device__ __forceinline__ void store_kv2(const Params& p, void* base, size_t i, float a, float b) {
+  if (p.kv_f32)
+    *reinterpret_cast<float2*>(static_cast<float*>(base) + i) = make_float2(a, b);
+  else
+    *reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(base) + i) = pack_bf16(a, b);
+}
+
 template <int NP>
 __device__ __forceinline__ void finish(const Params& p, int sg, int row, float (&v)[NP], const float2* rope) {
   const int n = sg * BM + row;
@@ -189,9 +204,9 @@ __device__ __forceinline__ void finish(const Params& p, int sg, int row, float (
         if (n < qd)
           p.q_out[(size_t)t * qd + n] = y;
         else
-          p.k_out[(size_t)t * p.kv_stride + (n - qd)] = __float2bfloat16_rn(y);
+          store_kv(p, p.k_out, (size_t)t * p.kv_stride + (n - qd), y);
       } else {
-        p.v_out[(size_t)t * p.kv_stride + (n - qd - kd)] = __float2bfloat16_rn(v[t]);
+        store_kv(p, p.v_out, (size_t)t * p.kv_stride + (n - qd - kd), v[t]);
       }
     }
   } else if (p.mode == PJ_OUT) {
@@ -232,9 +247,9 @@ __device__ __forceinline__ void finish_pair(const Params& p, int sg, int pr, int
       if (n < qd)
         *reinterpret_cast<float2*>(p.q_out + (size_t)t * qd + n) = make_float2(a, b);
       else
-        *reinterpret_cast<uint32_t*>(p.k_out + (size_t)t * p.kv_stride + (n - qd)) = pack_bf16(a, b);
+        store_kv2(p, p.k_out, (size_t)t * p.kv_stride + (n - qd), a, b);
     } else {
-      *reinterpret_cast<uint32_t*>(p.v_out + (size_t)t * p.kv_stride + (n - qd - kd)) = pack_bf16(y0, y1);
+      store_kv2(p, p.v_out, (size_t)t * p.kv_stride + (n - qd - kd), y0, y1);
     }
   } else if (p.mode == PJ_OUT) {
     float2* r = reinterpret_cast<float2*>(p.resid + (size_t)t * p.N + n);
@@ -723,8 +738,9 @@ static int launch_proj(pj::Params p, const float* x, const void* w_packed, void*
     if (p.mode == pj::PJ_QKV) {
       q.pos = p.pos + m0;
       q.q_out = p.q_out + (size_t)m0 * qd;
-      q.k_out = p.k_out + (size_t)m0 * p.kv_stride;
-      q.v_out = p.v_out + (size_t)m0 * p.kv_stride;
+      const size_t kv_off = (size_t)m0 * p.kv_stride * (p.kv_f32 ? 4 : 2);
+      q.k_out = static_cast<uint8_t*>(p.k_out) + kv_off;
+      q.v_out = static_cast<uint8_t*>(p.v_out) + kv_off;
     } else if (p.mode == pj::PJ_OUT) {
       q.resid = p.resid + (size_t)m0 * p.N;
     } else if (m0 > 0) {
@@ -872,7 +888,16 @@ size_t rk_proj_workspace_bytes(int m, int k, int n) {
 int rk_qkv_rope(const float* x, int m, int d_model, const void* w_qkv_packed, int hq, int hkv, int d,
                 const int32_t* pos, const double* rope_freq, float* q_out, void* k_out, void* v_out,
                 int64_t kv_row_stride, void* workspace, size_t workspace_bytes, rk_stream_t stream) {
+  return rk_qkv_rope_kv(x, m, d_model, w_qkv_packed, hq, hkv, d, pos, rope_freq, q_out, k_out, v_out, RK_BF16,
+                        kv_row_stride, workspace, workspace_bytes, stream);
+}
+
+int rk_qkv_rope_kv(const float* x, int m, int d_model, const void* w_qkv_packed, int hq, int hkv, int d,
+                   const int32_t* pos, const double* rope_freq, float* q_out, void* k_out, void* v_out,
+                   int kv_dtype, int64_t kv_row_stride, void* workspace, size_t workspace_bytes,
+                   rk_stream_t stream) {
   if (hkv <= 0 || hq % hkv != 0 || d % 2 != 0) return fail(RK_ERR_DOMAIN, "qkv heads %d/%d, d %d", hq, hkv, d);
+  if (kv_dtype != RK_BF16 && kv_dtype != RK_F32) return fail(RK_ERR_DOMAIN, "kv dtype %d", kv_dtype);
   pj::Params p{};
   p.m = m;
   p.K = d_model;
@@ -884,9 +909,10 @@ int rk_qkv_rope(const float* x, int m, int d_model, const void* w_qkv_packed, in
   p.pos = pos;
   p.freq = rope_freq;
   p.q_out = q_out;
-  p.k_out = reinterpret_cast<__nv_bfloat16*>(k_out);
-  p.v_out = reinterpret_cast<__nv_bfloat16*>(v_out);
+  p.k_out = k_out;
+  p.v_out = v_out;
   p.kv_stride = kv_row_stride;
+  p.kv_f32 = kv_dtype == RK_F32;
   return launch_proj(p, x, w_qkv_packed, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -117,17 +117,18 @@ static inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D bf16 map: inner = `inner` elements (row pitch `pitch_bytes`), outer = rows;
-// box = 64 elements x box_rows rows, 128-byte swizzle
+// 2-D bf16 (elem_bytes 2) or fp32 (4) map: inner = `inner` elements (row pitch
+// `pitch_bytes`), outer = rows; box = one 128-byte row slab (64 bf16 / 32 fp32
+// elements) x box_rows rows, 128-byte swizzle
 static inline int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch_bytes,
-                           uint32_t box_rows = 128) {
+                           uint32_t box_rows = 128, int elem_bytes = 2) {
   auto fn = encode_fn();
   if (!fn) return fail(RK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, rows};
   cuuint64_t strides[1] = {pitch_bytes};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(RK_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);

@@ -78,6 +78,7 @@ class EngineConfig:
     max_kept: int = 0             # working-cache capacity in rounds (0: top_percent -> its K, else every round)
     drop_window: float = math.inf  # inactivity drop policy (selection.py:168-204); inf = off
     drop_protect: int = 2         # newest rounds never dropped
+    kv_dtype: str = "bf16"        # KV caches and host blocks: "bf16" or "f32" (the reference's float32 KV)
 
     @property
     def group(self) -> int:
@@ -105,7 +106,12 @@ class RoundDecodeEngine:
             raise ValueError(f"policy {c.policy.kind!r} is not a round-selection strategy")
         if c.capture_mode not in ("post", "pre"):
             raise ValueError(f"capture_mode must be 'post' or 'pre', got {c.capture_mode!r}")
-        self.dtype = torch.bfloat16
+        if c.kv_dtype not in ("bf16", "f32"):
+            raise ValueError(f"kv_dtype must be 'bf16' or 'f32', got {c.kv_dtype!r}")
+        self.dtype = torch.bfloat16 if c.kv_dtype == "bf16" else torch.float32
+        self.es = 2 if c.kv_dtype == "bf16" else 4           # bytes per KV element
+        if c.kv_dtype == "f32" and c.question_rows > 1:
+            raise ValueError("multi-row questions (tcgen05 prefill) need bf16 KV")
         L, lw, B, T, R = c.num_layers, c.watershed, c.batch, c.round_tokens, c.rounds
         if dialogues is None:
             base = 0 if seed is None else int(seed)
@@ -158,7 +164,7 @@ class RoundDecodeEngine:
         n_sets = B if c.host_unique <= 0 else min(B, c.host_unique)
         self.host_sets = n_sets
         self.host_blocks = []
-        pool = torch.randn(1 << 24, generator=torch.Generator().manual_seed(7)).to(self.dtype)   # 32 MiB of bf16 noise
+        pool = torch.randn(1 << 24, generator=torch.Generator().manual_seed(7)).to(self.dtype)   # 16 M noise values
         for u in range(n_sets):
             gid = self.dialogues[u]
             offs = np.random.default_rng(gid + 17).integers(0, 1 << 23, size=R)
@@ -542,7 +548,7 @@ class RoundDecodeEngine:
         """Per upper layer: (src, spitch, dst, dpitch, width, height) arrays, one
         2-row (K, V) strided copy per (dialogue, newly kept round)."""
         c = self.cfg
-        es = 2
+        es = self.es
         T = c.round_tokens
         width = T * self.row * es
         spitch = width
@@ -724,7 +730,7 @@ class RoundDecodeEngine:
         """Algorithmic attention bytes of one decode token (all dialogues, all
         layers): K and V of every visible key, SURVEY.md §8d."""
         c = self.cfg
-        es = 2
+        es = self.es
         mid = self.nq + c.decode_steps // 2           # mean rows of the turn visible to a decode token
         lower = c.watershed * (self.hist + mid) * self.row * 2 * es
         upper = self.L_up * (self.K * c.round_tokens + mid) * self.row * 2 * es
@@ -738,7 +744,7 @@ class RoundDecodeEngine:
     def gpu_kv_bytes(self) -> tuple[int, int]:
         """(resident KV bytes of the round engine, full-cache bytes) at turn end."""
         c = self.cfg
-        es = 2
+        es = self.es
         full = c.batch * c.num_layers * 2 * (self.hist + self.turn_rows) * self.row * es
         resident = c.batch * 2 * self.row * es * (c.watershed * (self.hist + self.turn_rows)
                                                    + self.L_up * (self.K * c.round_tokens + self.turn_rows))

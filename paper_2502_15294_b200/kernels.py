@@ -255,11 +255,14 @@ def _proj_ws(ws, m, k, n, device, tag):
 def qkv_rope(x: torch.Tensor, w_qkv_packed: torch.Tensor, hq: int, hkv: int, d: int, pos: torch.Tensor,
              freq: torch.Tensor, q_out: torch.Tensor, k_out: torch.Tensor, v_out: torch.Tensor,
              kv_row_stride: int | None = None, ws: torch.Tensor | None = None, stream=None) -> None:
-    """q, k, v = RoPE(x W_q), RoPE(x W_k), x W_v for m rows of x (m, d_model) f32."""
+    """q, k, v = RoPE(x W_q), RoPE(x W_k), x W_v for m rows of x (m, d_model) f32;
+    k / v rows in k_out's dtype (bf16 or fp32 caches)."""
     m, dm = x.shape
+    if k_out.dtype != v_out.dtype:
+        raise ValueError("k_out and v_out must share a dtype")
     ws = _proj_ws(ws, m, dm, (hq + 2 * hkv) * d, x.device, "proj")
-    _lib.call("rk_qkv_rope", _lib.ptr(x), m, dm, _lib.ptr(w_qkv_packed), hq, hkv, d, _lib.ptr(pos), _lib.ptr(freq),
-              _lib.ptr(q_out), _lib.ptr(k_out), _lib.ptr(v_out),
+    _lib.call("rk_qkv_rope_kv", _lib.ptr(x), m, dm, _lib.ptr(w_qkv_packed), hq, hkv, d, _lib.ptr(pos),
+              _lib.ptr(freq), _lib.ptr(q_out), _lib.ptr(k_out), _lib.ptr(v_out), kv_code(k_out),
               int(hkv * d if kv_row_stride is None else kv_row_stride), _lib.ptr(ws), ws.numel(),
               _lib.stream_ptr(stream))
 

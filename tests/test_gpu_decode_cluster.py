@@ -29,19 +29,20 @@ from paper_2502_15294_b200 import kernels  # noqa: E402
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _run(lens, hkv, G, d, append=True, cap=None, seed=0):
+def _run(lens, hkv, G, d, append=True, cap=None, seed=0, dtype=None):
+    dtype = dtype or torch.bfloat16
     B = len(lens)
     lens = np.array(lens)
     cap = cap or int(lens.max()) + 1
     g = torch.Generator(device="cuda").manual_seed(seed)
-    kc = torch.randn(B, cap, hkv, d, device="cuda", generator=g).bfloat16()
-    vc = torch.randn(B, cap, hkv, d, device="cuda", generator=g).bfloat16()
+    kc = torch.randn(B, cap, hkv, d, device="cuda", generator=g).to(dtype)
+    vc = torch.randn(B, cap, hkv, d, device="cuda", generator=g).to(dtype)
     q = 2.0 * torch.randn(B, hkv * G, d, device="cuda", generator=g)
-    kn = torch.randn(B, hkv, d, device="cuda", generator=g).bfloat16() if append else None
-    vn = torch.randn(B, hkv, d, device="cuda", generator=g).bfloat16() if append else None
+    kn = torch.randn(B, hkv, d, device="cuda", generator=g).to(dtype) if append else None
+    vn = torch.randn(B, hkv, d, device="cuda", generator=g).to(dtype) if append else None
     sl = torch.from_numpy(lens.astype(np.int32)).cuda()
     max_len = int(lens.max()) + (1 if append else 0)
-    plan = kernels.decode_plan(B, hkv * G, hkv, d, torch.bfloat16, max_len, kc.stride(0))
+    plan = kernels.decode_plan(B, hkv * G, hkv, d, dtype, max_len, kc.stride(0))
     out = kernels.decode_attention(q, kc, vc, sl, max_len, k_new=kn, v_new=vn)
     torch.cuda.synchronize()
     worst = 0.0
@@ -182,3 +183,24 @@ def test_randomized_shapes_vs_oracle():
         plans.add(plan)
         assert err < 2e-5, (i, B, hkv, G, d, append, plan, err)
     assert any(p > 1 for p in plans) and any(p >= 0 for p in plans), plans
+
+
+@pytest.mark.parametrize("lens,hkv,G,d", [
+    ([16512], 8, 4, 128),                 # B=1 C2 lower layer, fp32 KV (the reference's precision)
+    ([2176], 8, 4, 128),
+    ([3000, 1100], 8, 4, 128),
+    ([700, 2999, 64, 1500], 8, 4, 128),   # ragged, one dialogue shorter than a stage
+    ([2999] * 8, 8, 4, 128),
+    ([2999, 17, 1024, 1, 700, 2048, 5, 333, 1500, 64, 2999, 900], 8, 4, 128),
+    ([5000], 4, 7, 128),
+    ([4000, 333], 2, 8, 64),
+    ([1234], 8, 1, 128),
+    ([63, 64, 65, 127, 129], 4, 2, 64),   # stage (64 keys) boundaries
+])
+def test_cluster_decode_f32_vs_oracle(lens, hkv, G, d):
+    """fp32 KV on the cluster decode (64-key fp32 stages, two alternating consumer
+    warp sets, K / V split into bf16 hi + lo on the fly): outputs within 2e-5
+    relative of the fp64 oracle on the identical fp32 inputs (_attn_np.py:26-28)."""
+    plan, err = _run(lens, hkv, G, d, dtype=torch.float32, seed=3)
+    assert plan > 0, plan
+    assert err < 2e-5, err         # same class as the bf16 path; north star: 1e-3

@@ -116,3 +116,43 @@ def test_engine_rejects_overflowing_kept_count():
     with pytest.raises(RuntimeError, match="capacity"):
         with torch.cuda.stream(eng.compute_stream):
             eng.run_turn_eager()
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_engine_f32_kv_matches_oracle(graphs):
+    """fp32 KV caches and host blocks (the reference's float32 KV, _attn_np.py:26-28):
+    the projections write fp32 rows, the cluster decode streams fp32 boxes, the exact
+    scorer reads fp32 keys; kept rounds and answers equal the oracle's turn on
+    unrounded fp32 KV."""
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=8, hkv=2, head_dim=128, rounds=7, round_tokens=64, batch=3,
+                       decode_steps=4, item_chunk=32, plant=2, plant_beta=0.3, question_variants=1,
+                       policy=SelectionPolicy("top_percent", fraction=0.3), kv_dtype="f32")
+    model = DecodeModel(cfg.shape, "cuda", seed=8, prefill_gemm=True)
+    eng = RoundDecodeEngine(cfg, model=model, dialogues=[1, 4, 6])
+    assert eng.lower.dtype == torch.float32 and eng.host_blocks[0][0].dtype == torch.float32
+    lower0 = eng.lower[:, :, :, : eng.hist].cpu().numpy()
+    if graphs:
+        eng.prepare()
+        eng.slot_round[:] = -1
+        kept, _ = eng.run_turn()
+    else:
+        with torch.cuda.stream(eng.compute_stream):
+            kept = eng.run_turn_eager()
+    torch.cuda.synchronize()
+    answers = eng.answers()
+    w = model.host_weights()
+    orc = odm.TurnOracle(w, cfg.hq, cfg.hkv, cfg.head_dim, model.freq.cpu().numpy(), kv_bf16=False)
+    lw, T = cfg.watershed, cfg.round_tokens
+    for b in range(cfg.batch):
+        slots = [int(r) for r in eng.slot_round[b][: len(kept[b])]]
+
+        def blocks(kk, b=b, slots=slots):
+            return [(np.concatenate([eng.host_blocks[b][r][u][0].numpy() for r in slots]),
+                     np.concatenate([eng.host_blocks[b][r][u][1].numpy() for r in slots])) for u in range(eng.L_up)]
+
+        ref = odm.run_turn(orc, [lower0[b, l, 0] for l in range(lw)], [lower0[b, l, 1] for l in range(lw)], blocks,
+                           int(eng.q_tok_all[0, b, 0]), eng.hist, T, cfg.rounds, lw,
+                           orr.SelectionPolicy("top_percent", fraction=0.3), cfg.decode_steps)
+        assert tuple(int(x) for x in kept[b]) == ref["kept"], b
+        assert list(answers[b]) == ref["answer"][:cfg.decode_steps], (b, ref["logit_gaps"])
+        np.testing.assert_array_equal(eng.x[b].cpu().numpy(), ref["x"])

@@ -21,16 +21,19 @@ ap.add_argument("--keys", default="2177,16513")       # C2 upper (4 x 512 + turn
 ap.add_argument("--hq", type=int, default=32)
 ap.add_argument("--hkv", type=int, default=8)
 ap.add_argument("--calls", type=int, default=64)
+ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
 a = ap.parse_args()
+dt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
+es = 2 if a.dtype == "bf16" else 4
 peak = 6547.2
 d = 128
 for S in [int(x) for x in a.keys.split(",")]:
     for B in [int(x) for x in a.batches.split(",")]:
-        kc = torch.randn(B, S + 1, a.hkv, d, device="cuda").bfloat16()
-        vc = torch.randn(B, S + 1, a.hkv, d, device="cuda").bfloat16()
+        kc = torch.randn(B, S + 1, a.hkv, d, device="cuda").to(dt)
+        vc = torch.randn(B, S + 1, a.hkv, d, device="cuda").to(dt)
         q = torch.randn(B, a.hq, d, device="cuda")
-        kn = torch.randn(B, a.hkv, d, device="cuda").bfloat16()
-        vn = torch.randn(B, a.hkv, d, device="cuda").bfloat16()
+        kn = torch.randn(B, a.hkv, d, device="cuda").to(dt)
+        vn = torch.randn(B, a.hkv, d, device="cuda").to(dt)
         sl = torch.full((B,), S, dtype=torch.int32, device="cuda")
         out = torch.empty(B, a.hq, d, device="cuda")
         ws = kernels.decode_workspace(B, a.hq, a.hkv, d, 592, "cuda", tag=f"l{B}_{S}")
@@ -53,8 +56,9 @@ for S in [int(x) for x in a.keys.split(",")]:
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1) / a.calls)
         ms = sorted(ts)[3]
-        byts = B * (S + 1) * a.hkv * d * 2 * 2
-        print(json.dumps(dict(keys=S, B=B, us_per_call=round(ms * 1000, 2), GBps=round(byts / ms / 1e6),
+        byts = B * (S + 1) * a.hkv * d * 2 * es
+        plan = kernels.decode_plan(B, a.hq, a.hkv, d, dt, S + 1, kc.stride(0))
+        print(json.dumps(dict(dtype=a.dtype, keys=S, B=B, plan=plan, us_per_call=round(ms * 1000, 2), GBps=round(byts / ms / 1e6),
                               frac=round(byts / ms / 1e6 / peak, 3), MB=round(byts / 1e6, 1))), flush=True)
         del kc, vc, g
         torch.cuda.empty_cache()
