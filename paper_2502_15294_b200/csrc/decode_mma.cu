@@ -46,6 +46,17 @@ struct MmaTile {
   static_assert(TK % GK == 0, "a stage holds whole runs");
   static constexpr int SB = (TK / GK) * GS;         // bytes per operand per stage
   __host__ __device__ static constexpr int row_off(int r) { return (r / GK) * GS + (r % GK) * ROWB; }
+  // Key of row i (0..7) of n-tile t (0/1) of a warp's 16-key group.  Rows of one
+  // run are ROWB (a multiple of 128 B) apart, i.e. on the same banks, so the 8
+  // rows an ldmatrix reads are taken from as many different runs as the group
+  // has (runs are GS = k*128 + 16 B apart: distinct 16-byte bank slots): with
+  // GK = 2 (C2: 8 kv-heads x 128 dims) every row of a matrix sits in its own
+  // run — conflict-free; GK = 1 keeps the natural order.  The softmax and the
+  // PV product only need P's key order to match V's, which uses the same map.
+  static constexpr int R = GK >= 16 ? 1 : (16 / GK < 8 ? 16 / GK : 8);   // runs one matrix spans
+  __host__ __device__ static constexpr int key(int t, int i) {
+    return GK == 1 ? 8 * t + i : (i % R) * GK + i / R + t * (8 / R);
+  }
   static constexpr size_t smem = 2 * kStages * (size_t)SB + 2 * kStages * sizeof(uint64_t);
 };
 
@@ -195,18 +206,18 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
 #pragma unroll
         for (int kk = 0; kk < KC / 2; ++kk) {
           uint32_t r[4];
-          ldmatrix_x4(r, kb + Tl::row_off(16 * slice + (lane & 7)) + (32 * kk + 8 * (lane >> 3)) * 2);
+          ldmatrix_x4(r, kb + Tl::row_off(16 * slice + Tl::key(0, lane & 7)) + (32 * kk + 8 * (lane >> 3)) * 2);
           mma_bf16_16816(s0, qa[2 * kk], r[0], r[1]);
           mma_bf16_16816(s0, qa[2 * kk + 1], r[2], r[3]);
-          ldmatrix_x4(r, kb + Tl::row_off(16 * slice + 8 + (lane & 7)) + (32 * kk + 8 * (lane >> 3)) * 2);
+          ldmatrix_x4(r, kb + Tl::row_off(16 * slice + Tl::key(1, lane & 7)) + (32 * kk + 8 * (lane >> 3)) * 2);
           mma_bf16_16816(s1, qa[2 * kk], r[0], r[1]);
           mma_bf16_16816(s1, qa[2 * kk + 1], r[2], r[3]);
         }
         float sc[4];
-        sc[0] = (2 * c < nkw) ? s0[0] + s0[2] : -INFINITY;          // key 2c
-        sc[1] = (2 * c + 1 < nkw) ? s0[1] + s0[3] : -INFINITY;      // key 2c+1
-        sc[2] = (2 * c + 8 < nkw) ? s1[0] + s1[2] : -INFINITY;      // key 2c+8
-        sc[3] = (2 * c + 9 < nkw) ? s1[1] + s1[3] : -INFINITY;      // key 2c+9
+        sc[0] = (Tl::key(0, 2 * c) < nkw) ? s0[0] + s0[2] : -INFINITY;
+        sc[1] = (Tl::key(0, 2 * c + 1) < nkw) ? s0[1] + s0[3] : -INFINITY;
+        sc[2] = (Tl::key(1, 2 * c) < nkw) ? s1[0] + s1[2] : -INFINITY;
+        sc[3] = (Tl::key(1, 2 * c + 1) < nkw) ? s1[1] + s1[3] : -INFINITY;
         float tmax = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
@@ -240,7 +251,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) decode_mma_kernel(const __gri
 #pragma unroll
         for (int jj = 0; jj < NT / 2; ++jj) {
           uint32_t r[4];
-          ldmatrix_x4_trans(r, vb + Tl::row_off(16 * slice + (lane & 7) + 8 * ((lane >> 3) & 1)) +
+          ldmatrix_x4_trans(r, vb + Tl::row_off(16 * slice + Tl::key((lane >> 3) & 1, lane & 7)) +
                                    (16 * jj + 8 * (lane >> 4)) * 2);
           mma_bf16_16816(o[2 * jj], pa, r[0], r[1]);
           mma_bf16_16816(o[2 * jj + 1], pa, r[2], r[3]);
