@@ -374,13 +374,19 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // both CTAs' barriers initialised before any remote arrive; also orders the
+  // pair allocation below after both CTAs' start-up writes of the reserved
+  // shared-memory words tcgen05.alloc.cta_group::2 reads (compute-sanitizer
+  // racecheck reported that read, at reserved offsets 0x58-0x5f of both CTAs,
+  // as a RAW hazard against the launch preamble when the alloc came first)
+  cluster_sync();
   if (warp == kMmaWarp) {     // same warp in both CTAs: the pair's TMEM (same columns on both SMs)
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tmem_slot)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   fence_before();
-  cluster_sync();             // both CTAs' barriers initialised before any remote arrive
+  __syncthreads();            // the TMEM address is in this CTA's slot
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_o = tmem + NB * BN;
