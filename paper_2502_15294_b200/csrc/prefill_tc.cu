@@ -700,27 +700,20 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           }
           const float rs = acc2.x + acc2.y;
           l_half = (rescale ? l_half * fac : l_half) + rs;
-          // ---- per-item scoring statistics: this half's tile-local (max, sum), recomputed
-          // from S instead of rescaling rs (which is relative to the running max m_run and
-          // so depends on the keys before the item): identical rounds then get bit-identical
-          // masses wherever they sit in a unit, and exact ties resolve to the lower index
-          // as the reference's stable argsort does (tests/test_gpu_selection_variants.py)
+          // ---- per-item scoring statistics from the softmax's own sum: this half's
+          // tile sum rs is relative to the reference max mu, so (mu, rs) folds into the
+          // item's (m, l) like a tile-local (max, sum) — no second exp per score.  The
+          // masses equal the tile-local form up to fp32 rounding (identical rounds may
+          // differ in the last bits); a kept set decided by such a near-tie has a
+          // K-boundary margin below the engines' refine threshold, and the fp64 exact
+          // re-score (rk_round_scores_exact) decides it as the reference does
           if (p.item_m && hmax != -INFINITY) {
-            const float tm = hmax;
-            float2 t2 = make_float2(0.f, 0.f);
-            const float2 nh = make_float2(-hmax, -hmax);
-#pragma unroll
-            for (int i = 0; i < HK; i += 2) {
-              const float2 dlt = ffma2(make_float2(sc[i], sc[i + 1]), one, nh);
-              t2 = ffma2(make_float2(fast_exp2(dlt.x), fast_exp2(dlt.y)), one, t2);
-            }
-            const float tl = t2.x + t2.y;
             if (m_it == -INFINITY) {
-              m_it = tm;
-              l_it = tl;
+              m_it = mu;
+              l_it = rs;
             } else {
-              const float M = fmaxf(m_it, tm);
-              l_it = l_it * fast_exp2(m_it - M) + tl * fast_exp2(tm - M);
+              const float M = fmaxf(m_it, mu);
+              l_it = l_it * fast_exp2(m_it - M) + rs * fast_exp2(mu - M);
               m_it = M;
             }
           }

@@ -47,7 +47,15 @@ __global__ void probe(const uint8_t* src, const __grid_constant__ CUtensorMap ma
       if (i >= stages) bar_wait(&empty[s], ((i / stages) - 1) & 1);
       bar_expect(&full[s], CHUNK);
       const size_t g = off + (size_t)i * CHUNK;
-      if (mode == 0) {
+      if (mode >= 2) {
+        // `mode` interleaved streams: copy i comes from stream i % mode, each stream a
+        // contiguous 1/mode of this CTA's share (same bytes, more DRAM locality spread)
+        const int per_stream = n / mode;
+        const size_t gs = off + ((size_t)(i % mode) * per_stream + i / mode) * CHUNK;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+            ::"r"(sa(sm + (size_t)s * CHUNK)), "l"(src + gs), "r"(CHUNK), "r"(sa(&full[s])), "l"(pol) : "memory");
+      } else if (mode == 0) {
         const int part = CHUNK / split;
         for (int k = 0; k < split; ++k)
           asm volatile(
@@ -102,9 +110,11 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   for (int g : {64, 96, 128, sms})
-    for (int mode : {0, 1})
+    for (int mode : {0, 1, 2, 4, 8})
       for (int split : {1, 2, 4})
         for (int stages : {6, 11}) {
+          if ((mode != 0 && mode != 1) && split != 1) continue;
+          if (mode == 1 && split != 1) continue;
           const size_t smem = (size_t)stages * CHUNK + 2 * stages * 8;
           probe<<<g, 64, smem>>>(buf, maps[split == 1 ? 0 : split == 2 ? 1 : 2], total, stages, mode, split, sink);
           cudaEventRecord(a);
@@ -115,7 +125,8 @@ int main() {
           float ms = 0;
           cudaEventElapsedTime(&ms, a, b);
           const double moved = 5.0 * (double)(total / g / CHUNK * CHUNK) * g;
-          printf("ctas %4d %s x%d stages %2d: %7.1f GB/s  (%.1f GB/s per SM)\n", g, mode ? "tensor" : "bulk  ", split,
+          printf("ctas %4d %s x%d streams %d stages %2d: %7.1f GB/s  (%.1f GB/s per SM)\n", g,
+                 mode == 1 ? "tensor" : "bulk  ", split, mode >= 2 ? mode : 1,
                  stages, moved / (ms * 1e-3) / 1e9, moved / (ms * 1e-3) / 1e9 / g);
         }
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
