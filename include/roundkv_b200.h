@@ -109,11 +109,11 @@ int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream);
 /* Which decode kernel rk_decode_attention runs for this shape (no launch).
  * The cluster decode reads the caches through 2-D TMA tensor maps spanning the
  * batch, so it also needs cache_stride to be a multiple of hkv*d when batch > 1
- * (else the persistent kernel runs); bf16 only; the rest of the contract
+ * (else the persistent kernel runs); bf16 or fp32 KV; the rest of the contract
  * (append, lengths, PDL ordering, workspace) is the same for every kernel:
  * C > 0  one thread-block cluster of C CTAs per (dialogue, kv-head), split-K
  *        merged in distributed shared memory (small batches: batch*hkv <= SMs,
- *        bf16, d 64/128, no item table);
+ *        bf16 or fp32 (128-key / 64-key TMA stages), d 64/128, no item table);
  * 0      persistent split-K over the concatenated key ranges + merge kernel;
  * -1     the generic split kernel (other dtypes / head shapes). */
 int rk_decode_plan(int batch, int hq, int hkv, int d, int kv_dtype, int max_seq_len, int64_t cache_stride,
