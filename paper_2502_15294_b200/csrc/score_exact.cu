@@ -211,6 +211,171 @@ __global__ void __launch_bounds__(kExThreads) exact_stats_kernel(
   }
 }
 
+// Multi-row questions on the FP64 tensor pipe (mma.sync m8n8k4 f64): the
+// DFMA kernel above reads one q operand from shared memory per FMA and runs at
+// ~1/3 of the FP64 peak; here a warp computes 8 keys x 8 (row, head) combos per
+// instruction with both operands in registers.  The products q*k are exact in
+// fp64 as before; the sum over t is split into 4 interleaved partial sums that
+// the tensor core adds (dims j*D/4 + s for lane j of the k4 step s), so a logit
+// may differ from the sequential sum by fp64 rounding (~1e-16 relative) — the
+// same class as the exp and summation roundings the masses already carry (a
+// kept-set flip needs a K-boundary gap below ~1e-14).  Each key's logit depends
+// only on its own values (not its position), and the statistics are reduced per
+// 128-key sub-chunk aligned to the item start in a fixed order, so identical
+// rounds still get bit-identical masses.
+// Block = 4 warps over 128-key sub-chunks (warp w: keys 32w..32w+31 as 4 n8
+// tiles); combos c = r * G + h (r < 4 rows of the tile, h < G heads) padded to
+// MT x 8.  K: bf16, D % 32 == 0.  grid (items_stride, hkv, batch * row_tiles).
+constexpr int kDmRT = 4;
+template <int MT, int D>
+__global__ void __launch_bounds__(kExThreads) exact_stats_dmma_kernel(
+    const float* __restrict__ q, int n_q, int hq, int G, const __nv_bfloat16* __restrict__ k, int64_t k_bstride,
+    int hkv, const int32_t* __restrict__ seq_len, int s_static, const int64_t* __restrict__ q_pos,
+    const int64_t* __restrict__ k_pos, const int32_t* __restrict__ items, int items_stride,
+    const int32_t* __restrict__ n_items_dev, double scale, int row_tiles, double* __restrict__ part_m,
+    double* __restrict__ part_l) {
+  constexpr int NC = MT * 8, DS = D / 4, JS = DS + 1;        // combos, k4 steps, padded j-stride (doubles)
+  __shared__ double qs[NC * 4 * JS];                          // [combo][j][s] = q[combo][j * DS + s]
+  __shared__ double red[kExWarps][NC];
+  __shared__ double run_m[NC], run_l[NC], sub_m[NC];
+  const int it = blockIdx.x, g = blockIdx.y;
+  const int b = blockIdx.z / row_tiles;
+  const int r0 = (blockIdx.z % row_tiles) * kDmRT;
+  const int n_items = n_items_dev ? n_items_dev[b] : items_stride;
+  if (it >= n_items) return;
+  const int32_t* tab = items + ((size_t)b * items_stride + it) * 3;
+  const int s_b = seq_len ? seq_len[b] : s_static;
+  const int lo = tab[0];
+  const int hi = min(tab[1], s_b);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nr = min(kDmRT, n_q - r0);
+  const int ncombo = kDmRT * G;
+
+  for (int x = tid; x < NC * D; x += kExThreads) {
+    const int c = x / D, t = x - c * D;
+    const int r = c / G, h = c - r * G;
+    const double v = (c < ncombo && r < nr) ? (double)q[(((size_t)b * n_q + r0 + r) * hq + g * G + h) * D + t] : 0.0;
+    qs[c * 4 * JS + (t / DS) * JS + (t % DS)] = v;
+  }
+  for (int x = tid; x < NC; x += kExThreads) {
+    run_m[x] = -INFINITY;
+    run_l[x] = 0.0;
+  }
+  // this thread's combo rows (one per M tile) and their query positions
+  int64_t qp[MT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int c = mt * 8 + (lane >> 2), r = c / G;
+    qp[mt] = (c < ncombo && r < nr) ? q_pos[r0 + r] : INT64_MIN;
+  }
+  __syncthreads();
+
+  const __nv_bfloat16* kb = k + (size_t)b * k_bstride + (size_t)g * D;
+  const int64_t row_stride = (int64_t)hkv * D;
+  const int j = lane & 3, kn = lane >> 2;                   // k4 lane (dim quarter), key of the n8 tile
+  const double* qa = qs + (lane >> 2) * 4 * JS + j * JS;     // + mt * 8 * 4 * JS + s
+  for (int c0 = lo; c0 < hi; c0 += kExThreads) {
+    double acc[4][MT][2];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) acc[nt][mt][0] = acc[nt][mt][1] = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int key = c0 + 32 * warp + 8 * nt + kn;
+      // dims j*DS .. j*DS + DS-1 of this key (bf16), 8 per 16-byte load
+      const uint4* src = reinterpret_cast<const uint4*>(kb + (int64_t)min(key, hi - 1) * row_stride + j * DS);
+      const bool kin = key < hi;
+#pragma unroll 2
+      for (int v = 0; v < DS / 8; ++v) {
+        uint4 w4 = src[v];
+        if (!kin) w4 = make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t w = ww[e >> 1];
+          const double bv = (double)__uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const double av = qa[mt * 8 * 4 * JS + 8 * v + e];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[nt][mt][0]), "+d"(acc[nt][mt][1]) : "d"(av), "d"(bv));
+          }
+        }
+      }
+    }
+    // logits of this thread's 8 keys per combo row: C[row lane/4][cols 2j, 2j+1] of each n8 tile
+    double sv[MT][8];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = c0 + 32 * warp + 8 * nt + 2 * j + e;
+        const bool in = key < hi;
+        const int64_t kp = in ? (k_pos ? k_pos[key] : (int64_t)key) : 0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          sv[mt][2 * nt + e] = (in && kp <= qp[mt]) ? __dmul_rn(acc[nt][mt][e], scale) : -INFINITY;
+      }
+    // sub-chunk max per combo: thread -> 4-lane group -> warp order
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      double m = sv[mt][0];
+#pragma unroll
+      for (int e = 1; e < 8; ++e) m = fmax(m, sv[mt][e]);
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      if (j == 0) red[warp][mt * 8 + kn] = m;
+    }
+    __syncthreads();
+    if (tid < NC) {
+      double m = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kExWarps; ++w) m = fmax(m, red[w][tid]);
+      sub_m[tid] = m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const double m = sub_m[mt * 8 + kn];
+      double l = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) l = __dadd_rn(l, sv[mt][e] == -INFINITY ? 0.0 : exp(__dsub_rn(sv[mt][e], m)));
+      l = __dadd_rn(l, __shfl_xor_sync(0xffffffffu, l, 1));
+      l = __dadd_rn(l, __shfl_xor_sync(0xffffffffu, l, 2));
+      if (j == 0) red[warp][mt * 8 + kn] = l;
+    }
+    __syncthreads();
+    if (tid < NC) {
+      double l = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kExWarps; ++w) l = __dadd_rn(l, red[w][tid]);
+      const double m = sub_m[tid];
+      if (m != -INFINITY) {
+        const double M = run_m[tid];
+        if (M == -INFINITY) {
+          run_m[tid] = m;
+          run_l[tid] = l;
+        } else if (m > M) {
+          run_l[tid] = __fma_rn(run_l[tid], exp(__dsub_rn(M, m)), l);
+          run_m[tid] = m;
+        } else {
+          run_l[tid] = __fma_rn(l, exp(__dsub_rn(m, M)), run_l[tid]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < ncombo) {
+    const int r = tid / G, h = tid - r * G;
+    if (r < nr) {
+      const size_t o = (((size_t)b * n_q + r0 + r) * hq + g * G + h) * items_stride + it;
+      part_m[o] = run_m[tid];
+      part_l[o] = run_l[tid];
+    }
+  }
+}
+
 // capture_mode="pre" (engine.py:187-200): ONE logit per (row, key), the
 // head-summed dot product sum_h q_h . k_kv(h) in fp64 (h ascending, t sequential
 // within a head, as the einsum "nhd,shd->ns"), divided by Hq * sqrt(d); one
@@ -399,6 +564,41 @@ static int launch_exact_stats(const float* q, int batch, int n_q, int hq, int d,
 #undef RK_EXACT_G
 }
 
+// multi-row bf16 questions with d % 32 == 0 on the FP64 tensor pipe (RK_EXACT_DMMA=0: the DFMA kernel)
+static bool use_dmma(int kv_dtype, int n_q, int d, int G) {
+  static const int mode = getenv("RK_EXACT_DMMA") ? atoi(getenv("RK_EXACT_DMMA")) : 1;
+  return mode != 0 && kv_dtype == RK_BF16 && n_q > 1 && (d == 128 || d == 64) && G >= 1 && G <= 8;
+}
+
+template <int MT, int D>
+static int launch_dmma_md(const float* q, int batch, int n_q, int hq, int G, const void* k, int64_t k_bstride,
+                          int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                          const int32_t* items, int items_stride, const int32_t* n_items, double scale, double* pm,
+                          double* pl, cudaStream_t st) {
+  const int row_tiles = (n_q + kDmRT - 1) / kDmRT;
+  dim3 grid(items_stride, hkv, batch * row_tiles);
+  exact_stats_dmma_kernel<MT, D><<<grid, kExThreads, 0, st>>>(
+      q, n_q, hq, G, reinterpret_cast<const __nv_bfloat16*>(k), k_bstride, hkv, seq_len, s, q_pos, k_pos, items,
+      items_stride, n_items, scale, row_tiles, pm, pl);
+  RK_CHECK_LAUNCH("exact_stats_dmma_kernel");
+  return RK_OK;
+}
+
+static int launch_exact_dmma(const float* q, int batch, int n_q, int hq, int d, const void* k, int64_t k_bstride,
+                             int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
+                             const int32_t* items, int items_stride, const int32_t* n_items, double scale,
+                             double* pm, double* pl, cudaStream_t st) {
+  const int G = hq / hkv;
+  const int mt = (kDmRT * G + 7) / 8;
+#define RK_DM(MTV, DV)                                                                                             \
+  if (mt == MTV && d == DV)                                                                                        \
+    return launch_dmma_md<MTV, DV>(q, batch, n_q, hq, G, k, k_bstride, hkv, seq_len, s, q_pos, k_pos, items,        \
+                                   items_stride, n_items, scale, pm, pl, st);
+  RK_DM(1, 128) RK_DM(2, 128) RK_DM(3, 128) RK_DM(4, 128) RK_DM(1, 64) RK_DM(2, 64) RK_DM(3, 64) RK_DM(4, 64)
+#undef RK_DM
+  return fail(RK_ERR_DOMAIN, "exact scoring (dmma): group %d, d %d", G, d);
+}
+
 template <typename KT>
 static int launch_exact_pre(const float* q, int batch, int n_q, int hq, int d, const void* k, int64_t k_bstride,
                             int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
@@ -471,6 +671,9 @@ static int round_scores_exact_impl(int pre, const float* q, int batch, int n_q, 
                                                items, items_stride, n_items, denom, pm, pl, st)
              : launch_exact_pre<float>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos, k_pos, items,
                                        items_stride, n_items, denom, pm, pl, st);
+  } else if (use_dmma(kv_dtype, n_q, d, hq / hkv)) {
+    rc = launch_exact_dmma(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s, q_pos, k_pos, items,
+                           items_stride, n_items, scale, pm, pl, st);
   } else if (kv_dtype == RK_BF16)
     rc = n_q == 1 ? launch_exact_stats<__nv_bfloat16, 1>(q, batch, n_q, hq, d, k, k_batch_stride, hkv, seq_len, s,
                                                          q_pos, k_pos, items, items_stride, n_items, scale, pm, pl, st)
