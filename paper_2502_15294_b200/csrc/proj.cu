@@ -936,30 +936,36 @@ int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int v
                float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                void* workspace, size_t workspace_bytes, rk_stream_t stream) {
   if (m <= 0) return RK_OK;
-  if (m > 64) return fail(RK_ERR_DOMAIN, "lm_head rows %d > 64", m);
-  pj::Params p{};
-  p.m = m;
-  p.K = d_model;
-  p.N = vocab;
-  p.mode = pj::PJ_HEAD;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int rc = launch_proj(p, x, emb_packed, workspace, workspace_bytes, st);
-  if (rc != RK_OK) return rc;
-  const ProjPlan pl = proj_plan(m, d_model, vocab);
-  const float* logits = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(workspace) + pl.logits_off);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(m);
-  cfg.blockDim = dim3(256);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, argmax_embed_kernel, logits, pl.Npad, vocab,
-                                     (const __nv_bfloat16*)emb, d_model, x_next, tokens, pos, tokens_log,
-                                     log_stride);
-  if (e != cudaSuccess) return cuda_status(e, "argmax_embed_kernel launch");
+  // rows in chunks of 64 (the projection's MMA N bound); each chunk's logits reuse the
+  // workspace after the previous chunk's argmax (stream order; the projection's epilogue
+  // writes only after griddepcontrol.wait)
+  for (int m0 = 0; m0 < m; m0 += 64) {
+    const int mc = m - m0 < 64 ? m - m0 : 64;
+    pj::Params p{};
+    p.m = mc;
+    p.K = d_model;
+    p.N = vocab;
+    p.mode = pj::PJ_HEAD;
+    int rc = launch_proj(p, x + (size_t)m0 * d_model, emb_packed, workspace, workspace_bytes, st);
+    if (rc != RK_OK) return rc;
+    const ProjPlan pl = proj_plan(mc, d_model, vocab);
+    const float* logits = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(workspace) + pl.logits_off);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(mc);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, argmax_embed_kernel, logits, pl.Npad, vocab,
+                                       (const __nv_bfloat16*)emb, d_model, x_next + (size_t)m0 * d_model,
+                                       tokens ? tokens + m0 : tokens, pos ? pos + m0 : pos,
+                                       tokens_log ? tokens_log + (size_t)m0 * log_stride : tokens_log, log_stride);
+    if (e != cudaSuccess) return cuda_status(e, "argmax_embed_kernel launch");
+  }
   return RK_OK;
 }
 
