@@ -358,6 +358,8 @@ def main():
         "k_boundary": {"min_rel_gap": eng.min_margin, "scorer": "fp64 exact (rk_round_scores_exact)" if g0.nq == 1
                        else "tcgen05 fused fp32-class, fp64 re-score below the margin",
                        "refine_margin": cfg.refine_margin, "refined_turns": eng.refined_turns,
+                       "refined_dialogue_turns": eng.refined_dialogues,
+                       "max_fused_rel_err": eng.max_fused_rel_err,
                        "note": "relative gap between the K-th and (K+1)-th largest masses, minimum over every "
                                "dialogue and turn of the run"},
         "gpu_kv_saved": {"resident_bytes": resident, "full_cache_bytes": full, "saved_frac": 1 - resident / full},

@@ -71,8 +71,10 @@ class EngineConfig:
     question_rows: int = 1        # n_q: 1 = single-token question (decode path); > 1 = tensor-core prefill
     round_cache: bool = True      # keep rounds kept again in their working-cache slots (no re-fetch)
     question_variants: int = 4    # distinct questions cycled over turns
-    refine_margin: float = 1e-3   # multi-row questions: re-score in fp64 when the K-boundary gap of the
-                                  # fp32-class fused scoring is below this (1-row questions always score in fp64)
+    refine_margin: float = 1e-5   # multi-row questions: re-score in fp64 the dialogues whose K-boundary gap
+                                  # of the fp32-class fused scoring is below this (measured fused error vs the
+                                  # exact masses <= 3e-8 relative on C3, profiles/r02_bench_c3.json;
+                                  # 1-row questions always score in fp64)
     model_seed: int = 42
     capture_mode: str = "post"    # "pre": head-summed-logit softmax scoring (engine.py:187-200)
     max_kept: int = 0             # working-cache capacity in rounds (0: top_percent -> its K, else every round)
@@ -252,6 +254,8 @@ class RoundDecodeEngine:
         self.margin_host = torch.zeros(B, dtype=torch.float64, pin_memory=True)
         self.min_margin = math.inf            # smallest K-boundary margin seen (fp64 masses)
         self.refined_turns = 0                # multi-row turns re-scored in fp64
+        self.refined_dialogues = 0            # dialogue-turns re-scored
+        self.max_fused_rel_err = 0.0          # largest |fused - exact| / exact mass seen when re-scoring
         self.copy_stream = torch.cuda.Stream(self.dev)
         self.compute_stream = torch.cuda.Stream(self.dev)
         # torch creates CUDA events lazily: record once so the handles exist
@@ -386,18 +390,29 @@ class RoundDecodeEngine:
         if not self.uniform_k:
             torch.mul(self.sel_meta[0], self.cfg.round_tokens, out=self.upper_len)
 
-    def _refine_exact(self):
+    def _refine_exact(self, dialogues):
         """Multi-row question whose fused fp32-class scoring left a K-boundary
-        gap below cfg.refine_margin: re-score every dialogue of the group with
+        gap below cfg.refine_margin: re-score those dialogues with
         rk_round_scores_exact (fp64, the reference's arithmetic) and select
-        again (eager, on the current stream)."""
+        again (eager, on the current stream).  Records the largest relative
+        difference between the fused and the exact masses (the fused scorer's
+        measured error, which the margin must exceed)."""
         c = self.cfg
         lw1 = c.watershed - 1
-        kernels.round_scores_exact(self.qq.view(c.batch, self.nq, c.hq, c.head_dim), self.lower[:, lw1, 0],
-                                   self.q_pos, self.items, c.rounds, seq_len=self.lower_len, n_items=self.n_items,
-                                   raw=self.raw, ws=self.ws_exact, capture_mode=c.capture_mode)
+        qq = self.qq.view(c.batch, self.nq, c.hq, c.head_dim)
+        fused = self.raw.clone()
+        for b in dialogues:
+            kernels.round_scores_exact(qq[b:b + 1], self.lower[b:b + 1, lw1, 0], self.q_pos, self.items[b:b + 1],
+                                       c.rounds, seq_len=self.lower_len[b:b + 1], n_items=self.n_items[b:b + 1],
+                                       raw=self.raw[b:b + 1], ws=self.ws_exact, capture_mode=c.capture_mode)
+        if c.capture_mode == "post":
+            rows = torch.as_tensor(list(dialogues), device=self.dev)
+            ex, fu = self.raw[rows], fused[rows]
+            err = ((fu - ex).abs() / ex.abs().clamp_min(1e-300)).max()
+            self.max_fused_rel_err = max(self.max_fused_rel_err, float(err))
         self._select()
         self.refined_turns += 1
+        self.refined_dialogues += len(dialogues)
 
     # ---- multi-row question: projections as library GEMMs, tensor-core prefill attention
     @staticmethod
@@ -603,9 +618,16 @@ class RoundDecodeEngine:
         torch.cuda.current_stream().synchronize()
         if int(self.meta_host[2].abs().sum()) != 0:
             raise RuntimeError("selection reported a negative raw mass")
-        if refine and self.nq > 1 and float(self.margin_host.min()) < self.cfg.refine_margin:
-            self._refine_exact()
-            return self._select_to_host(refine=False)
+        if refine and self.nq > 1:
+            # the fused prefill scoring is the "post" statistic: "pre" questions are always
+            # scored exactly; otherwise only the dialogues whose K-boundary gap is small
+            if self.cfg.capture_mode == "pre":
+                low = list(range(self.cfg.batch))
+            else:
+                low = [b for b in range(self.cfg.batch) if float(self.margin_host[b]) < self.cfg.refine_margin]
+            if low:
+                self._refine_exact(low)
+                return self._select_to_host(refine=False)
         self.min_margin = min(self.min_margin, float(self.margin_host.min()))
         kept = []
         for b in range(self.cfg.batch):
@@ -865,6 +887,14 @@ class GroupedDecoder:
     @property
     def refined_turns(self):
         return sum(e.refined_turns for e in self.groups)
+
+    @property
+    def refined_dialogues(self):
+        return sum(e.refined_dialogues for e in self.groups)
+
+    @property
+    def max_fused_rel_err(self):
+        return max(e.max_fused_rel_err for e in self.groups)
 
     def kv_bytes_per_token(self):
         return sum(e.kv_bytes_per_token() for e in self.groups)
