@@ -77,6 +77,8 @@ def parse():
                     help="fetch every kept round every turn (the reference's transfer pattern)")
     ap.add_argument("--kv-dtype", default="bf16", choices=["bf16", "f32"],
                     help="KV caches / host blocks: bf16 (BASELINE configs[1]) or f32 (the reference's precision)")
+    ap.add_argument("--upper-tier", default="host", choices=["host", "hbm"],
+                    help="deep-layer round blocks in pinned host memory (default) or in HBM (peer-HBM tier)")
     ap.add_argument("--groups", type=int, default=None,
                     help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
@@ -231,6 +233,7 @@ def main():
     if args.host_unique is not None:
         w["host_unique"] = args.host_unique
     w["kv_dtype"] = args.kv_dtype
+    w["upper_tier"] = args.upper_tier
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
@@ -331,7 +334,8 @@ def main():
                                f"decode tokens/turn={eng.turn_tokens} (fixed; EOT ignored) "
                                f"host_round_sets/group={g0.host_sets} (unique per dialogue: "
                                f"{g0.host_sets == g0.cfg.batch}) round_cache={cfg.round_cache} "
-                               f"question_variants={cfg.question_variants} kv_dtype={args.kv_dtype}",
+                               f"question_variants={cfg.question_variants} kv_dtype={args.kv_dtype} "
+                               f"upper_tier={args.upper_tier}",
                    "model": "reference toy transformer (attention + residual, RoPE, tied logits) at "
                             f"{'Llama-3-8B' if cfg.hq == 32 else 'Qwen2-7B'} shapes, GQA, bf16 weights",
                    "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
@@ -352,7 +356,8 @@ def main():
                                 "rounds_fetched_group0_last_turn": g0.last_copied_rounds,
                                 "rounds_kept_group0": g0.cfg.batch * g0.K},
                 "GBps": g0.last_h2d_bytes / (brk["h2d"] / 1000.0) / 1e9 if brk["h2d"] > 0 else None,
-                "link": "PCIe Gen5 x16 (~63 GB/s/dir theoretical)",
+                "link": ("PCIe Gen5 x16 (~63 GB/s/dir theoretical)" if args.upper_tier == "host"
+                 else "HBM tier on this GPU (a peer GPU's HBM over NVLink on a multi-GPU box)"),
                 "link_peak_GBps": link_peak,
                 "link_peak_how": "one 256 MiB pinned-host -> HBM copy, best of 5, CUDA events, before the timed region"},
         "k_boundary": {"min_rel_gap": eng.min_margin, "scorer": "fp64 exact (rk_round_scores_exact)" if g0.nq == 1

@@ -247,6 +247,19 @@ int rk_h2d_gather(int n, const void* const* src_host, const size_t* src_pitch,
                   const size_t* width, const size_t* height,
                   rk_stream_t stream, void* done_event);
 
+/* The peer-HBM tier: the same batched gather when the kept
+ * rounds' upper blocks live in GPU memory — another GPU's HBM over NVLink
+ * (after rk_enable_peer_access) or this GPU's — instead of pinned host memory
+ * (cudaMemcpyDefault: unified addressing picks the path). */
+int rk_peer_gather(int n, const void* const* src, const size_t* src_pitch,
+                   void* const* dst, const size_t* dst_pitch,
+                   const size_t* width, const size_t* height,
+                   rk_stream_t stream, void* done_event);
+
+/* Enable direct loads / copies from peer_device's memory on the current device
+ * (no-op for the current device; RK_ERR_CUDA when the topology forbids it). */
+int rk_enable_peer_access(int peer_device);
+
 /* D2H counterpart for the new round's upper block (writeback_upper :265-278). */
 int rk_d2h_scatter(int n, const void* const* src, const size_t* src_pitch,
                    void* const* dst_host, const size_t* dst_pitch,

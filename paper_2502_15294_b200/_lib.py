@@ -51,6 +51,8 @@ _SIGS = {
     "rk_round_scores_exact_pre": (_i, [_p, _i, _i, _i, _i, _p, _i, _i, _i64, _p, _i, _p, _p, _p, _i, _p, _i, _p, _i,
                                        _p, _p, _sz, _p]),
     "rk_h2d_gather": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "rk_peer_gather": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "rk_enable_peer_access": (_i, [_i]),
     "rk_d2h_scatter": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p]),
     "rk_prefill_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i]),
     "rk_prefill_attention": (_i, [_p, _i, _i, _i, _p, _p, _i, _i, _i, _p, _p, _p, _p, _i, _i, _p, _p, _p, _p, _p,

@@ -33,6 +33,31 @@ int rk_h2d_gather(int n, const void* const* src_host, const size_t* src_pitch, v
                     done_event, "rk_h2d_gather");
 }
 
+int rk_peer_gather(int n, const void* const* src, const size_t* src_pitch, void* const* dst,
+                   const size_t* dst_pitch, const size_t* width, const size_t* height, rk_stream_t stream,
+                   void* done_event) {
+  // source blocks in HBM (this GPU's, or a peer's over NVLink once peer access is
+  // enabled): unified addressing picks the path
+  return copy_batch(n, src, src_pitch, dst, dst_pitch, width, height, cudaMemcpyDefault, stream, done_event,
+                    "rk_peer_gather");
+}
+
+int rk_enable_peer_access(int peer_device) {
+  int cur = 0;
+  RK_CUDA(cudaGetDevice(&cur), "cudaGetDevice");
+  if (peer_device == cur) return RK_OK;
+  int can = 0;
+  RK_CUDA(cudaDeviceCanAccessPeer(&can, cur, peer_device), "cudaDeviceCanAccessPeer");
+  if (!can) return rk::fail(RK_ERR_CUDA, "GPU %d cannot access GPU %d's memory", cur, peer_device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return RK_OK;
+  }
+  RK_CUDA(e, "cudaDeviceEnablePeerAccess");
+  return RK_OK;
+}
+
 int rk_d2h_scatter(int n, const void* const* src, const size_t* src_pitch, void* const* dst_host,
                    const size_t* dst_pitch, const size_t* width, const size_t* height, rk_stream_t stream,
                    void* done_event) {

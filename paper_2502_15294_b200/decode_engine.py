@@ -81,6 +81,9 @@ class EngineConfig:
     drop_window: float = math.inf  # inactivity drop policy (selection.py:168-204); inf = off
     drop_protect: int = 2         # newest rounds never dropped
     kv_dtype: str = "bf16"        # KV caches and host blocks: "bf16" or "f32" (the reference's float32 KV)
+    upper_tier: str = "host"      # where the rounds' deep-layer blocks live: "host" (pinned host memory) or
+                                  # "hbm" (a GPU's HBM: the peer-HBM tier)
+    tier_device: int = -1         # the GPU holding an "hbm" tier (-1: this engine's GPU; another GPU = peer over NVLink)
 
     @property
     def group(self) -> int:
@@ -162,7 +165,17 @@ class RoundDecodeEngine:
             g = _dialogue_gen(self.dev, gid, 1)
             self.lower[b, :, :, : self.hist] = torch.randn((lw, 2, self.hist, c.hkv, c.head_dim), generator=g,
                                                            device=self.dev).to(self.dtype)
-        # ---- pinned host tier: one contiguous upper block per (dialogue set, round)
+        # ---- upper tier: one contiguous upper block per (dialogue set, round), in pinned host
+        # memory (the reference's host tier) or in a GPU's HBM (the peer-HBM tier)
+        if c.upper_tier not in ("host", "hbm"):
+            raise ValueError(f"upper_tier must be 'host' or 'hbm', got {c.upper_tier!r}")
+        tier_dev = None
+        if c.upper_tier == "hbm":
+            tier_dev = torch.device("cuda", self.dev.index if c.tier_device < 0 else c.tier_device)
+            if tier_dev != self.dev:
+                with torch.cuda.device(self.dev):
+                    _lib.call("rk_enable_peer_access", tier_dev.index)
+        self.tier_dev = tier_dev
         n_sets = B if c.host_unique <= 0 else min(B, c.host_unique)
         self.host_sets = n_sets
         self.host_blocks = []
@@ -178,10 +191,13 @@ class RoundDecodeEngine:
                 for s0 in range(0, flat.numel(), 1 << 23):       # distinct window of the pool per block
                     n = min(1 << 23, flat.numel() - s0)
                     flat[s0:s0 + n].copy_(pool[o:o + n])
+                if tier_dev is not None:
+                    blk = blk.to(tier_dev)
                 blocks.append(blk)
             self.host_blocks.append(blocks)
-        self.writeback = torch.empty((B, self.L_up, 2, self.turn_rows, c.hkv, c.head_dim), dtype=self.dtype,
-                                     pin_memory=True)
+        wb_shape = (B, self.L_up, 2, self.turn_rows, c.hkv, c.head_dim)
+        self.writeback = (torch.empty(wb_shape, dtype=self.dtype, pin_memory=True) if tier_dev is None
+                          else torch.empty(wb_shape, dtype=self.dtype, device=tier_dev))    # the new round's tier
 
         # ---- lengths and positions (device) and their per-turn reset values
         self.lower_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
@@ -583,14 +599,15 @@ class RoundDecodeEngine:
         return plans
 
     def issue_gather(self, plans):
-        """rk_h2d_gather per upper layer on the copy stream, one event per layer."""
+        """rk_h2d_gather (host tier) or rk_peer_gather (HBM tier) per upper layer
+        on the copy stream, one event per layer."""
         vp = C.c_void_p
         s = self.copy_stream
         total = 0
         for u, pl in enumerate(plans):
             ev = self.layer_events[u]
             assert ev.cuda_event, "gather event not created"
-            _lib.call("rk_h2d_gather", pl["n"], pl["src"].ctypes.data_as(vp), pl["spitch"].ctypes.data_as(vp),
+            _lib.call("rk_h2d_gather" if self.tier_dev is None else "rk_peer_gather", pl["n"], pl["src"].ctypes.data_as(vp), pl["spitch"].ctypes.data_as(vp),
                       pl["dst"].ctypes.data_as(vp), pl["dpitch"].ctypes.data_as(vp), pl["width"].ctypes.data_as(vp),
                       pl["height"].ctypes.data_as(vp), s.cuda_stream, ev.cuda_event)
             total += int((pl["width"] * pl["height"]).sum())

@@ -156,3 +156,37 @@ def test_engine_f32_kv_matches_oracle(graphs):
         assert tuple(int(x) for x in kept[b]) == ref["kept"], b
         assert list(answers[b]) == ref["answer"][:cfg.decode_steps], (b, ref["logit_gaps"])
         np.testing.assert_array_equal(eng.x[b].cpu().numpy(), ref["x"])
+
+
+def test_engine_hbm_tier_matches_oracle():
+    """The peer-HBM tier: the rounds' deep-layer blocks in GPU
+    memory (here this GPU's; another GPU's over NVLink after rk_enable_peer_access),
+    gathered with rk_peer_gather — kept rounds and answers equal the oracle's turn."""
+    cfg = EngineConfig(num_layers=4, watershed=2, hq=8, hkv=2, head_dim=128, rounds=7, round_tokens=64, batch=2,
+                       decode_steps=4, item_chunk=32, plant=2, plant_beta=0.3, question_variants=1,
+                       policy=SelectionPolicy("top_percent", fraction=0.3), upper_tier="hbm")
+    model = DecodeModel(cfg.shape, "cuda", seed=9, prefill_gemm=True)
+    eng = RoundDecodeEngine(cfg, model=model, dialogues=[3, 8])
+    assert eng.host_blocks[0][0].is_cuda and eng.writeback.is_cuda
+    lower0 = _f(eng.lower[:, :, :, : eng.hist])
+    eng.prepare()
+    eng.slot_round[:] = -1
+    kept, nbytes = eng.run_turn()
+    torch.cuda.synchronize()
+    assert nbytes > 0
+    answers = eng.answers()
+    w = model.host_weights()
+    orc = odm.TurnOracle(w, cfg.hq, cfg.hkv, cfg.head_dim, model.freq.cpu().numpy())
+    lw, T = cfg.watershed, cfg.round_tokens
+    for b in range(cfg.batch):
+        slots = [int(r) for r in eng.slot_round[b][: len(kept[b])]]
+
+        def blocks(kk, b=b, slots=slots):
+            return [(np.concatenate([_f(eng.host_blocks[b][r][u][0]) for r in slots]),
+                     np.concatenate([_f(eng.host_blocks[b][r][u][1]) for r in slots])) for u in range(eng.L_up)]
+
+        ref = odm.run_turn(orc, [lower0[b, l, 0] for l in range(lw)], [lower0[b, l, 1] for l in range(lw)], blocks,
+                           int(eng.q_tok_all[0, b, 0]), eng.hist, T, cfg.rounds, lw,
+                           orr.SelectionPolicy("top_percent", fraction=0.3), cfg.decode_steps)
+        assert tuple(int(x) for x in kept[b]) == ref["kept"], b
+        assert list(answers[b]) == ref["answer"][:cfg.decode_steps], (b, ref["logit_gaps"])
