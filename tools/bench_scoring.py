@@ -22,6 +22,7 @@ ap.add_argument("--nq", default="128,512,1024")
 ap.add_argument("--rounds", type=int, default=64)
 ap.add_argument("--T", type=int, default=1024)
 ap.add_argument("--json")
+ap.add_argument("--exact", action="store_true", help="time rk_round_scores_exact (fp64) instead of the tcgen05 scorer")
 a = ap.parse_args()
 hq, hkv, d = 28, 4, 128
 rows = []
@@ -34,13 +35,13 @@ for nq in [int(x) for x in a.nq.split(",")]:
     kp = torch.arange(s, device="cuda")
     bounds = [(r * a.T, (r + 1) * a.T, r) for r in range(a.rounds)] + [(hist, s, a.rounds)]
     for _ in range(2):
-        stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024)
+        stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024, exact=a.exact)
     torch.cuda.synchronize()
     ts = []
     for _ in range(5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024)
+        stats.round_scores(q, k, qp, kp, bounds, a.rounds, chunk=1024, exact=a.exact)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -50,7 +51,7 @@ for nq in [int(x) for x in a.nq.split(",")]:
     exps = hq * visible
     r = dict(n_q=nq, keys=s, ms=ms, algo_tflops=flop / ms / 1e9, frac_bf16_peak=flop / ms / 1e9 / PEAK_TF,
              tensor_tflops_issued=2 * flop / ms / 1e9, gexp_s=exps / ms / 1e6,
-             path="tcgen05" if os.environ.get("RK_SCORE_TC", "1") != "0" else "cuda-core")
+             path="exact fp64" if a.exact else "tcgen05" if os.environ.get("RK_SCORE_TC", "1") != "0" else "cuda-core")
     rows.append(r)
     print(json.dumps(r), flush=True)
 if a.json:
