@@ -237,7 +237,15 @@ def main():
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
-    groups = args.groups if args.groups else (2 if cfg.batch >= 2 and cfg.batch % 2 == 0 else 1)
+    # dialogue groups in flight: two groups hide one group's per-turn KV gather under the other's decode,
+    # but each group reads the weights once per token step.  Measured (C2 shapes): one group is faster up
+    # to 16 dialogues (B=2 1.82 K vs 1.32 K tok/s, B=8 4.40 K vs 3.89 K), two from 32 (7.64 K vs 6.85 K);
+    # C3 (gathers mostly served by the round cache): one group 2.35 K vs 2.17 K; C4 (1.4 GB gathered per
+    # dialogue-turn): two groups 1.30 K vs 0.98 K
+    default_groups = {"c2": 2 if cfg.batch >= 32 else 1, "c3": 1, "c4": 2}[args.workload]
+    groups = args.groups if args.groups else default_groups
+    if cfg.batch % groups:
+        groups = 1
     eng = GroupedDecoder(cfg, groups=groups, dialogues=shard)
     eng.prepare(e2e=not args.no_e2e)
     link_peak = pcie_h2d_peak(torch, dev_index)

@@ -1,5 +1,6 @@
 # C5 batch sweep on one GPU (the per-GPU share of 1-256 dialogues over 1/2/4/8 GPUs) at C2 shapes:
-# dialogues in 2 groups (1 when B = 1), the model on the GPU; one JSON line per batch on stdout
+# dialogues in bench.py's default groups (one below 32 dialogues, two from 32), the model on the GPU;
+# one JSON line per batch on stdout
 for B in ${BATCHES:-1 2 4 8 16 32 64 128 256}; do
   HU=0; if [ $B -ge 64 ]; then HU=16; fi
   timeout 1200 python bench.py --workload ${WORKLOAD:-c2} --batch $B --host-unique $HU --no-e2e --no-cpu --no-fetch-all --steps ${STEPS:-2} --warmup 3 2>/dev/null |
