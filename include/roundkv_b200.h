@@ -103,6 +103,16 @@ int rk_decode_attention(const float* q, int batch, int hq, int d,
                         float* out, int32_t* advance_len,
                         void* workspace, size_t workspace_bytes, rk_stream_t stream);
 
+/* Row-masked decode for a batch whose rows are not all in the decode loop
+ * (cohort serving): rows with row_active[b] == 0 are skipped entirely — no
+ * append, no output, no length advance.  Runs the cluster decode (one CTA per
+ * (dialogue, kv-head) in several waves beyond one wave of pairs); RK_ERR_DOMAIN
+ * for shapes it does not serve. */
+int rk_decode_attention_rows(const float* q, int batch, int hq, int d, void* k_cache, void* v_cache,
+                             int kv_dtype, int hkv, int64_t cache_stride, const int32_t* seq_len,
+                             int max_seq_len, const void* k_new, const void* v_new, const int32_t* row_active,
+                             float* out, int32_t* advance_len, rk_stream_t stream);
+
 /* seq_len[i] += delta for i < n (advance one decode step) */
 int rk_advance_lengths(int32_t* seq_len, int n, int delta, rk_stream_t stream);
 
@@ -342,6 +352,17 @@ int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int v
                float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                void* workspace, size_t workspace_bytes, rk_stream_t stream);
 int rk_embed(const int32_t* tokens, int m, const void* emb, int d_model, float* x, rk_stream_t stream);
+/* Row-masked forms for a decode batch whose rows (dialogues) are not all in the
+ * decode loop (cohort serving): rows with row_active[t] == 0 keep their
+ * residual (rk_out_proj_rows) / token, position and input row (rk_lm_head_rows).
+ * rk_lm_head_rows with log_pos_base >= 0 logs row t's token at
+ * tokens_log[t * log_stride + pos[t] - log_pos_base + 1] (rows at different steps). */
+int rk_out_proj_rows(const float* a, int m, int k, const void* w_o_packed, int d_model, float* resid,
+                     const int32_t* row_active, void* workspace, size_t workspace_bytes, rk_stream_t stream);
+int rk_lm_head_rows(const float* x, int m, int d_model, const void* emb_packed, int vocab, const void* emb,
+                    float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
+                    const int32_t* row_active, int log_pos_base, void* workspace, size_t workspace_bytes,
+                    rk_stream_t stream);
 /* RoPE + cache append for projections computed by a library GEMM (the multi-row
  * question prefill): qkv [m][(hq + 2 hkv) d] f32 -> q_out [m][hq][d]; k / v rows
  * of row r at k_out / v_out + (r / rows_per_group) * kv_group_stride +

@@ -36,6 +36,9 @@ _SIGS = {
     "rk_decode_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
     "rk_decode_attention": (_i, [_p, _i, _i, _i, _p, _p, _i, _i, _i64, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p, _sz, _p]),
     "rk_advance_lengths": (_i, [_p, _i, _i, _p]),
+    "rk_decode_attention_rows": (_i, [_p, _i, _i, _i, _p, _p, _i, _i, _i64, _p, _i, _p, _p, _p, _p, _p, _p]),
+    "rk_out_proj_rows": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _sz, _p]),
+    "rk_lm_head_rows": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _p, _p, _i, _p, _i, _p, _sz, _p]),
     "rk_decode_plan": (_i, [_i, _i, _i, _i, _i, _i, _i64, _i]),
     "rk_round_scores_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
     "rk_round_scores": (_i, [_p, _i, _i, _i, _p, _i, _i, _i, _p, _p, _p, _i, _i, _p, _p, _p, _sz, _p]),

@@ -127,6 +127,27 @@ __global__ void advance_after_kernel(int32_t* len, int n, int delta) {
   if (i < n) len[i] += delta;
 }
 
+__global__ void advance_after_rows_kernel(int32_t* len, int n, int delta, const int32_t* active) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && active[i]) len[i] += delta;
+}
+
+static int advance_after_rows(int32_t* len, int n, const int32_t* active, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((n + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, advance_after_rows_kernel, len, n, 1, active);
+  if (e != cudaSuccess) return cuda_status(e, "advance_after_rows_kernel launch");
+  return RK_OK;
+}
+
 static int advance_after(int32_t* len, int n, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((n + 255) / 256);
@@ -404,6 +425,28 @@ int rk_decode_attention(const float* q, int batch, int hq, int d, void* k_cache,
   st = dispatch_split(kv_dtype, true, false, G, sh, grid, cs, p);
   if (st) return st;
   if (advance_len) return rk_advance_lengths(advance_len, batch, 1, stream);
+  return RK_OK;
+}
+
+int rk_decode_attention_rows(const float* q, int batch, int hq, int d, void* k_cache, void* v_cache,
+                             int kv_dtype, int hkv, int64_t cache_stride, const int32_t* seq_len,
+                             int max_seq_len, const void* k_new, const void* v_new, const int32_t* row_active,
+                             float* out, int32_t* advance_len, rk_stream_t stream) {
+  Shape sh;
+  int st = check_heads(hq, hkv, d, &sh);
+  if (st) return st;
+  if (batch <= 0) return RK_OK;
+  if (max_seq_len <= 0) return fail(RK_ERR_DOMAIN, "max_seq_len must be positive");
+  if ((k_new == nullptr) != (v_new == nullptr)) return fail(RK_ERR_DOMAIN, "k_new and v_new go together");
+  if (row_active == nullptr) return fail(RK_ERR_DOMAIN, "rk_decode_attention_rows needs row_active");
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  const int C = cluster_decode_size(kv_dtype, d, hkv, hq / hkv, batch, max_seq_len, cache_stride, true);
+  if (C <= 0)
+    return fail(RK_ERR_DOMAIN, "row-masked decode runs the cluster kernel (bf16/fp32, d 64/128, G 1/2/4/7/8)");
+  st = launch_decode_cluster(C, kv_dtype, q, batch, hq, d, k_cache, v_cache, hkv, cache_stride, seq_len,
+                             max_seq_len, k_new, v_new, out, cs, row_active);
+  if (st) return st;
+  if (advance_len) return advance_after_rows(advance_len, batch, row_active, cs);
   return RK_OK;
 }
 

@@ -31,9 +31,12 @@ int launch_decode_bulk(int kv_dtype, int d, int hkv, int G, int nsplit, const Bu
                        int32_t* advance, cudaStream_t st, bool pdl);
 
 // small-batch cluster decode (decode_cluster.cu): cluster size, 0 = not applicable
-int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride);
+// multiwave: beyond one wave of (dialogue, kv-head) pairs, one CTA per pair in several waves
+int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride,
+                        bool multiwave = false);
 int launch_decode_cluster(int C, int kv_dtype, const float* q, int batch, int hq, int d, void* k_cache,
                           void* v_cache, int hkv, int64_t batch_stride, const int32_t* seq_len, int max_len,
-                          const void* k_new, const void* v_new, float* out, cudaStream_t st);
+                          const void* k_new, const void* v_new, float* out, cudaStream_t st,
+                          const int32_t* active = nullptr);
 
 }  // namespace rk

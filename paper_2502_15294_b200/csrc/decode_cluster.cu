@@ -132,6 +132,7 @@ struct ClusterParams {
   int hq, hkv;
   float scale_log2;
   float* out;              // [B][Hq][D]
+  const int32_t* active;   // [B] or null: rows with 0 are skipped (no append, no output)
 };
 
 // fp32 K / V rows r, r+1 at 16-byte chunk c16 (+ byte offset) of one stage -> bf16 hi / lo pairs
@@ -171,6 +172,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_cluster_kernel(const __gri
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.z, h = blockIdx.y;
+  // an inactive row (a dialogue outside the decode loop this step): every CTA of its
+  // cluster leaves before any barrier, so nothing is appended, read or written
+  if (p.active != nullptr && !p.active[b]) {
+    pdl_trigger();
+    return;
+  }
   const uint32_t C = cl_size(), rank = cl_rank();
   const bool append = p.k_new != nullptr;
   const int len = p.seq_len[b] + (append ? 1 : 0);
@@ -573,7 +580,8 @@ int max_clusters(int C) {
 // differ widely runs at the pace of its longest dialogue (the persistent
 // kernel balances keys across SMs instead).  RK_DECODE_CLUSTER=0 disables
 // (A/B runs, tests of the persistent kernel).
-int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride) {
+int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_len, int64_t batch_stride,
+                        bool multiwave) {
   static int mode = -1;
   if (mode < 0) {
     const char* e = std::getenv("RK_DECODE_CLUSTER");
@@ -595,7 +603,7 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
   // the waves are nearly full (B=32: 45.5 vs 50.1 us upper, 297.6 vs 301.4 us lower;
   // B=48 67.0 vs 70.5 us), worse otherwise (B=20: 38.5 vs 33.4 us) and exposed to
   // ragged lengths, so the default keeps the persistent kernel there
-  if (mode == 2 && pairs > sm_count()) return 1;
+  if ((mode == 2 || multiwave) && pairs > sm_count()) return 1;
   for (int C : {16, 12, 8, 6, 4, 3, 2, 1}) {   // 10 (11 co-resident) measured slower at B=1 upper layers
     if (C > cmax) continue;
     if ((int64_t)pairs * C > sm_count()) continue;
@@ -612,7 +620,8 @@ int cluster_decode_size(int kv_dtype, int d, int hkv, int G, int batch, int max_
 
 int launch_decode_cluster(int C, int kv_dtype, const float* q, int batch, int hq, int d, void* k_cache,
                           void* v_cache, int hkv, int64_t batch_stride, const int32_t* seq_len, int max_len,
-                          const void* k_new, const void* v_new, float* out, cudaStream_t st) {
+                          const void* k_new, const void* v_new, float* out, cudaStream_t st,
+                          const int32_t* active) {
   const bool f32 = kv_dtype == RK_F32;
   const int es = f32 ? 4 : 2;
   const uint32_t tk = f32 ? (uint32_t)CTile<float, 128>::TK : (uint32_t)CTile<__nv_bfloat16, 128>::TK;
@@ -641,6 +650,7 @@ int launch_decode_cluster(int C, int kv_dtype, const float* q, int batch, int hq
   p.hkv = hkv;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.out = out;
+  p.active = active;
   const int G = hq / hkv;
   cudaError_t e;
   if (f32)

@@ -118,6 +118,7 @@ struct Params {
   int kv_f32;
   // out
   float* resid;
+  const int32_t* row_active;               // out: rows with 0 keep their residual (nullable = all rows)
   // head
   float* logits;
   // split-K reduction
@@ -216,7 +217,7 @@ __device__ __forceinline__ void finish(const Params& p, int sg, int row, float (
     for (int t = 0; t < NP; ++t) r[t] = t < p.m ? p.resid[(size_t)t * p.N + n] : 0.f;   // all loads in flight
 #pragma unroll
     for (int t = 0; t < NP; ++t)
-      if (t < p.m) p.resid[(size_t)t * p.N + n] = r[t] + v[t];
+      if (t < p.m && (p.row_active == nullptr || p.row_active[t])) p.resid[(size_t)t * p.N + n] = r[t] + v[t];
   } else {
 #pragma unroll
     for (int t = 0; t < NP; ++t) {
@@ -252,6 +253,7 @@ __device__ __forceinline__ void finish_pair(const Params& p, int sg, int pr, int
       store_kv2(p, p.v_out, (size_t)t * p.kv_stride + (n - qd - kd), y0, y1);
     }
   } else if (p.mode == PJ_OUT) {
+    if (p.row_active != nullptr && !p.row_active[t]) return;
     float2* r = reinterpret_cast<float2*>(p.resid + (size_t)t * p.N + n);
     const float2 o = *r;
     *r = make_float2(o.x + y0, o.y + y1);
@@ -743,6 +745,7 @@ static int launch_proj(pj::Params p, const float* x, const void* w_packed, void*
       q.v_out = static_cast<uint8_t*>(p.v_out) + kv_off;
     } else if (p.mode == pj::PJ_OUT) {
       q.resid = p.resid + (size_t)m0 * p.N;
+      if (p.row_active) q.row_active = p.row_active + m0;
     } else if (m0 > 0) {
       return fail(RK_ERR_DOMAIN, "lm_head rows %d > 64 per call", m_all);
     }
@@ -773,11 +776,16 @@ static int launch_proj(pj::Params p, const float* x, const void* w_packed, void*
 __global__ void argmax_embed_kernel(const float* __restrict__ logits, int ld, int V,
                                     const __nv_bfloat16* __restrict__ emb, int D, float* __restrict__ x,
                                     int32_t* __restrict__ tokens, int32_t* __restrict__ pos,
-                                    int32_t* __restrict__ tokens_log, int log_stride) {
+                                    int32_t* __restrict__ tokens_log, int log_stride,
+                                    const int32_t* __restrict__ row_active, int log_pos_base) {
   pdl_wait();
   __shared__ float sv[256];
   __shared__ int si[256];
   const int b = blockIdx.x;
+  if (row_active != nullptr && !row_active[b]) {   // an inactive row keeps its token, position and input
+    pdl_trigger();
+    return;
+  }
   const float* lg = logits + (size_t)b * ld;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -803,7 +811,12 @@ __global__ void argmax_embed_kernel(const float* __restrict__ logits, int ld, in
   for (int e = threadIdx.x; e < D; e += blockDim.x) x[(size_t)b * D + e] = __bfloat162float(emb[(size_t)tok * D + e]);
   if (threadIdx.x == 0) {
     if (tokens) tokens[b] = tok;
-    if (tokens_log) tokens_log[(size_t)b * log_stride] = tok;
+    // log_pos_base >= 0: the token goes to entry pos[b] - log_pos_base + 1 of the row (rows of a cohort
+    // batch sit at different steps); otherwise to the row's entry at tokens_log
+    if (tokens_log) {
+      const int64_t at = log_pos_base >= 0 && pos ? (int64_t)(pos[b] - log_pos_base + 1) : 0;
+      tokens_log[(size_t)b * log_stride + at] = tok;
+    }
     if (pos) pos[b] += 1;
   }
   pdl_trigger();
@@ -918,7 +931,13 @@ int rk_qkv_rope_kv(const float* x, int m, int d_model, const void* w_qkv_packed,
 
 int rk_out_proj(const float* a, int m, int k, const void* w_o_packed, int d_model, float* resid,
                 void* workspace, size_t workspace_bytes, rk_stream_t stream) {
+  return rk_out_proj_rows(a, m, k, w_o_packed, d_model, resid, nullptr, workspace, workspace_bytes, stream);
+}
+
+int rk_out_proj_rows(const float* a, int m, int k, const void* w_o_packed, int d_model, float* resid,
+                     const int32_t* row_active, void* workspace, size_t workspace_bytes, rk_stream_t stream) {
   pj::Params p{};
+  p.row_active = row_active;
   p.m = m;
   p.K = k;
   p.N = d_model;
@@ -935,6 +954,14 @@ size_t rk_lm_head_workspace_bytes(int m, int vocab, int d_model) {
 int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int vocab, const void* emb,
                float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                void* workspace, size_t workspace_bytes, rk_stream_t stream) {
+  return rk_lm_head_rows(x, m, d_model, emb_packed, vocab, emb, x_next, tokens, pos, tokens_log, log_stride, nullptr,
+                         -1, workspace, workspace_bytes, stream);
+}
+
+int rk_lm_head_rows(const float* x, int m, int d_model, const void* emb_packed, int vocab, const void* emb,
+                    float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
+                    const int32_t* row_active, int log_pos_base, void* workspace, size_t workspace_bytes,
+                    rk_stream_t stream) {
   if (m <= 0) return RK_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // rows in chunks of 64 (the projection's MMA N bound); each chunk's logits reuse the
@@ -963,7 +990,8 @@ int rk_lm_head(const float* x, int m, int d_model, const void* emb_packed, int v
     cudaError_t e = cudaLaunchKernelEx(&cfg, argmax_embed_kernel, logits, pl.Npad, vocab,
                                        (const __nv_bfloat16*)emb, d_model, x_next + (size_t)m0 * d_model,
                                        tokens ? tokens + m0 : tokens, pos ? pos + m0 : pos,
-                                       tokens_log ? tokens_log + (size_t)m0 * log_stride : tokens_log, log_stride);
+                                       tokens_log ? tokens_log + (size_t)m0 * log_stride : tokens_log, log_stride,
+                                       row_active ? row_active + m0 : row_active, log_pos_base);
     if (e != cudaSuccess) return cuda_status(e, "argmax_embed_kernel launch");
   }
   return RK_OK;

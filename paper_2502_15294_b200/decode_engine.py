@@ -104,7 +104,10 @@ def _dialogue_gen(device, gid: int, salt: int) -> torch.Generator:
 
 class RoundDecodeEngine:
     def __init__(self, cfg: EngineConfig, device: str = "cuda", model: DecodeModel | None = None,
-                 dialogues=None, seed: int | None = None):
+                 dialogues=None, seed: int | None = None, shared: dict | None = None):
+        """shared (cohort serving, cohort.py): views of a larger batch's caches and
+        length arrays ('lower', 'upper', 'lower_len', 'upper_len') this engine's
+        dialogues live in, so one decode loop can serve several engines' rows."""
         self.cfg = c = cfg
         self.dev = torch.device(device)
         if c.policy.kind not in ("top_percent", "fixed", "adaptive", "all"):
@@ -159,8 +162,15 @@ class RoundDecodeEngine:
         D = c.hq * c.head_dim
 
         # ---- HBM tiers (per-dialogue synthetic history, seeded by the global dialogue id)
-        self.lower = torch.empty((B, lw, 2, self.s_lo, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
-        self.upper = torch.zeros((B, self.L_up, 2, self.s_up, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        if shared is not None:
+            self.lower, self.upper = shared["lower"], shared["upper"]
+            if (tuple(self.lower.shape) != (B, lw, 2, self.s_lo, c.hkv, c.head_dim)
+                    or tuple(self.upper.shape) != (B, self.L_up, 2, self.s_up, c.hkv, c.head_dim)):
+                raise ValueError("shared caches do not match the engine shape")
+        else:
+            self.lower = torch.empty((B, lw, 2, self.s_lo, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+            self.upper = torch.zeros((B, self.L_up, 2, self.s_up, c.hkv, c.head_dim), dtype=self.dtype,
+                                     device=self.dev)
         for b, gid in enumerate(self.dialogues):
             g = _dialogue_gen(self.dev, gid, 1)
             self.lower[b, :, :, : self.hist] = torch.randn((lw, 2, self.hist, c.hkv, c.head_dim), generator=g,
@@ -200,8 +210,11 @@ class RoundDecodeEngine:
                           else torch.empty(wb_shape, dtype=self.dtype, device=tier_dev))    # the new round's tier
 
         # ---- lengths and positions (device) and their per-turn reset values
-        self.lower_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
-        self.upper_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
+        if shared is not None:
+            self.lower_len, self.upper_len = shared["lower_len"], shared["upper_len"]
+        else:
+            self.lower_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
+            self.upper_len = torch.zeros(B, dtype=torch.int32, device=self.dev)
         self.lower_len0 = torch.full((B,), self.hist, dtype=torch.int32, device=self.dev)
         self.upper_len0 = torch.full((B,), self.K * T, dtype=torch.int32, device=self.dev)
         self.pos = torch.zeros(B, dtype=torch.int32, device=self.dev)
@@ -614,8 +627,9 @@ class RoundDecodeEngine:
         return total
 
     # ------------------------------------------------------------------ turn
-    def prepare(self, e2e: bool = False):
-        """Warm up (module attributes, workspace) and capture the CUDA graphs."""
+    def prepare(self, e2e: bool = False, decode_graph: bool = True):
+        """Warm up (module attributes, workspace) and capture the CUDA graphs
+        (decode_graph=False: the answer loop runs elsewhere, cohort.py)."""
         with torch.cuda.stream(self.compute_stream):
             self.run_turn_eager()                     # warm-up, sets kernel attributes
             torch.cuda.synchronize()
@@ -623,9 +637,10 @@ class RoundDecodeEngine:
                 self.graph_a = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self.graph_a, stream=self.compute_stream):
                     self._phase_a()
-                self.graph_b = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(self.graph_b, stream=self.compute_stream):
-                    self._phase_b2()
+                if decode_graph:
+                    self.graph_b = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(self.graph_b, stream=self.compute_stream):
+                        self._phase_b2()
         torch.cuda.synchronize()
 
     def _select_to_host(self, refine: bool = True):

@@ -57,6 +57,24 @@ def decode_attention(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tens
     return out
 
 
+def decode_attention_rows(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, seq_len: torch.Tensor,
+                          max_seq_len: int, row_active: torch.Tensor, *, k_new=None, v_new=None,
+                          out: torch.Tensor | None = None, advance: torch.Tensor | None = None,
+                          stream=None) -> torch.Tensor:
+    """rk_decode_attention_rows: decode_attention over the rows with
+    row_active[b] != 0 (int32 device); the other rows are not touched."""
+    B, hq, d = q.shape
+    stride, hkv = k_cache.stride(0), k_cache.shape[2]
+    if out is None:
+        out = torch.empty((B, hq, d), dtype=torch.float32, device=q.device)
+    if row_active.dtype != torch.int32 or row_active.numel() != B:
+        raise ValueError("row_active must be (B,) int32")
+    _lib.call("rk_decode_attention_rows", _lib.ptr(q), B, hq, d, _lib.ptr(k_cache), _lib.ptr(v_cache),
+              kv_code(k_cache), hkv, stride, _lib.ptr(seq_len), int(max_seq_len), _lib.ptr(k_new), _lib.ptr(v_new),
+              _lib.ptr(row_active), _lib.ptr(out), _lib.ptr(advance), _lib.stream_ptr(stream))
+    return out
+
+
 def decode_plan(batch: int, hq: int, hkv: int, d: int, kv_dtype: torch.dtype, max_seq_len: int,
                 cache_stride: int = 0, has_items: bool = False) -> int:
     """rk_decode_plan: C > 0 = cluster decode with C CTAs per (dialogue, kv-head),
@@ -268,25 +286,27 @@ def qkv_rope(x: torch.Tensor, w_qkv_packed: torch.Tensor, hq: int, hkv: int, d: 
 
 
 def out_proj(a: torch.Tensor, w_o_packed: torch.Tensor, resid: torch.Tensor, ws: torch.Tensor | None = None,
-             stream=None) -> None:
-    """resid (m, d_model) += a (m, k) W_o."""
+             stream=None, row_active: torch.Tensor | None = None) -> None:
+    """resid (m, d_model) += a (m, k) W_o (only the rows with row_active != 0 when given)."""
     m, k = a.shape
     ws = _proj_ws(ws, m, k, resid.shape[1], a.device, "proj")
-    _lib.call("rk_out_proj", _lib.ptr(a), m, k, _lib.ptr(w_o_packed), resid.shape[1], _lib.ptr(resid),
-              _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
+    _lib.call("rk_out_proj_rows", _lib.ptr(a), m, k, _lib.ptr(w_o_packed), resid.shape[1], _lib.ptr(resid),
+              _lib.ptr(row_active), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
 
 
 def lm_head(x: torch.Tensor, emb_packed: torch.Tensor, vocab: int, emb: torch.Tensor, x_next: torch.Tensor,
             tokens: torch.Tensor | None, pos: torch.Tensor | None, tokens_log: torch.Tensor | None = None,
-            log_stride: int = 0, ws: torch.Tensor | None = None, stream=None) -> None:
-    """tokens = first argmax of x E^T; x_next = E[tokens]; pos += 1 (when given)."""
+            log_stride: int = 0, ws: torch.Tensor | None = None, stream=None,
+            row_active: torch.Tensor | None = None, log_pos_base: int = -1) -> None:
+    """tokens = first argmax of x E^T; x_next = E[tokens]; pos += 1 (when given);
+    rows with row_active == 0 (when given) are left unchanged."""
     m, dm = x.shape
     need = _lib.lib.rk_lm_head_workspace_bytes(m, vocab, dm)
     if ws is None or ws.numel() < need:
         ws = scratch(need, x.device, "lm_head")
-    _lib.call("rk_lm_head", _lib.ptr(x), m, dm, _lib.ptr(emb_packed), vocab, _lib.ptr(emb), _lib.ptr(x_next),
-              _lib.ptr(tokens), _lib.ptr(pos), _lib.ptr(tokens_log), int(log_stride), _lib.ptr(ws), ws.numel(),
-              _lib.stream_ptr(stream))
+    _lib.call("rk_lm_head_rows", _lib.ptr(x), m, dm, _lib.ptr(emb_packed), vocab, _lib.ptr(emb), _lib.ptr(x_next),
+              _lib.ptr(tokens), _lib.ptr(pos), _lib.ptr(tokens_log), int(log_stride), _lib.ptr(row_active),
+              int(log_pos_base), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
 
 
 def embed(tokens: torch.Tensor, emb: torch.Tensor, x: torch.Tensor, stream=None) -> None:
