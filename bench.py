@@ -79,6 +79,9 @@ def parse():
                     help="KV caches / host blocks: bf16 (BASELINE configs[1]) or f32 (the reference's precision)")
     ap.add_argument("--upper-tier", default="host", choices=["host", "hbm"],
                     help="deep-layer round blocks in pinned host memory (default) or in HBM (peer-HBM tier)")
+    ap.add_argument("--serving", default="groups", choices=["groups", "cohorts"],
+                    help="groups: independent dialogue groups, each with its own decode loop; cohorts: two "
+                         "phase-offset cohorts sharing one row-masked decode loop (weights read once per step)")
     ap.add_argument("--groups", type=int, default=None,
                     help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
@@ -246,7 +249,12 @@ def main():
     groups = args.groups if args.groups else default_groups
     if cfg.batch % groups:
         groups = 1
-    eng = GroupedDecoder(cfg, groups=groups, dialogues=shard)
+    if args.serving == "cohorts":
+        from paper_2502_15294_b200.cohort import CohortDecoder
+        groups = 2
+        eng = CohortDecoder(cfg, cohorts=2, dialogues=shard)
+    else:
+        eng = GroupedDecoder(cfg, groups=groups, dialogues=shard)
     eng.prepare(e2e=not args.no_e2e)
     link_peak = pcie_h2d_peak(torch, dev_index)
 
@@ -338,7 +346,7 @@ def main():
         "data": "synthetic (random-init weights of the config's shape, random KV history, random question ids)",
         "config": {"workload": f"{args.workload}: L={cfg.num_layers} Lw={cfg.watershed} Hq={cfg.hq} "
                                f"Hkv={cfg.hkv} d={cfg.head_dim} rounds={cfg.rounds}x{cfg.round_tokens} "
-                               f"K={g0.K} batch/GPU={cfg.batch} in {groups} groups question_rows={g0.nq} "
+                               f"K={g0.K} batch/GPU={cfg.batch} in {groups} {'cohorts sharing one decode loop' if args.serving == 'cohorts' else 'groups'} question_rows={g0.nq} "
                                f"decode tokens/turn={eng.turn_tokens} (fixed; EOT ignored) "
                                f"host_round_sets/group={g0.host_sets} (unique per dialogue: "
                                f"{g0.host_sets == g0.cfg.batch}) round_cache={cfg.round_cache} "

@@ -103,6 +103,16 @@ def _dialogue_gen(device, gid: int, salt: int) -> torch.Generator:
 
 
 class RoundDecodeEngine:
+    @staticmethod
+    def shapes(c: EngineConfig) -> dict:
+        """Round slots K of the working cache and the per-dialogue cache capacities
+        (keys) of the lower (s_lo) and upper (s_up) tiers for a config."""
+        R, T = c.rounds, c.round_tokens
+        k_policy = top_k_count(R, c.policy.fraction, c.policy.min_rounds) if c.policy.kind == "top_percent" else R
+        K = min(R, c.max_kept) if c.max_kept > 0 else k_policy
+        turn_rows = max(1, c.question_rows) + c.decode_steps
+        return dict(K=K, s_lo=R * T + turn_rows, s_up=K * T + turn_rows)
+
     def __init__(self, cfg: EngineConfig, device: str = "cuda", model: DecodeModel | None = None,
                  dialogues=None, seed: int | None = None, shared: dict | None = None):
         """shared (cohort serving, cohort.py): views of a larger batch's caches and
