@@ -82,6 +82,7 @@ def parse():
     ap.add_argument("--serving", default="groups", choices=["groups", "cohorts"],
                     help="groups: independent dialogue groups, each with its own decode loop; cohorts: two "
                          "phase-offset cohorts sharing one row-masked decode loop (weights read once per step)")
+    ap.add_argument("--cohorts", type=int, default=2, help="cohorts sharing the decode loop (--serving cohorts)")
     ap.add_argument("--groups", type=int, default=None,
                     help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
@@ -251,8 +252,8 @@ def main():
         groups = 1
     if args.serving == "cohorts":
         from paper_2502_15294_b200.cohort import CohortDecoder
-        groups = 2
-        eng = CohortDecoder(cfg, cohorts=2, dialogues=shard)
+        groups = args.cohorts
+        eng = CohortDecoder(cfg, cohorts=groups, dialogues=shard)
     else:
         eng = GroupedDecoder(cfg, groups=groups, dialogues=shard)
     eng.prepare(e2e=not args.no_e2e)

@@ -28,11 +28,11 @@ def _cfg(**kw):
     return EngineConfig(**base)
 
 
-@pytest.mark.parametrize("turns", [1, 3])
-def test_cohorts_match_single_group(turns):
+@pytest.mark.parametrize("turns,cohorts", [(1, 2), (3, 2), (3, 4)])
+def test_cohorts_match_single_group(turns, cohorts):
     cfg = _cfg()
     dialogues = [2, 5, 9, 11]
-    co = CohortDecoder(cfg, cohorts=2, dialogues=dialogues)
+    co = CohortDecoder(cfg, cohorts=cohorts, dialogues=dialogues)
     co.prepare()
     co.run_turns(turns)
     kept = co.last_kept_by_dialogue
