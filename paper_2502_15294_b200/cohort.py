@@ -95,7 +95,6 @@ class CohortDecoder:
                                  dtype=torch.uint8, device=self.dev)
         self.stream = torch.cuda.Stream(self.dev)
         self.graph = None
-        self.window_log = None
         self.dec_marks = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(cohorts)]
 
     # ------------------------------------------------------------------ the shared token step
