@@ -642,6 +642,13 @@ class RoundDecodeEngine:
         (decode_graph=False: the answer loop runs elsewhere, cohort.py)."""
         with torch.cuda.stream(self.compute_stream):
             self.run_turn_eager()                     # warm-up, sets kernel attributes
+            if self.nq > 1:                           # load the fp64 re-score kernels now, not in a timed turn
+                c = self.cfg
+                kernels.round_scores_exact(self.qq.view(c.batch, self.nq, c.hq, c.head_dim)[:1],
+                                           self.lower[:1, c.watershed - 1, 0], self.q_pos, self.items[:1],
+                                           c.rounds, seq_len=self.lower_len[:1], n_items=self.n_items[:1],
+                                           raw=torch.empty_like(self.raw[:1]), ws=self.ws_exact,
+                                           capture_mode=c.capture_mode)
             torch.cuda.synchronize()
             if self.graph_a is None:
                 self.graph_a = torch.cuda.CUDAGraph()
