@@ -649,6 +649,8 @@ class RoundDecodeEngine:
                                            c.rounds, seq_len=self.lower_len[:1], n_items=self.n_items[:1],
                                            raw=torch.empty_like(self.raw[:1]), ws=self.ws_exact,
                                            capture_mode=c.capture_mode)
+                r0 = self.raw[torch.as_tensor([0], device=self.dev)]            # the error check's torch ops
+                float(((r0 - r0).abs() / r0.abs().clamp_min(1e-300)).max())
             torch.cuda.synchronize()
             if self.graph_a is None:
                 self.graph_a = torch.cuda.CUDAGraph()
