@@ -44,8 +44,6 @@ class CohortDecoder:
     def __init__(self, cfg: EngineConfig, cohorts: int = 2, device: str = "cuda", dialogues=None, seed: int = 0):
         if cfg.batch % cohorts:
             raise ValueError(f"batch {cfg.batch} not divisible by cohorts {cohorts}")
-        if cfg.question_rows != 1:
-            raise ValueError("cohort serving runs 1-row questions")
         self.cfg = c = cfg
         self.dev = torch.device(device)
         self.n_c = cohorts
@@ -54,7 +52,7 @@ class CohortDecoder:
         if dialogues is None:
             dialogues = list(range(seed, seed + c.batch))
         self.dialogues = list(dialogues)
-        self.model = DecodeModel(c.shape, self.dev, seed=c.model_seed)
+        self.model = DecodeModel(c.shape, self.dev, seed=c.model_seed, prefill_gemm=c.question_rows > 1)
         m = self.model
         B, L, lw = c.batch, c.num_layers, c.watershed
         sub = dataclasses.replace(c, batch=per, host_unique=max(1, c.host_unique // cohorts) if c.host_unique else 0)

@@ -28,16 +28,18 @@ def _cfg(**kw):
     return EngineConfig(**base)
 
 
-@pytest.mark.parametrize("turns,cohorts", [(1, 2), (3, 2), (3, 4)])
-def test_cohorts_match_single_group(turns, cohorts):
-    cfg = _cfg()
+@pytest.mark.parametrize("turns,cohorts,rows", [(1, 2, 1), (3, 2, 1), (3, 4, 1), (2, 2, 24)])
+def test_cohorts_match_single_group(turns, cohorts, rows):
+    """rows > 1: multi-row questions (tcgen05 prefill prologue, fused scoring)."""
+    cfg = _cfg(question_rows=rows)
     dialogues = [2, 5, 9, 11]
     co = CohortDecoder(cfg, cohorts=cohorts, dialogues=dialogues)
     co.prepare()
     co.run_turns(turns)
     kept = co.last_kept_by_dialogue
     got = co.answers()
-    ref = RoundDecodeEngine(cfg, model=DecodeModel(cfg.shape, "cuda", seed=cfg.model_seed), dialogues=dialogues)
+    ref = RoundDecodeEngine(cfg, model=DecodeModel(cfg.shape, "cuda", seed=cfg.model_seed, prefill_gemm=rows > 1),
+                            dialogues=dialogues)
     ref.prepare()
     # prepare ran one eager turn on both sides (each cohort engine and the reference)
     for _ in range(turns):
