@@ -9,10 +9,12 @@
 // and round k's keys of capn.
 //
 // Here:
-//  * logits: one thread per key, the same sequential fp64 sum over t.  q is fp32
-//    and K fp32 or bf16, so every product q*k is EXACT in fp64 (<= 48 of 53
-//    mantissa bits): an FMA and the reference's separate multiply + add round
-//    identically, and the logits are bit-identical to the reference's;
+//  * logits: q is fp32 and K fp32 or bf16, so every product q*k is EXACT in fp64
+//    (<= 48 of 53 mantissa bits).  bf16 keys with d 64 / 128 run on the FP64
+//    tensor pipe (exact_stats_dmma_kernel: the sum over t in four interleaved
+//    partial sums, ~1e-16 relative from the reference's sequential sum); other
+//    shapes run one thread per key with the reference's sequential fp64 sum
+//    (an FMA and its separate multiply + add round identically: bit-identical);
 //  * per (row, head, round-aligned item): (m, l = sum exp(s - m)) in fp64,
 //    reduced in a fixed tree relative to the item's first key, so identical
 //    rounds get bit-identical statistics wherever they sit (exact ties go to
@@ -226,8 +228,7 @@ __global__ void __launch_bounds__(kExThreads) exact_stats_kernel(
 // Block = 4 warps over 128-key sub-chunks (warp w: keys 32w..32w+31 as 4 n8
 // tiles); combos c = r * G + h (r < 4 rows of the tile, h < G heads) padded to
 // MT x 8.  K: bf16, D % 32 == 0.  grid (items_stride, hkv, batch * row_tiles).
-constexpr int kDmRT = 4;
-template <int MT, int D>
+template <int RT, int MT, int D>
 __global__ void __launch_bounds__(kExThreads) exact_stats_dmma_kernel(
     const float* __restrict__ q, int n_q, int hq, int G, const __nv_bfloat16* __restrict__ k, int64_t k_bstride,
     int hkv, const int32_t* __restrict__ seq_len, int s_static, const int64_t* __restrict__ q_pos,
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kExThreads) exact_stats_dmma_kernel(
   __shared__ double run_m[NC], run_l[NC], sub_m[NC];
   const int it = blockIdx.x, g = blockIdx.y;
   const int b = blockIdx.z / row_tiles;
-  const int r0 = (blockIdx.z % row_tiles) * kDmRT;
+  const int r0 = (blockIdx.z % row_tiles) * RT;
   const int n_items = n_items_dev ? n_items_dev[b] : items_stride;
   if (it >= n_items) return;
   const int32_t* tab = items + ((size_t)b * items_stride + it) * 3;
@@ -248,8 +249,8 @@ __global__ void __launch_bounds__(kExThreads) exact_stats_dmma_kernel(
   const int lo = tab[0];
   const int hi = min(tab[1], s_b);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nr = min(kDmRT, n_q - r0);
-  const int ncombo = kDmRT * G;
+  const int nr = min(RT, n_q - r0);
+  const int ncombo = RT * G;
 
   for (int x = tid; x < NC * D; x += kExThreads) {
     const int c = x / D, t = x - c * D;
@@ -564,20 +565,21 @@ static int launch_exact_stats(const float* q, int batch, int n_q, int hq, int d,
 #undef RK_EXACT_G
 }
 
-// multi-row bf16 questions with d % 32 == 0 on the FP64 tensor pipe (RK_EXACT_DMMA=0: the DFMA kernel)
+// bf16 keys with d 64 / 128 on the FP64 tensor pipe, 1-row (decode questions: 4 row tiles would
+// waste 3/4 of the combos) or 4-row tiles (RK_EXACT_DMMA=0: the DFMA kernels)
 static bool use_dmma(int kv_dtype, int n_q, int d, int G) {
   static const int mode = getenv("RK_EXACT_DMMA") ? atoi(getenv("RK_EXACT_DMMA")) : 1;
-  return mode != 0 && kv_dtype == RK_BF16 && n_q > 1 && (d == 128 || d == 64) && G >= 1 && G <= 8;
+  return mode != 0 && kv_dtype == RK_BF16 && (d == 128 || d == 64) && G >= 1 && G <= 8;
 }
 
-template <int MT, int D>
+template <int RT, int MT, int D>
 static int launch_dmma_md(const float* q, int batch, int n_q, int hq, int G, const void* k, int64_t k_bstride,
                           int hkv, const int32_t* seq_len, int s, const int64_t* q_pos, const int64_t* k_pos,
                           const int32_t* items, int items_stride, const int32_t* n_items, double scale, double* pm,
                           double* pl, cudaStream_t st) {
-  const int row_tiles = (n_q + kDmRT - 1) / kDmRT;
+  const int row_tiles = (n_q + RT - 1) / RT;
   dim3 grid(items_stride, hkv, batch * row_tiles);
-  exact_stats_dmma_kernel<MT, D><<<grid, kExThreads, 0, st>>>(
+  exact_stats_dmma_kernel<RT, MT, D><<<grid, kExThreads, 0, st>>>(
       q, n_q, hq, G, reinterpret_cast<const __nv_bfloat16*>(k), k_bstride, hkv, seq_len, s, q_pos, k_pos, items,
       items_stride, n_items, scale, row_tiles, pm, pl);
   RK_CHECK_LAUNCH("exact_stats_dmma_kernel");
@@ -589,11 +591,17 @@ static int launch_exact_dmma(const float* q, int batch, int n_q, int hq, int d, 
                              const int32_t* items, int items_stride, const int32_t* n_items, double scale,
                              double* pm, double* pl, cudaStream_t st) {
   const int G = hq / hkv;
-  const int mt = (kDmRT * G + 7) / 8;
+  if (n_q == 1) {
+    if (d == 128) return launch_dmma_md<1, 1, 128>(q, batch, n_q, hq, G, k, k_bstride, hkv, seq_len, s, q_pos, k_pos,
+                                                   items, items_stride, n_items, scale, pm, pl, st);
+    return launch_dmma_md<1, 1, 64>(q, batch, n_q, hq, G, k, k_bstride, hkv, seq_len, s, q_pos, k_pos, items,
+                                    items_stride, n_items, scale, pm, pl, st);
+  }
+  const int mt = (4 * G + 7) / 8;
 #define RK_DM(MTV, DV)                                                                                             \
   if (mt == MTV && d == DV)                                                                                        \
-    return launch_dmma_md<MTV, DV>(q, batch, n_q, hq, G, k, k_bstride, hkv, seq_len, s, q_pos, k_pos, items,        \
-                                   items_stride, n_items, scale, pm, pl, st);
+    return launch_dmma_md<4, MTV, DV>(q, batch, n_q, hq, G, k, k_bstride, hkv, seq_len, s, q_pos, k_pos, items,     \
+                                      items_stride, n_items, scale, pm, pl, st);
   RK_DM(1, 128) RK_DM(2, 128) RK_DM(3, 128) RK_DM(4, 128) RK_DM(1, 64) RK_DM(2, 64) RK_DM(3, 64) RK_DM(4, 64)
 #undef RK_DM
   return fail(RK_ERR_DOMAIN, "exact scoring (dmma): group %d, d %d", G, d);
