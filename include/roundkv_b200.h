@@ -202,17 +202,20 @@ int rk_select_batch_active(const double* raw, int n, int ld, int batch, const ui
  * margin_out [batch] float64.  The fp32-class scorers (rk_round_scores, the
  * fused decode / prefill scoring) reproduce the reference's kept set whenever
  * the margin exceeds twice their relative error; below that the caller
- * re-scores with rk_round_scores_exact (the engines use 1e-4). */
+ * re-scores with rk_round_scores_exact (the engines use 1e-5 for multi-row
+ * questions; 1-row questions are always scored exactly). */
 int rk_selection_margin(const double* masses, int n, int ld, int batch, int kind, double v, int k_top,
                         double kappa, double* margin_out, rk_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * 4b. Exact (fp64) watershed round scoring with the reference kernel's
- *    arithmetic (_attn_ext.pyx:52-76,113-114 + stats.py:59-94): logits are the
- *    same sequential fp64 dot products (every q*k product is exact in fp64, so
- *    they are bit-identical), softmax statistics per (row, head, round-aligned
- *    item) in fp64, Eq. 1 masses in fp64 — the kept set is the reference's up
- *    to fp64 rounding (~1e-16 relative), and identical rounds tie exactly.
+ *    arithmetic (_attn_ext.pyx:52-76,113-114 + stats.py:59-94): logits are fp64
+ *    dot products of exact fp64 products (q fp32 x k bf16/fp32), summed on the
+ *    FP64 tensor pipe for bf16 keys with d 64/128 (~1e-16 from the reference's
+ *    sequential sum) and sequentially otherwise; softmax statistics per (row,
+ *    head, round-aligned item) in fp64, Eq. 1 masses in fp64 — the kept set is
+ *    the reference's up to fp64 rounding (~1e-16 relative), and identical rounds
+ *    tie exactly (a key's logit never depends on its position).
  *    batch dialogues: q [batch][n_q][hq][d] f32; dialogue b's keys start at
  *    k + b*k_batch_stride elements, [s_b][hkv][d] (s_b = seq_len[b], or s when
  *    seq_len is NULL); q_pos [n_q] int64 (shared), k_pos [s] int64 or NULL
