@@ -213,10 +213,17 @@ class CohortDecoder:
                 errors.append(exc)
                 stop.set()
 
+        copied = [None] * len(self.active_host)    # event of the last copy out of each pinned mask buffer
+
         def set_mask(mask, nbuf):
-            hb = self.active_host[nbuf % len(self.active_host)]
+            i = nbuf % len(self.active_host)
+            if copied[i] is not None:
+                copied[i].synchronize()             # never rewrite a buffer a pending copy still reads
+            hb = self.active_host[i]
             hb.copy_(torch.from_numpy(mask))
             self.active.copy_(hb, non_blocking=True)
+            copied[i] = torch.cuda.Event()
+            copied[i].record(self.stream)
 
         threads = [threading.Thread(target=cohort, args=(k,)) for k in range(n_c)]
         torch.cuda.synchronize()
