@@ -366,6 +366,52 @@ int rk_lm_head_rows(const float* x, int m, int d_model, const void* emb_packed, 
                     float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                     const int32_t* row_active, int log_pos_base, void* workspace, size_t workspace_bytes,
                     rk_stream_t stream);
+/* ---- the whole decode token step in one persistent launch (small batches) ----
+ * One answer token of every dialogue through all num_layers layers + the tied
+ * logits and first-max argmax (reference engine.py:244-271 forward_range per
+ * layer, pipeline.py:298-313 the greedy decode loop body): for each layer
+ * x -> RoPE(x W_q), RoPE(x W_k), x W_v (rows appended at lower_len / upper_len),
+ * attention over the cached keys + the new one, x += attn W_o; then
+ * tokens = argmax(x E^T), x = E[tokens], pos / lower_len / upper_len += 1 and
+ * tokens_log[b * log_stride] = token (when tokens_log is given).
+ * Layout as the layered entries: lower [batch][watershed][2][lower_seq][hkv][head_dim]
+ * and upper [batch][num_layers - watershed][2][upper_seq][hkv][head_dim] bf16;
+ * w_qkv / w_o: DEVICE arrays of num_layers rk_pack_weight images (W_q|W_k|W_v,
+ * W_o); emb_packed = rk_pack_weight(E^T), emb = E [vocab][d_model] bf16.
+ * One CTA per SM for the whole step (producer warp streaming every weight tile
+ * and cached K/V box of the step through a shared-memory ring; consumers
+ * synchronised by device-scope counters), so nothing else may occupy the GPU's
+ * SMs concurrently.  The workspace (rk_decode_step_workspace_bytes) is zeroed
+ * once and then reused by every launch (monotonic counters, epoch in word 0).
+ * Supported: rk_decode_step_supported() (batch <= 16, group <= 8, head_dim 128,
+ * bf16 KV). */
+typedef struct rk_decode_step_args {
+  int batch, num_layers, watershed, hq, hkv, head_dim, vocab;
+  float* x;                        /* [batch][hq * head_dim] residual in; next token's embedding out */
+  void* lower;
+  int64_t lower_seq;
+  void* upper;
+  int64_t upper_seq;
+  int32_t* lower_len;
+  int32_t* upper_len;
+  int32_t* pos;
+  const double* rope_freq;         /* [head_dim / 2] (engine.py:162-164) */
+  const void* const* w_qkv;
+  const void* const* w_o;
+  const void* emb_packed;
+  const void* emb;
+  int32_t* tokens;                 /* nullable */
+  int32_t* tokens_log;             /* nullable */
+  int log_stride;
+  void* workspace;
+  size_t workspace_bytes;
+} rk_decode_step_args;
+size_t rk_decode_step_workspace_bytes(int batch, int num_layers, int hq, int hkv, int head_dim, int vocab);
+int rk_decode_step_supported(int batch, int hq, int hkv, int head_dim, int kv_dtype);
+int rk_decode_step(const rk_decode_step_args* args, rk_stream_t stream);
+/* the code a bounded wait left in the workspace before trapping (0 = none) */
+int rk_decode_step_watchdog(const void* workspace, unsigned* code_out, rk_stream_t stream);
+
 /* RoPE + cache append for projections computed by a library GEMM (the multi-row
  * question prefill): qkv [m][(hq + 2 hkv) d] f32 -> q_out [m][hq][d]; k / v rows
  * of row r at k_out / v_out + (r / rows_per_group) * kv_group_stride +

@@ -70,7 +70,20 @@ _SIGS = {
     "rk_lm_head": (_i, [_p, _i, _i, _p, _i, _p, _p, _p, _p, _p, _i, _p, _sz, _p]),
     "rk_embed": (_i, [_p, _i, _p, _i, _p, _p]),
     "rk_rope_rows": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _i64, _i, _i64, _p]),
+    "rk_decode_step_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
+    "rk_decode_step_supported": (_i, [_i, _i, _i, _i, _i]),
+    "rk_decode_step": (_i, [_p, _p]),
+    "rk_decode_step_watchdog": (_i, [_p, _p, _p]),
 }
+
+
+class DecodeStepArgs(C.Structure):
+    """rk_decode_step_args (include/roundkv_b200.h)."""
+    _fields_ = [(n, _i) for n in ("batch", "num_layers", "watershed", "hq", "hkv", "head_dim", "vocab")] + [
+        ("x", _p), ("lower", _p), ("lower_seq", _i64), ("upper", _p), ("upper_seq", _i64),
+        ("lower_len", _p), ("upper_len", _p), ("pos", _p), ("rope_freq", _p), ("w_qkv", _p), ("w_o", _p),
+        ("emb_packed", _p), ("emb", _p), ("tokens", _p), ("tokens_log", _p), ("log_stride", _i),
+        ("workspace", _p), ("workspace_bytes", _sz)]
 
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)

@@ -55,7 +55,8 @@ class CohortDecoder:
         self.model = DecodeModel(c.shape, self.dev, seed=c.model_seed, prefill_gemm=c.question_rows > 1)
         m = self.model
         B, L, lw = c.batch, c.num_layers, c.watershed
-        sub = dataclasses.replace(c, batch=per, host_unique=max(1, c.host_unique // cohorts) if c.host_unique else 0)
+        sub = dataclasses.replace(c, batch=per, host_unique=max(1, c.host_unique // cohorts) if c.host_unique else 0,
+                                  step_kernel="layers")    # the masked answer loop is this class's own
         # the shared HBM tiers and length arrays, sized as one engine's
         probe = RoundDecodeEngine.shapes(sub)
         dt = torch.bfloat16 if c.kv_dtype == "bf16" else torch.float32

@@ -84,6 +84,10 @@ class EngineConfig:
     upper_tier: str = "host"      # where the rounds' deep-layer blocks live: "host" (pinned host memory) or
                                   # "hbm" (a GPU's HBM: the peer-HBM tier)
     tier_device: int = -1         # the GPU holding an "hbm" tier (-1: this engine's GPU; another GPU = peer over NVLink)
+    step_kernel: str = "layers"   # answer loop: "persistent" = one rk_decode_step launch per token (whole step,
+                                  # every layer, one CTA per SM); "layers" = qkv / attention / out kernels per
+                                  # layer; "auto" = persistent when supported (batch <= 16, bf16 KV, d = 128)
+                                  # and the engine has the GPU to itself (one group)
 
     @property
     def group(self) -> int:
@@ -126,6 +130,8 @@ class RoundDecodeEngine:
             raise ValueError(f"capture_mode must be 'post' or 'pre', got {c.capture_mode!r}")
         if c.kv_dtype not in ("bf16", "f32"):
             raise ValueError(f"kv_dtype must be 'bf16' or 'f32', got {c.kv_dtype!r}")
+        if c.step_kernel not in ("auto", "persistent", "layers"):
+            raise ValueError(f"step_kernel must be 'auto', 'persistent' or 'layers', got {c.step_kernel!r}")
         self.dtype = torch.bfloat16 if c.kv_dtype == "bf16" else torch.float32
         self.es = 2 if c.kv_dtype == "bf16" else 4           # bytes per KV element
         if c.kv_dtype == "f32" and c.question_rows > 1:
@@ -310,6 +316,21 @@ class RoundDecodeEngine:
         self.meta_host = torch.empty((3, B), dtype=torch.int32, pin_memory=True)
         self.graph_a = None
         self.graph_b = None
+        # ---- the persistent whole-step kernel (rk_decode_step) for the answer loop
+        supported = kernels.decode_step_supported(B, c.hq, c.hkv, c.head_dim, self.dtype)
+        if c.step_kernel == "persistent" and not supported:
+            raise ValueError("step_kernel='persistent' needs batch <= 16, group <= 8, head_dim 128 and bf16 KV")
+        self.persistent = supported and c.step_kernel in ("auto", "persistent")
+        if self.persistent:
+            m = self.model
+            self.w_qkv_table = torch.tensor([w.data_ptr() for w in m.w_qkv_packed], dtype=torch.int64, device=self.dev)
+            self.w_o_table = torch.tensor([w.data_ptr() for w in m.w_o_packed], dtype=torch.int64, device=self.dev)
+            self.step_ws = kernels.decode_step_workspace(B, L, c.hq, c.hkv, c.head_dim, m.shape.vocab, self.dev)
+            self.step_args = [kernels.decode_step_args(
+                self.x, self.lower, self.upper, self.lower_len, self.upper_len, self.pos, m.freq, self.w_qkv_table,
+                self.w_o_table, m.emb_packed, m.emb, c.hq, c.hkv, lw, self.step_ws, tokens=self.tokens,
+                tokens_log=self.answer[:, t + 1:], log_stride=self.answer.shape[1], vocab=m.shape.vocab)
+                for t in range(c.decode_steps)]
         self.last_kept = None
         self.marks = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         self.window_log = None        # list of (start, end) decode-loop events per turn when enabled
@@ -374,6 +395,8 @@ class RoundDecodeEngine:
     def decode_kernel_desc(self) -> str:
         """The decode attention kernels the answer tokens run (lower / upper layers)."""
         c = self.cfg
+        if self.persistent:
+            return "step_kernel (one persistent launch per token: every layer's projections, attention, merge)"
         out = []
         for name, kc, cap in (("lower", self.lower[:, 0, 0], self.s_lo), ("upper", self.upper[:, 0, 0], self.s_up)):
             plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0))
@@ -385,6 +408,8 @@ class RoundDecodeEngine:
         """Kernels of one answer token: per layer qkv_rope + attention (+ length
         advance) + out_proj; then the logits GEMV + argmax/embed."""
         c = self.cfg
+        if self.persistent:
+            return 1
         return sum(2 + self._attn_launches(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
                    for l in range(c.num_layers)) + 2
 
@@ -550,6 +575,10 @@ class RoundDecodeEngine:
         c, m = self.cfg, self.model
         self.pos.copy_(self.pos_dec0)
         kernels.embed(self.sep, m.emb, self.x)
+        if self.persistent:
+            for t in range(c.decode_steps):
+                kernels.decode_step(self.step_args[t])
+            return
         for t in range(c.decode_steps):
             for l in range(c.num_layers):
                 self._layer(l, advance=(l == c.watershed - 1 or l == c.num_layers - 1))
@@ -844,6 +873,9 @@ class GroupedDecoder:
         per = cfg.batch // groups
         sub = dataclasses.replace(cfg, batch=per,
                                   host_unique=max(1, cfg.host_unique // groups) if cfg.host_unique else 0)
+        if groups > 1 and cfg.step_kernel == "auto":
+            # concurrent groups share the SMs: the persistent step needs one CTA on every SM
+            sub = dataclasses.replace(sub, step_kernel="layers")
         if dialogues is None:
             dialogues = list(range(seed, seed + cfg.batch))
         self.cfg = cfg

@@ -309,6 +309,47 @@ def lm_head(x: torch.Tensor, emb_packed: torch.Tensor, vocab: int, emb: torch.Te
               int(log_pos_base), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
 
 
+def decode_step_supported(batch: int, hq: int, hkv: int, head_dim: int, kv_dtype=torch.bfloat16) -> bool:
+    """Whether rk_decode_step (the persistent whole-step kernel) covers this shape."""
+    code = {torch.bfloat16: _lib.RK_BF16, torch.float32: _lib.RK_F32}.get(kv_dtype, -1)
+    return bool(_lib.lib.rk_decode_step_supported(batch, hq, hkv, head_dim, code))
+
+
+def decode_step_workspace(batch: int, num_layers: int, hq: int, hkv: int, head_dim: int, vocab: int,
+                          device) -> torch.Tensor:
+    """The zeroed workspace rk_decode_step reuses across launches (monotonic counters)."""
+    need = _lib.lib.rk_decode_step_workspace_bytes(batch, num_layers, hq, hkv, head_dim, vocab)
+    return torch.zeros(max(256, int(need)), dtype=torch.uint8, device=device)
+
+
+def decode_step_args(x, lower, upper, lower_len, upper_len, pos, freq, w_qkv_table, w_o_table, emb_packed, emb,
+                     hq: int, hkv: int, watershed: int, ws, tokens=None, tokens_log=None, log_stride: int = 0,
+                     vocab: int | None = None):
+    """rk_decode_step_args for one token step over all layers (see the header):
+    lower (B, Lw, 2, S_lo, hkv, d), upper (B, L - Lw, 2, S_up, hkv, d) bf16;
+    w_*_table: int64 device tensors of the layers' packed-weight addresses."""
+    B, d = x.shape[0], lower.shape[-1]
+    a = _lib.DecodeStepArgs()
+    a.batch, a.num_layers, a.watershed = B, int(w_qkv_table.numel()), int(watershed)
+    a.hq, a.hkv, a.head_dim, a.vocab = hq, hkv, d, int(emb.shape[0] if vocab is None else vocab)
+    a.x = _lib.ptr(x)
+    a.lower, a.lower_seq = _lib.ptr(lower), int(lower.shape[3])
+    a.upper, a.upper_seq = _lib.ptr(upper), int(upper.shape[3])
+    a.lower_len, a.upper_len, a.pos, a.rope_freq = (_lib.ptr(lower_len), _lib.ptr(upper_len), _lib.ptr(pos),
+                                                     _lib.ptr(freq))
+    a.w_qkv, a.w_o = _lib.ptr(w_qkv_table), _lib.ptr(w_o_table)
+    a.emb_packed, a.emb = _lib.ptr(emb_packed), _lib.ptr(emb)
+    a.tokens, a.tokens_log, a.log_stride = _lib.ptr(tokens), _lib.ptr(tokens_log), int(log_stride)
+    a.workspace, a.workspace_bytes = _lib.ptr(ws), ws.numel()
+    return a
+
+
+def decode_step(args, stream=None) -> None:
+    """One persistent launch of the whole decode token step (rk_decode_step)."""
+    import ctypes
+    _lib.call("rk_decode_step", ctypes.addressof(args), _lib.stream_ptr(stream))
+
+
 def embed(tokens: torch.Tensor, emb: torch.Tensor, x: torch.Tensor, stream=None) -> None:
     """x (m, d_model) f32 = emb[tokens] (bf16 table)."""
     _lib.call("rk_embed", _lib.ptr(tokens), tokens.numel(), _lib.ptr(emb), emb.shape[1], _lib.ptr(x),
