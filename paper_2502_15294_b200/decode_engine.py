@@ -873,6 +873,8 @@ class GroupedDecoder:
         per = cfg.batch // groups
         sub = dataclasses.replace(cfg, batch=per,
                                   host_unique=max(1, cfg.host_unique // groups) if cfg.host_unique else 0)
+        if groups > 1 and cfg.step_kernel == "persistent":
+            raise ValueError("step_kernel='persistent' needs the GPU to itself (one CTA on every SM): use groups=1")
         if groups > 1 and cfg.step_kernel == "auto":
             # concurrent groups share the SMs: the persistent step needs one CTA on every SM
             sub = dataclasses.replace(sub, step_kernel="layers")

@@ -90,3 +90,14 @@ def test_activity_ledger_matches_oracle_and_reference(window, protect):
         import importlib
         rsel = importlib.import_module("roundkv.selection")
         assert ours == _ledger_runs(rsel.ActivityLedger, window, protect, R, seq)
+
+
+def test_step_kernel_config_validation():
+    """The answer-loop selector: unknown values are rejected before any
+    allocation, and the persistent whole-step kernel (one CTA on every SM) is
+    refused for concurrent groups."""
+    from paper_2502_15294_b200.decode_engine import EngineConfig, GroupedDecoder, RoundDecodeEngine
+    with pytest.raises(ValueError, match="step_kernel"):
+        RoundDecodeEngine(EngineConfig(batch=2, step_kernel="fused"), device="cpu")
+    with pytest.raises(ValueError, match="groups=1"):
+        GroupedDecoder(EngineConfig(batch=4, step_kernel="persistent"), groups=2, device="cpu")
