@@ -41,6 +41,7 @@
 // Counters are monotonic (targets = (epoch + 1) x count), so nothing is
 // reset between launches; every wait is bounded (trap, never a hang).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "decode_common.cuh"
@@ -137,7 +138,9 @@ __device__ __forceinline__ void watchdog(unsigned* hdr, unsigned code) {
   __threadfence();
   asm volatile("trap;");
 }
-constexpr long long kPatience = 4ll << 30;     // ~2 s of SM clocks
+// bounded waits: SM clocks before a wait traps (~2 s by default; RK_STEP_PATIENCE_S for
+// slowed-down runs such as compute-sanitizer)
+__device__ long long g_patience = 4ll << 30;
 
 __device__ __forceinline__ bool bar_try(uint64_t* bar, unsigned parity) {
   uint32_t ok;
@@ -151,10 +154,14 @@ __device__ __forceinline__ bool bar_try(uint64_t* bar, unsigned parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void bar_wait_b(uint64_t* bar, unsigned parity, unsigned* hdr, unsigned code) {
+#ifdef STP_PLAIN_WAIT      // sanitizer experiments: the unbounded wait loop of the other kernels
+  mbar_wait(bar, parity);
+  return;
+#endif
   if (bar_try(bar, parity)) return;
   const long long t0 = clock64();
   while (!bar_try(bar, parity))
-    if (clock64() - t0 > kPatience) watchdog(hdr, code);
+    if (clock64() - t0 > g_patience) watchdog(hdr, code);
 }
 // every consumer thread calls this: thread 0 polls, the rest wait at the barrier
 __device__ __forceinline__ void wait_count(const unsigned* c, unsigned target, unsigned* hdr, unsigned code) {
@@ -162,7 +169,7 @@ __device__ __forceinline__ void wait_count(const unsigned* c, unsigned target, u
     const long long t0 = clock64();
     while ((int)(ld_acquire(c) - target) < 0) {
       __nanosleep(32);
-      if (clock64() - t0 > kPatience) watchdog(hdr, code);
+      if (clock64() - t0 > g_patience) watchdog(hdr, code);
     }
   }
   consumer_sync();
@@ -887,6 +894,10 @@ template <int NT>
 static int launch_step(const stp::Params& p, const StepPlan& pl, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
+    if (const char* e = getenv("RK_STEP_PATIENCE_S")) {
+      const long long cycles = (long long)(atof(e) * 2.0e9);
+      if (cycles > 0) RK_CUDA(cudaMemcpyToSymbol(stp::g_patience, &cycles, sizeof(cycles)), "step patience");
+    }
     RK_CUDA(cudaFuncSetAttribute(stp::step_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem),
             "step smem attribute");
     attr_set = true;
