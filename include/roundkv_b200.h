@@ -366,6 +366,22 @@ int rk_lm_head_rows(const float* x, int m, int d_model, const void* emb_packed, 
                     float* x_next, int32_t* tokens, int32_t* pos, int32_t* tokens_log, int log_stride,
                     const int32_t* row_active, int log_pos_base, void* workspace, size_t workspace_bytes,
                     rk_stream_t stream);
+/* ---- the drop-in model's layer body (engine.Model: the reference's toy
+ * transformer, float32 weights [d_model][d_model] row-major, x @ W) ----
+ * rk_small_qkv_rope: q, k = RoPE(x W_q), RoPE(x W_k), v = x W_v for n rows
+ *   (engine.py:244-251; RoPE with float64 angles / trig, engine.py:175-185),
+ *   outputs [n][d_model] float32 (q as [n][heads][d_k]).
+ * rk_small_out_proj: x_out = x + a W_o (engine.py:267); x_out may not alias a.
+ * rk_small_logits: logits = x E^T ([n][vocab], nullable) and the first maximum
+ *   per row (engine.py:270-271, pipeline.py:308 np.argmax). d_model <= 4096. */
+int rk_small_qkv_rope(const float* x, int n, int d_model, const float* w_q, const float* w_k, const float* w_v,
+                      int heads, const int64_t* pos, const double* rope_freq, float* q_out, float* k_out,
+                      float* v_out, rk_stream_t stream);
+int rk_small_out_proj(const float* a, int n, int d_model, const float* w_o, const float* x, float* x_out,
+                      rk_stream_t stream);
+int rk_small_logits(const float* x, int n, int d_model, const float* emb, int vocab, float* logits,
+                    int32_t* argmax, rk_stream_t stream);
+
 /* ---- the whole decode token step in one persistent launch (small batches) ----
  * One answer token of every dialogue through all num_layers layers + the tied
  * logits and first-max argmax (reference engine.py:244-271 forward_range per

@@ -309,6 +309,41 @@ def lm_head(x: torch.Tensor, emb_packed: torch.Tensor, vocab: int, emb: torch.Te
               int(log_pos_base), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
 
 
+def small_qkv_rope(x: torch.Tensor, w_q: torch.Tensor, w_k: torch.Tensor, w_v: torch.Tensor, heads: int,
+                   positions: torch.Tensor, freq: torch.Tensor, stream=None):
+    """The drop-in model's q, k = RoPE(x W_q), RoPE(x W_k); v = x W_v (float32,
+    rk_small_qkv_rope): returns q (n, heads, d_k), k (n, d_model), v (n, d_model)."""
+    x = x.contiguous()
+    n, dm = x.shape
+    q = torch.empty((n, dm), dtype=torch.float32, device=x.device)
+    k = torch.empty_like(q)
+    v = torch.empty_like(q)
+    pos = positions.to(torch.int64).contiguous()
+    _lib.call("rk_small_qkv_rope", _lib.ptr(x), n, dm, _lib.ptr(w_q), _lib.ptr(w_k), _lib.ptr(w_v), heads,
+              _lib.ptr(pos), _lib.ptr(freq), _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.stream_ptr(stream))
+    return q.view(n, heads, dm // heads), k, v
+
+
+def small_out_proj(a: torch.Tensor, w_o: torch.Tensor, x: torch.Tensor, stream=None) -> torch.Tensor:
+    """x + a W_o (float32, rk_small_out_proj), a new tensor."""
+    a, x = a.contiguous(), x.contiguous()
+    out = torch.empty_like(x)
+    _lib.call("rk_small_out_proj", _lib.ptr(a), a.shape[0], a.shape[1], _lib.ptr(w_o), _lib.ptr(x), _lib.ptr(out),
+              _lib.stream_ptr(stream))
+    return out
+
+
+def small_logits(x: torch.Tensor, emb: torch.Tensor, want_logits: bool = True, stream=None):
+    """(logits = x E^T or None, first-max argmax per row) (float32, rk_small_logits)."""
+    x = x.contiguous()
+    n, dm = x.shape
+    logits = torch.empty((n, emb.shape[0]), dtype=torch.float32, device=x.device) if want_logits else None
+    am = torch.empty(n, dtype=torch.int32, device=x.device)
+    _lib.call("rk_small_logits", _lib.ptr(x), n, dm, _lib.ptr(emb), emb.shape[0], _lib.ptr(logits), _lib.ptr(am),
+              _lib.stream_ptr(stream))
+    return logits, am
+
+
 def decode_step_supported(batch: int, hq: int, hkv: int, head_dim: int, kv_dtype=torch.bfloat16) -> bool:
     """Whether rk_decode_step (the persistent whole-step kernel) covers this shape."""
     code = {torch.bfloat16: _lib.RK_BF16, torch.float32: _lib.RK_F32}.get(kv_dtype, -1)

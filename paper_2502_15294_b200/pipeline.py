@@ -233,7 +233,7 @@ class RoundPipeline:
         while True:
             answer_ids.append(cur)
             hid, _ = model.forward_range(working, 0, L, tokens=[cur], positions=[pos], allowed_fn=allowed_fn)
-            nxt = int(torch.argmax(model.logits(hid)[0]))
+            nxt = model.greedy(hid) if hasattr(model, "greedy") else int(torch.argmax(model.logits(hid)[0]))
             if nxt == EOT_TOKEN or generated >= max_decode_steps:
                 break
             cur, pos, generated = nxt, pos + 1, generated + 1
@@ -275,17 +275,15 @@ class RoundPipeline:
     def _forward_capture_q(self, working, l, tokens, hidden, positions):
         """Layer l (= Lw-1) of the question prefill, returning the hidden state
         after the layer and the layer's rotated queries (the scorer's input)."""
-        model, c = self.model, self.model.config
+        model = self.model
         if tokens is not None:
             x = model.embed_tokens(tokens)
         else:
             x = hidden
-        pos = torch.as_tensor(positions, device=model.device)
-        n = x.shape[0]
-        H, dk = c.num_heads, c.d_k
-        q = model._rope((x @ model.w_q[l]).view(n, H, dk), pos)
-        out, _ = model.forward_range(working, l, l + 1, hidden=x, positions=positions)
-        return out, q
+        seen = {}
+        out, _ = model.forward_range(working, l, l + 1, hidden=x, positions=positions,
+                                     layer_hook=lambda _l, q, _kv: seen.setdefault("q", q))
+        return out, seen["q"]
 
     def run_conversation(self, questions, max_decode_steps: int = 16) -> list:
         return [self.run_turn(q, max_decode_steps) for q in questions]
