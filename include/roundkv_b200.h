@@ -381,6 +381,12 @@ int rk_small_out_proj(const float* a, int n, int d_model, const float* w_o, cons
                       rk_stream_t stream);
 int rk_small_logits(const float* x, int n, int d_model, const float* emb, int vocab, float* logits,
                     int32_t* argmax, rk_stream_t stream);
+/* capture_mode="pre" capture matrix (engine.py:187-200): out[i][j] = softmax_j over the
+ * visible keys (k_pos[j] <= q_pos[i], allowed[j] when given) of
+ * sum_h q[i][h] . k[j][h] / (heads sqrt(d_k)), float64; q [n][heads][d_k], k [s][heads][d_k]
+ * float32; a row without a visible key is NaN (as the reference). */
+int rk_capture_pre(const float* q, int n, int heads, int d_k, const float* k, int s, const int64_t* q_pos,
+                   const int64_t* k_pos, const uint8_t* allowed, double* out, rk_stream_t stream);
 
 /* ---- the whole decode token step in one persistent launch (small batches) ----
  * One answer token of every dialogue through all num_layers layers + the tied

@@ -73,6 +73,7 @@ _SIGS = {
     "rk_small_qkv_rope": (_i, [_p, _i, _i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p]),
     "rk_small_out_proj": (_i, [_p, _i, _i, _p, _p, _p, _p]),
     "rk_small_logits": (_i, [_p, _i, _i, _p, _i, _p, _p, _p]),
+    "rk_capture_pre": (_i, [_p, _i, _i, _i, _p, _i, _p, _p, _p, _p, _p]),
     "rk_decode_step_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i]),
     "rk_decode_step_supported": (_i, [_i, _i, _i, _i, _i]),
     "rk_decode_step": (_i, [_p, _p]),

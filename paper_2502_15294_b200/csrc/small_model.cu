@@ -5,6 +5,7 @@
 //                         (engine.py:244-251; RoPE in float64, engine.py:175-185)
 //   rk_small_out_proj     x_out = x + a W_o                 (engine.py:267)
 //   rk_small_logits       logits = x E^T, first-max argmax  (engine.py:270-271, pipeline.py:308)
+//   rk_capture_pre        the capture_mode="pre" score matrix (engine.py:187-200), float64
 // These shapes are tiny (the batched engine's tcgen05 projections, proj.cu,
 // serve the large bf16 models): one CTA per (row, column block), the row of x
 // in shared memory, one output column per thread, coalesced weight reads
@@ -118,6 +119,56 @@ __global__ void __launch_bounds__(kThreads) small_logits_kernel(const float* __r
   }
 }
 
+// capture_mode="pre" (engine.py:187-200): one float64 softmax per query row over
+// the head-summed logits sum_h q_h . k_h / (H sqrt(d_k)) of the visible keys
+// (k_pos <= q_pos, allowed); products of the float32 inputs are exact in float64.
+// Row with no visible key: NaN (the reference's -inf - -inf).
+__global__ void __launch_bounds__(kThreads) capture_pre_kernel(
+    const float* __restrict__ q, int hd, const float* __restrict__ k, int s, const int64_t* __restrict__ q_pos,
+    const int64_t* __restrict__ k_pos, const uint8_t* __restrict__ allowed, double denom, double* __restrict__ out) {
+  extern __shared__ double qs[];
+  __shared__ double red[kThreads / 32];
+  const int row = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < hd; e += kThreads) qs[e] = (double)q[(size_t)row * hd + e];
+  __syncthreads();
+  const int64_t qp = q_pos[row];
+  double* o = out + (size_t)row * s;
+  double m = -INFINITY;
+  for (int j = threadIdx.x; j < s; j += kThreads) {
+    double v = -INFINITY;
+    if (k_pos[j] <= qp && (allowed == nullptr || allowed[j])) {
+      const float* kr = k + (size_t)j * hd;
+      double acc = 0.0;
+      for (int e = 0; e < hd; ++e) acc = fma(qs[e], (double)kr[e], acc);
+      v = acc / denom;
+    }
+    o[j] = v;
+    m = fmax(m, v);
+  }
+  auto block_reduce = [&](double v, bool is_max) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, v, off);
+      v = is_max ? fmax(v, w) : v + w;
+    }
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int w = 1; w < kThreads / 32; ++w) r = is_max ? fmax(r, red[w]) : r + red[w];
+    return r;
+  };
+  const double M = block_reduce(m, true);
+  double sum = 0.0;
+  for (int j = threadIdx.x; j < s; j += kThreads) {
+    const double e = M == -INFINITY ? NAN : exp(o[j] - M);
+    o[j] = e;
+    sum += e;
+  }
+  const double S = block_reduce(sum, false);
+  for (int j = threadIdx.x; j < s; j += kThreads) o[j] = o[j] / S;
+}
+
 }  // namespace sm
 }  // namespace rk
 
@@ -157,6 +208,18 @@ int rk_small_logits(const float* x, int n, int d_model, const float* emb, int vo
   sm::small_logits_kernel<<<n, sm::kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, d_model, emb, vocab,
                                                                                          logits, argmax);
   RK_CHECK_LAUNCH("small_logits_kernel");
+  return RK_OK;
+}
+
+int rk_capture_pre(const float* q, int n, int heads, int d_k, const float* k, int s, const int64_t* q_pos,
+                   const int64_t* k_pos, const uint8_t* allowed, double* out, rk_stream_t stream) {
+  if (n <= 0 || s <= 0) return RK_OK;
+  const int hd = heads * d_k;
+  if (heads <= 0 || d_k <= 0 || hd > 6144) return fail(RK_ERR_DOMAIN, "capture_pre: heads %d x d_k %d", heads, d_k);
+  const double denom = (double)heads * sqrt((double)d_k);
+  sm::capture_pre_kernel<<<n, sm::kThreads, sizeof(double) * hd, reinterpret_cast<cudaStream_t>(stream)>>>(
+      q, hd, k, s, q_pos, k_pos, allowed, denom, out);
+  RK_CHECK_LAUNCH("capture_pre_kernel");
   return RK_OK;
 }
 

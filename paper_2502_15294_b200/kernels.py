@@ -344,6 +344,23 @@ def small_logits(x: torch.Tensor, emb: torch.Tensor, want_logits: bool = True, s
     return logits, am
 
 
+def capture_pre(q: torch.Tensor, k: torch.Tensor, q_pos: torch.Tensor, k_pos: torch.Tensor,
+                allowed: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """capture_mode="pre" score matrix (rk_capture_pre): q (n, H, d_k), k (s, H*d_k)
+    float32 -> (n, s) float64 softmax of the head-summed logits / (H sqrt(d_k))."""
+    q = q.contiguous().to(torch.float32)
+    n, heads, dk = q.shape
+    k = k.contiguous().to(torch.float32)
+    s = k.shape[0]
+    out = torch.empty((n, s), dtype=torch.float64, device=q.device)
+    qp = q_pos.to(device=q.device, dtype=torch.int64).contiguous()
+    kp = k_pos.to(device=q.device, dtype=torch.int64).contiguous()
+    al = None if allowed is None else allowed.to(device=q.device, dtype=torch.uint8).contiguous()
+    _lib.call("rk_capture_pre", _lib.ptr(q), n, heads, dk, _lib.ptr(k), s, _lib.ptr(qp), _lib.ptr(kp), _lib.ptr(al),
+              _lib.ptr(out), _lib.stream_ptr(stream))
+    return out
+
+
 def decode_step_supported(batch: int, hq: int, hkv: int, head_dim: int, kv_dtype=torch.bfloat16) -> bool:
     """Whether rk_decode_step (the persistent whole-step kernel) covers this shape."""
     code = {torch.bfloat16: _lib.RK_BF16, torch.float32: _lib.RK_F32}.get(kv_dtype, -1)

@@ -62,3 +62,33 @@ def test_small_logits_first_max(n, dm, vocab):
     lg = logits.cpu().numpy()
     np.testing.assert_array_equal(got, np.argmax(lg, axis=1))   # np.argmax: the first maximum
     assert got[0] == vocab // 3
+
+
+@pytest.mark.parametrize("n,s,heads,dk,masked", [(5, 40, 4, 8, False), (3, 300, 4, 16, True), (2, 1000, 8, 64, True)])
+def test_capture_pre_matches_float64(n, s, heads, dk, masked):
+    """capture_mode="pre" (engine.py:187-200): softmax over the visible keys of the
+    head-summed logits / (H sqrt(d_k)), float64; a row with no visible key is NaN."""
+    rng = np.random.default_rng(s + n)
+    q = rng.standard_normal((n, heads, dk)).astype(np.float32)
+    k = rng.standard_normal((s, heads * dk)).astype(np.float32)
+    q_pos = np.sort(rng.integers(s // 2, s, size=n)).astype(np.int64)
+    q_pos[0] = -1 if masked else q_pos[0]                      # row 0 sees nothing when masked
+    k_pos = np.arange(s, dtype=np.int64)
+    allowed = (rng.random(s) > 0.3) if masked else None
+    got = kernels.capture_pre(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(q_pos),
+                              torch.from_numpy(k_pos),
+                              None if allowed is None else torch.from_numpy(allowed)).cpu().numpy()
+    logits = np.einsum("nhd,shd->ns", q.astype(np.float64), k.reshape(s, heads, dk).astype(np.float64))
+    logits /= heads * np.sqrt(dk)
+    vis = k_pos[None, :] <= q_pos[:, None]
+    if allowed is not None:
+        vis &= allowed[None, :]
+    with np.errstate(invalid="ignore"):
+        logits = np.where(vis, logits, -np.inf)
+        logits -= logits.max(axis=1, keepdims=True)
+        w = np.exp(logits)
+        ref = w / w.sum(axis=1, keepdims=True)
+    if masked:
+        assert np.isnan(got[0]).all() and np.isnan(ref[0]).all()
+        got, ref = got[1:], ref[1:]
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15)
