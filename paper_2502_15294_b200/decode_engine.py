@@ -118,12 +118,35 @@ class RoundDecodeEngine:
         return dict(K=K, s_lo=R * T + turn_rows, s_up=K * T + turn_rows)
 
     def __init__(self, cfg: EngineConfig, device: str = "cuda", model: DecodeModel | None = None,
-                 dialogues=None, seed: int | None = None, shared: dict | None = None):
+                 dialogues=None, seed: int | None = None, shared: dict | None = None,
+                 head_shard: tuple[int, int] = (0, 1), all_reduce=None):
         """shared (cohort serving, cohort.py): views of a larger batch's caches and
         length arrays ('lower', 'upper', 'lower_len', 'upper_len') this engine's
-        dialogues live in, so one decode loop can serve several engines' rows."""
+        dialogues live in, so one decode loop can serve several engines' rows.
+
+        head_shard = (rank, world): KV-head sharding of every dialogue over `world`
+        ranks (the option for fewer dialogues than GPUs): this engine
+        holds kv-heads [rank hkv/world, (rank+1) hkv/world) of every layer (caches,
+        host rounds, projections' columns, W_o's rows) and exchanges two things
+        through `all_reduce(tensor)` (in-place sum over the ranks, e.g.
+        torch.distributed.all_reduce): each layer's output-projection partial
+        (B x d_model f32) and, before selection, the per-round fp64 masses of its
+        heads — so every rank keeps the same rounds and the same residual stream."""
         self.cfg = c = cfg
         self.dev = torch.device(device)
+        self.shard_rank, self.shard_world = head_shard
+        if self.shard_world > 1:
+            if all_reduce is None:
+                raise ValueError("head sharding needs an all_reduce")
+            if c.hkv % self.shard_world:
+                raise ValueError(f"{c.hkv} kv-heads do not split over {self.shard_world} ranks")
+            if c.question_rows > 1 or c.capture_mode != "post" or shared is not None:
+                raise ValueError("head sharding serves 1-row questions, capture_mode='post', no cohorts")
+            if c.step_kernel == "persistent":
+                raise ValueError("head sharding runs the layered answer loop")
+        self.all_reduce = all_reduce
+        self.hq_l, self.hkv_l = c.hq // self.shard_world, c.hkv // self.shard_world
+        self.h0 = self.shard_rank * self.hkv_l              # first kv-head of this shard
         if c.policy.kind not in ("top_percent", "fixed", "adaptive", "all"):
             raise ValueError(f"policy {c.policy.kind!r} is not a round-selection strategy")
         if c.capture_mode not in ("post", "pre"):
@@ -144,9 +167,12 @@ class RoundDecodeEngine:
         if len(self.dialogues) != B:
             raise ValueError(f"{len(self.dialogues)} dialogue ids for batch {B}")
         self.model = model if model is not None else DecodeModel(c.shape, self.dev, seed=c.model_seed,
-                                                                 prefill_gemm=c.question_rows > 1)
+                                                                 prefill_gemm=c.question_rows > 1,
+                                                                 shard=head_shard)
         if self.model.shape != c.shape:
             raise ValueError("model shape does not match the engine config")
+        if getattr(self.model, "shard", (0, 1)) != tuple(head_shard):
+            raise ValueError(f"model shard {self.model.shard} != engine head_shard {head_shard}")
         self.L_up = L - lw
         # K = the working cache's round slots.  top_percent keeps the same number of
         # rounds every turn (uniform K); fixed / adaptive thresholds and the drop
@@ -174,23 +200,25 @@ class RoundDecodeEngine:
         self.turn_tokens = 1 + c.decode_steps if nq == 1 else c.decode_steps
         self.s_lo = self.hist + self.turn_rows
         self.s_up = self.K * T + self.turn_rows
-        self.row = c.hkv * c.head_dim                         # elements per key (all heads)
-        D = c.hq * c.head_dim
+        hq_l, hkv_l = self.hq_l, self.hkv_l
+        hs = slice(self.h0, self.h0 + hkv_l)                  # this shard's kv-heads of a full-width draw
+        self.row = hkv_l * c.head_dim                         # elements per key (this shard's heads)
+        D = c.hq * c.head_dim                                 # d_model
 
         # ---- HBM tiers (per-dialogue synthetic history, seeded by the global dialogue id)
         if shared is not None:
             self.lower, self.upper = shared["lower"], shared["upper"]
-            if (tuple(self.lower.shape) != (B, lw, 2, self.s_lo, c.hkv, c.head_dim)
-                    or tuple(self.upper.shape) != (B, self.L_up, 2, self.s_up, c.hkv, c.head_dim)):
+            if (tuple(self.lower.shape) != (B, lw, 2, self.s_lo, hkv_l, c.head_dim)
+                    or tuple(self.upper.shape) != (B, self.L_up, 2, self.s_up, hkv_l, c.head_dim)):
                 raise ValueError("shared caches do not match the engine shape")
         else:
-            self.lower = torch.empty((B, lw, 2, self.s_lo, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
-            self.upper = torch.zeros((B, self.L_up, 2, self.s_up, c.hkv, c.head_dim), dtype=self.dtype,
+            self.lower = torch.empty((B, lw, 2, self.s_lo, hkv_l, c.head_dim), dtype=self.dtype, device=self.dev)
+            self.upper = torch.zeros((B, self.L_up, 2, self.s_up, hkv_l, c.head_dim), dtype=self.dtype,
                                      device=self.dev)
         for b, gid in enumerate(self.dialogues):
             g = _dialogue_gen(self.dev, gid, 1)
             self.lower[b, :, :, : self.hist] = torch.randn((lw, 2, self.hist, c.hkv, c.head_dim), generator=g,
-                                                           device=self.dev).to(self.dtype)
+                                                           device=self.dev)[..., hs, :].to(self.dtype)
         # ---- upper tier: one contiguous upper block per (dialogue set, round), in pinned host
         # memory (the reference's host tier) or in a GPU's HBM (the peer-HBM tier)
         if c.upper_tier not in ("host", "hbm"):
@@ -211,17 +239,19 @@ class RoundDecodeEngine:
             offs = np.random.default_rng(gid + 17).integers(0, 1 << 23, size=R)
             blocks = []
             for r in range(R):
-                blk = torch.empty((self.L_up, 2, T, c.hkv, c.head_dim), dtype=self.dtype, pin_memory=True)
-                flat = blk.view(-1)
+                full = torch.empty((self.L_up, 2, T, c.hkv, c.head_dim), dtype=self.dtype,
+                                   pin_memory=self.shard_world == 1)
+                flat = full.view(-1)
                 o = int(offs[r])
                 for s0 in range(0, flat.numel(), 1 << 23):       # distinct window of the pool per block
                     n = min(1 << 23, flat.numel() - s0)
                     flat[s0:s0 + n].copy_(pool[o:o + n])
+                blk = full if self.shard_world == 1 else full[..., hs, :].contiguous().pin_memory()
                 if tier_dev is not None:
                     blk = blk.to(tier_dev)
                 blocks.append(blk)
             self.host_blocks.append(blocks)
-        wb_shape = (B, self.L_up, 2, self.turn_rows, c.hkv, c.head_dim)
+        wb_shape = (B, self.L_up, 2, self.turn_rows, hkv_l, c.head_dim)
         self.writeback = (torch.empty(wb_shape, dtype=self.dtype, pin_memory=True) if tier_dev is None
                           else torch.empty(wb_shape, dtype=self.dtype, device=tier_dev))    # the new round's tier
 
@@ -244,10 +274,12 @@ class RoundDecodeEngine:
 
         # ---- activations (one decode row per dialogue)
         self.x = torch.zeros((B, D), dtype=torch.float32, device=self.dev)          # residual stream
-        self.q_buf = torch.zeros((B, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
-        self.k_new = torch.zeros((B, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
-        self.v_new = torch.zeros((B, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
-        self.attn = torch.zeros((B, D), dtype=torch.float32, device=self.dev)       # attention output
+        self.q_buf = torch.zeros((B, hq_l, c.head_dim), dtype=torch.float32, device=self.dev)
+        self.k_new = torch.zeros((B, hkv_l, c.head_dim), dtype=self.dtype, device=self.dev)
+        self.v_new = torch.zeros((B, hkv_l, c.head_dim), dtype=self.dtype, device=self.dev)
+        self.attn = torch.zeros((B, hq_l * c.head_dim), dtype=torch.float32, device=self.dev)   # attention output
+        # head sharding: this shard's output-projection partial, summed over the ranks
+        self.delta = torch.zeros((B, D), dtype=torch.float32, device=self.dev) if self.shard_world > 1 else None
         self.tokens = torch.zeros(B, dtype=torch.int32, device=self.dev)
         self.sep = torch.full((B,), SEP_TOKEN, dtype=torch.int32, device=self.dev)
         # answer ids of the turn: [SEP, generated...] (the last entry is the argmax after the final forward)
@@ -259,8 +291,8 @@ class RoundDecodeEngine:
         self.proj_ws = kernels.proj_workspace(B, D, max(self.model.shape.qkv_width, D), self.dev)
         if nq > 1:
             self.xq = torch.zeros((B * nq, D), dtype=torch.float32, device=self.dev)
-            self.qq = torch.zeros((B * nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
-            self.qout = torch.zeros((B, nq, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
+            self.qq = torch.zeros((B * nq, hq_l, c.head_dim), dtype=torch.float32, device=self.dev)
+            self.qout = torch.zeros((B, nq, hq_l, c.head_dim), dtype=torch.float32, device=self.dev)
             self.q_pos = torch.arange(self.hist, self.hist + nq, dtype=torch.int64, device=self.dev)
             self.pos_rows = torch.arange(self.hist, self.hist + nq, dtype=torch.int32,
                                          device=self.dev).repeat(B).contiguous()
@@ -290,9 +322,9 @@ class RoundDecodeEngine:
         self.active_host = torch.ones((B, R), dtype=torch.uint8, pin_memory=True)
         self.active_dev = torch.ones((B, R), dtype=torch.uint8, device=self.dev)
         self.sel_out = None
-        ws_bytes = _lib.lib.rk_decode_workspace_bytes(B, c.hq, c.hkv, c.head_dim, max(592, self.items.shape[1] * 8))
+        ws_bytes = _lib.lib.rk_decode_workspace_bytes(B, hq_l, hkv_l, c.head_dim, max(592, self.items.shape[1] * 8))
         self.ws = torch.zeros(max(256, int(ws_bytes)), dtype=torch.uint8, device=self.dev)
-        ex_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, nq, c.hq, self.items.shape[1], R)
+        ex_bytes = _lib.lib.rk_round_scores_exact_workspace_bytes(B, nq, hq_l, self.items.shape[1], R)
         self.ws_exact = torch.zeros(max(256, int(ex_bytes)), dtype=torch.uint8, device=self.dev)
         self.q_pos_1 = torch.full((1,), self.hist, dtype=torch.int64, device=self.dev)
         self.margin = torch.zeros(B, dtype=torch.float64, device=self.dev)
@@ -317,7 +349,7 @@ class RoundDecodeEngine:
         self.graph_a = None
         self.graph_b = None
         # ---- the persistent whole-step kernel (rk_decode_step) for the answer loop
-        supported = kernels.decode_step_supported(B, c.hq, c.hkv, c.head_dim, self.dtype)
+        supported = self.shard_world == 1 and kernels.decode_step_supported(B, c.hq, c.hkv, c.head_dim, self.dtype)
         if c.step_kernel == "persistent" and not supported:
             raise ValueError("step_kernel='persistent' needs batch <= 16, group <= 8, head_dim 128 and bf16 KV")
         self.persistent = supported and c.step_kernel in ("auto", "persistent")
@@ -348,12 +380,12 @@ class RoundDecodeEngine:
         m = self.model
         tok = self.q_tok_all[0, :, -1].long()                            # (B,) last question token
         x = m.emb[tok].float().contiguous()
-        q = torch.zeros((c.batch, c.hq, c.head_dim), dtype=torch.float32, device=self.dev)
-        kd = torch.zeros((c.batch, c.hkv, c.head_dim), dtype=self.dtype, device=self.dev)
+        q = torch.zeros((c.batch, self.hq_l, c.head_dim), dtype=torch.float32, device=self.dev)
+        kd = torch.zeros((c.batch, self.hkv_l, c.head_dim), dtype=self.dtype, device=self.dev)
         vd = torch.zeros_like(kd)
         pos = torch.full((c.batch,), self.hist + self.nq - 1, dtype=torch.int32, device=self.dev)
-        kernels.qkv_rope(x, m.w_qkv_packed[lw1], c.hq, c.hkv, c.head_dim, pos, m.freq, q, kd, vd)
-        qm = q.view(c.batch, c.hkv, c.group, c.head_dim).mean(dim=2)
+        kernels.qkv_rope(x, m.w_qkv_packed[lw1], self.hq_l, self.hkv_l, c.head_dim, pos, m.freq, q, kd, vd)
+        qm = q.view(c.batch, self.hkv_l, c.group, c.head_dim).mean(dim=2)
         u = qm / qm.norm(dim=-1, keepdim=True)
         self.planted = []
         for b, gid in enumerate(self.dialogues):
@@ -379,17 +411,24 @@ class RoundDecodeEngine:
         (rk_decode_attention), output projection + residual (rk_out_proj)."""
         c, m = self.cfg, self.model
         kc, vc, ln, cap = self._caches(l)
-        kernels.qkv_rope(self.x, m.w_qkv_packed[l], c.hq, c.hkv, c.head_dim, self.pos, m.freq, self.q_buf,
+        kernels.qkv_rope(self.x, m.w_qkv_packed[l], self.hq_l, self.hkv_l, c.head_dim, self.pos, m.freq, self.q_buf,
                          self.k_new, self.v_new, ws=self.proj_ws)
         kernels.decode_attention(self.q_buf, kc, vc, ln, cap, k_new=self.k_new, v_new=self.v_new,
-                                 out=self.attn.view(c.batch, c.hq, c.head_dim), ws=self.ws,
+                                 out=self.attn.view(c.batch, self.hq_l, c.head_dim), ws=self.ws,
                                  advance=ln if advance else None)
-        kernels.out_proj(self.attn, m.w_o_packed[l], self.x, ws=self.proj_ws)
+        if self.shard_world > 1:
+            # row-parallel W_o: this shard's heads' contribution, summed over the ranks
+            self.delta.zero_()
+            kernels.out_proj(self.attn, m.w_o_packed[l], self.delta, ws=self.proj_ws)
+            self.all_reduce(self.delta)
+            self.x += self.delta
+        else:
+            kernels.out_proj(self.attn, m.w_o_packed[l], self.x, ws=self.proj_ws)
 
     def _attn_launches(self, l: int, advance: bool = False) -> int:
         c = self.cfg
         kc, _, _, cap = self._caches(l)
-        plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0), False)
+        plan = kernels.decode_plan(c.batch, self.hq_l, self.hkv_l, c.head_dim, kc.dtype, cap, kc.stride(0), False)
         return (1 + int(advance)) if plan > 0 else 2
 
     def decode_kernel_desc(self) -> str:
@@ -399,7 +438,7 @@ class RoundDecodeEngine:
             return "step_kernel (one persistent launch per token: every layer's projections, attention, merge)"
         out = []
         for name, kc, cap in (("lower", self.lower[:, 0, 0], self.s_lo), ("upper", self.upper[:, 0, 0], self.s_up)):
-            plan = kernels.decode_plan(c.batch, c.hq, c.hkv, c.head_dim, kc.dtype, cap, kc.stride(0))
+            plan = kernels.decode_plan(c.batch, self.hq_l, self.hkv_l, c.head_dim, kc.dtype, cap, kc.stride(0))
             out.append(f"{name}: " + (f"decode_cluster_kernel, {plan} CTA(s) per (dialogue, kv-head)" if plan > 0
                                       else "decode_mma_kernel + decode_merge_kernel"))
         return "; ".join(out)
@@ -437,6 +476,8 @@ class RoundDecodeEngine:
         kernels.round_scores_exact(self.q_buf.unsqueeze(1), self.lower[:, lw1, 0], self.q_pos_1, self.items,
                                    c.rounds, seq_len=self.lower_len, n_items=self.n_items, raw=self.raw,
                                    ws=self.ws_exact, capture_mode=c.capture_mode)
+        if self.shard_world > 1:
+            self.all_reduce(self.raw)      # Eq. 1 sums over heads: every rank selects from the same masses
         self._select()
 
     def _select(self):

@@ -54,10 +54,23 @@ class DecodeModel:
     row-major for the multi-row question prefill's library GEMMs."""
 
     def __init__(self, shape: ModelShape, device="cuda", seed: int = 42, weights: dict | None = None,
-                 prefill_gemm: bool = False):
+                 prefill_gemm: bool = False, shard: tuple[int, int] = (0, 1)):
+        """shard = (rank, world): KV-head sharding of every dialogue over `world`
+        ranks (SURVEY §8e's option for fewer dialogues than GPUs).  The same
+        seeded weights are drawn; this rank keeps the columns of W_q / W_k / W_v
+        of its query heads [rank hq/world, ...) and kv-heads [rank hkv/world, ...)
+        and the matching rows of W_o (a row-parallel output projection whose
+        partial sums the engine all-reduces); the tied embedding stays whole."""
         self.shape = s = shape
         self.device = dev = torch.device(device)
         D, L = s.d_model, s.num_layers
+        rank, world = shard
+        if world < 1 or not 0 <= rank < world or s.hkv % world:
+            raise ValueError(f"shard {shard}: kv-heads {s.hkv} must split evenly over the ranks")
+        self.shard = (rank, world)
+        self.hq_local, self.hkv_local = s.hq // world, s.hkv // world
+        qs = slice(rank * self.hq_local * s.head_dim, (rank + 1) * self.hq_local * s.head_dim)
+        ks = slice(rank * self.hkv_local * s.head_dim, (rank + 1) * self.hkv_local * s.head_dim)
         self.freq = torch.from_numpy(rope_freq(s.head_dim, s.rope_theta)).to(dev)
         self.w_qkv_packed, self.w_o_packed = [], []
         self.w_qkv_kn, self.w_o_kn = [], []
@@ -78,8 +91,8 @@ class DecodeModel:
             else:
                 wq, wk, wv, wo = (torch.as_tensor(weights[n][l], dtype=torch.float32).to(dev)
                                   for n in ("wq", "wk", "wv", "wo"))
-            wqkv = torch.cat([wq, wk, wv], dim=1).to(torch.bfloat16).contiguous()    # (D, (hq+2hkv) d)
-            wo16 = wo.to(torch.bfloat16).contiguous()
+            wqkv = torch.cat([wq[:, qs], wk[:, ks], wv[:, ks]], dim=1).to(torch.bfloat16).contiguous()
+            wo16 = wo[qs].to(torch.bfloat16).contiguous()               # (hq_local d, D)
             self.w_qkv_packed.append(kernels.pack_weight(wqkv))
             self.w_o_packed.append(kernels.pack_weight(wo16))
             if prefill_gemm:
@@ -93,11 +106,15 @@ class DecodeModel:
         and W_o of every layer + the tied embedding; the 128-row padding of the
         stored logits operand is not counted)."""
         s = self.shape
-        return 2 * (s.num_layers * (s.d_model * s.qkv_width + s.d_model * s.d_model) + s.vocab * s.d_model)
+        qkv_w = (self.hq_local + 2 * self.hkv_local) * s.head_dim
+        o_rows = self.hq_local * s.head_dim
+        return 2 * (s.num_layers * (s.d_model * qkv_w + o_rows * s.d_model) + s.vocab * s.d_model)
 
     def host_weights(self) -> dict:
         """The bf16 weights as float32 NumPy (for the oracle)."""
         s = self.shape
+        if self.shard[1] > 1:
+            raise ValueError("host_weights of a head-sharded model: use the unsharded model")
         qd, kd = s.hq * s.head_dim, s.hkv * s.head_dim
         out = {"emb": self.emb.float().cpu().numpy(), "wq": [], "wk": [], "wv": [], "wo": []}
         if not self.w_qkv_kn:
