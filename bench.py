@@ -83,6 +83,9 @@ def parse():
                     help="groups: independent dialogue groups, each with its own decode loop; cohorts: two "
                          "phase-offset cohorts sharing one row-masked decode loop (weights read once per step)")
     ap.add_argument("--cohorts", type=int, default=2, help="cohorts sharing the decode loop (--serving cohorts)")
+    ap.add_argument("--step-kernel", default="layers", choices=["layers", "persistent"],
+                    help="answer loop: per-layer kernels, or one persistent rk_decode_step launch per token "
+                         "(batch <= 16 per group, one group; DESIGN 3.2: measured slower)")
     ap.add_argument("--groups", type=int, default=None,
                     help="dialogue groups in flight per GPU (default: 2 when batch >= 2)")
     return ap.parse_args()
@@ -238,6 +241,7 @@ def main():
         w["host_unique"] = args.host_unique
     w["kv_dtype"] = args.kv_dtype
     w["upper_tier"] = args.upper_tier
+    w["step_kernel"] = args.step_kernel
     cfg = EngineConfig(**w)
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
@@ -248,8 +252,8 @@ def main():
     # dialogue-turn): two groups 1.30 K vs 0.98 K
     default_groups = {"c2": 2 if cfg.batch >= 32 else 1, "c3": 1, "c4": 2}[args.workload]
     groups = args.groups if args.groups else default_groups
-    if cfg.batch % groups:
-        groups = 1
+    if cfg.batch % groups or args.step_kernel == "persistent":
+        groups = 1                  # the persistent step holds one CTA on every SM
     if args.serving == "cohorts":
         from paper_2502_15294_b200.cohort import CohortDecoder
         groups = args.cohorts
@@ -322,7 +326,7 @@ def main():
     resident, full = eng.gpu_kv_bytes()
     traffic = None      # DRAM bytes per token-step from the committed ncu capture (same shapes)
     tp = REPO / "profiles" / "r02_traffic_c2_tokenstep.json"
-    if tp.exists() and args.workload == "c2" and args.kv_dtype == "bf16":
+    if tp.exists() and args.workload == "c2" and args.kv_dtype == "bf16" and args.step_kernel == "layers":
         t = json.loads(tp.read_text())
         if t.get("batch_per_group") == g0.cfg.batch:
             traffic = t["per_token_step_bytes_per_group"] * len(eng.groups)
@@ -360,8 +364,10 @@ def main():
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
-                     "kernel": f"decode step (per layer: rk_qkv_rope + rk decode attention [{eng.decode_kernel_desc()}]"
-                               " + rk_out_proj; rk_lm_head): KV + weight bytes of every timed decode token / union "
+                     "kernel": (f"decode step (per layer: rk_qkv_rope + rk decode attention [{eng.decode_kernel_desc()}]"
+                                " + rk_out_proj; rk_lm_head)" if args.step_kernel == "layers" else
+                                f"decode step ({eng.decode_kernel_desc()})")
+                               + ": KV + weight bytes of every timed decode token / union "
                                "of the groups' decode-loop intervals (CUDA events)",
                      "decode_busy_ms": dec_busy_ms, "launches": dec_launches,
                      "kv_GBps": dec_kv_bytes / (dec_busy_ms / 1000.0) / 1e9,
