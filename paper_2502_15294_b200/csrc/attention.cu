@@ -177,29 +177,62 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
                                   const uint8_t* __restrict__ active, double* __restrict__ out_rows) {
   extern __shared__ double sh[];
   double* mass = sh;                                   // [n_bins + 1]
-  double* Lh = mass + n_bins + 1;                      // [hq] fp64 denominators
+  double* Lh = mass + n_bins + 1;                      // [hq] fp64 1 / denominators
   float* Mh = reinterpret_cast<float*>(Lh + hq);       // [hq]
   int* bin_lo = reinterpret_cast<int*>(Mh + hq);       // [n_bins + 2]
-  const int row = blockIdx.x;
+  float* sm_m = reinterpret_cast<float*>(bin_lo + n_bins + 2);   // the row's [hq][nsplit] statistics
+  float* sm_l = sm_m + (size_t)hq * nsplit;
+  const int row = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int32_t* tab = items + (size_t)row * items_stride * 3;
-  int n_items = n_items_dev ? n_items_dev[items_stride ? row : 0] : n_items_static;
+  const int n_items = n_items_dev ? n_items_dev[items_stride ? row : 0] : n_items_static;
   const float* pm = part_m + (size_t)row * hq * nsplit;
   const float* pl = part_l + (size_t)row * hq * nsplit;
   const int n_slots = n_items * slots;
-  for (int h = threadIdx.x; h < hq; h += blockDim.x) {
-    float mx = -INFINITY;
-    for (int it = 0; it < n_slots; ++it) mx = fmaxf(mx, pm[h * nsplit + it]);
-    double L = 0.0;
-    for (int it = 0; it < n_slots; ++it)
-      L += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - mx);
-    Mh[h] = mx;
-    Lh[h] = L;
+  // the row's statistics into shared memory: up to 2 x 16 loads per thread in flight at once
+  constexpr int kU = 16;
+  const int n_stat = hq * nsplit;
+  for (int e0 = threadIdx.x; e0 < n_stat; e0 += kU * blockDim.x) {
+    float a[kU], b[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * blockDim.x;
+      a[u] = e < n_stat ? pm[e] : 0.f;
+      b[u] = e < n_stat ? pl[e] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < n_stat) {
+        sm_m[e] = a[u];
+        sm_l[e] = b[u];
+      }
+    }
   }
-  if (threadIdx.x == 0) {          // items are sorted by bin: first item of each bin
-    int it = 0;
-    for (int b = 0; b <= n_bins + 1; ++b) {
-      while (it < n_items && tab[it * 3 + 2] < b) ++it;
-      bin_lo[b] = it;
+  // first item of each bin (items are sorted by bin), one thread per item
+  if (n_items == 0) {
+    for (int b = threadIdx.x; b <= n_bins + 1; b += blockDim.x) bin_lo[b] = 0;
+  }
+  for (int it = threadIdx.x; it < n_items; it += blockDim.x) {
+    const int bin = tab[it * 3 + 2], prev = it > 0 ? tab[(it - 1) * 3 + 2] : -1;
+    for (int b = max(prev + 1, 0); b <= min(bin, n_bins + 1); ++b) bin_lo[b] = it;
+    if (it == n_items - 1)
+      for (int b = max(bin + 1, 0); b <= n_bins + 1; ++b) bin_lo[b] = n_items;
+  }
+  __syncthreads();
+  // per head: M_h = max over items, L_h = sum l exp2(m - M_h) (warp per head, fixed lane order)
+  for (int h = warp; h < hq; h += nw) {
+    float mx = -INFINITY;
+    for (int it = lane; it < n_slots; it += 32) mx = fmaxf(mx, sm_m[h * nsplit + it]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double L = 0.0;
+    for (int it = lane; it < n_slots; it += 32)
+      L += (double)sm_l[h * nsplit + it] * (double)exp2f(sm_m[h * nsplit + it] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) {
+      Mh[h] = mx;
+      Lh[h] = 1.0 / L;                         // the head's reciprocal denominator
     }
   }
   __syncthreads();
@@ -208,8 +241,8 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
     for (int h = 0; h < hq; ++h) {
       double hs = 0.0;
       for (int it = bin_lo[b] * slots; it < bin_lo[b + 1] * slots; ++it)
-        hs += (double)pl[h * nsplit + it] * (double)exp2f(pm[h * nsplit + it] - Mh[h]);
-      acc += hs / Lh[h];
+        hs += (double)sm_l[h * nsplit + it] * (double)exp2f(sm_m[h * nsplit + it] - Mh[h]);
+      acc += hs * Lh[h];
     }
     mass[b] = acc;
   }
@@ -217,31 +250,64 @@ __global__ void score_rows_kernel(const float* __restrict__ part_m, const float*
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int b = 0; b <= n_bins; ++b) tot += mass[b];
-    for (int b = 0; b < n_bins; ++b) {
-      bool on = active == nullptr || active[b];
-      out_rows[(size_t)row * n_bins + b] = on ? mass[b] / tot : 0.0;
-    }
+    mass[n_bins] = tot;                        // (the current round's own entry is not written out)
+  }
+  __syncthreads();
+  const double tot = mass[n_bins];
+  for (int b = threadIdx.x; b < n_bins; b += blockDim.x) {
+    const bool on = active == nullptr || active[b];
+    out_rows[(size_t)row * n_bins + b] = on ? mass[b] / tot : 0.0;
   }
 }
 
-// raw[a] over active bins (ascending) = sum over rows of massn[row][bin]
-__global__ void score_sum_rows_kernel(const double* __restrict__ rows_mass, int n_rows, int n_bins,
-                                      const uint8_t* __restrict__ active, double* __restrict__ raw) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n_bins) return;
-  if (active && !active[b]) return;
-  int a = b;
-  if (active) {
-    a = 0;
-    for (int x = 0; x < b; ++x) a += active[x] ? 1 : 0;
-  }
+// raw[a] over active bins (ascending) = sum over rows of massn[row][bin]: one block per bin,
+// a fixed-order tree over the rows (deterministic)
+constexpr int kSumThreads = 256;
+__global__ void __launch_bounds__(kSumThreads) score_sum_rows_kernel(const double* __restrict__ rows_mass,
+                                                                     int n_rows, int n_bins,
+                                                                     const uint8_t* __restrict__ active,
+                                                                     double* __restrict__ raw) {
+  __shared__ double red[kSumThreads];
+  const int b = blockIdx.x;
+  if (active && !active[b]) return;            // uniform over the block
+  int a = 0;                                   // this bin's rank among the active bins
+  if (active)
+    for (int x0 = 0; x0 < b; x0 += kSumThreads)
+      a += __syncthreads_count(x0 + (int)threadIdx.x < b && active[x0 + threadIdx.x]);
+  else
+    a = b;
   double acc = 0.0;
-  for (int r = 0; r < n_rows; ++r) acc += rows_mass[(size_t)r * n_bins + b];
-  raw[a] = acc;
+  for (int r = threadIdx.x; r < n_rows; r += kSumThreads) acc += rows_mass[(size_t)r * n_bins + b];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kSumThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) raw[a] = red[0];
 }
 
-static size_t score_rows_smem(int n_bins, int hq) {
-  return sizeof(double) * (n_bins + 1 + hq) + sizeof(float) * hq + sizeof(int) * (n_bins + 2);
+static size_t score_rows_smem(int n_bins, int hq, int nsplit) {
+  return sizeof(double) * (n_bins + 1 + hq) + sizeof(float) * hq + sizeof(int) * (n_bins + 2) +
+         2 * sizeof(float) * (size_t)hq * nsplit;
+}
+
+// launches score_rows_kernel with its shared memory (the row's statistics staged)
+static int launch_score_rows(int rows, const float* part_m, const float* part_l, int nsplit, int slots, int hq,
+                             const int32_t* items, int items_stride, const int32_t* n_items_dev, int n_items_static,
+                             int n_bins, const uint8_t* active, double* out_rows, cudaStream_t st) {
+  const size_t smem = score_rows_smem(n_bins, hq, nsplit);
+  if (smem > 227 * 1024) return fail(RK_ERR_CAPACITY, "score_rows: %zu bytes of statistics per row", smem);
+  static size_t attr = 48 * 1024;
+  if (smem > attr) {
+    RK_CUDA(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "score_rows smem attribute");
+    attr = smem;
+  }
+  score_rows_kernel<<<rows, 128, smem, st>>>(part_m, part_l, nsplit, slots, hq, items, items_stride, n_items_dev,
+                                             n_items_static, n_bins, active, out_rows);
+  RK_CHECK_LAUNCH("score_rows_kernel");
+  return RK_OK;
 }
 
 // the tensor-core multi-row path (prefill_tc.cu) serves bf16 K/V, d = 128,
@@ -503,6 +569,7 @@ int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int k
   double* rows_mass = reinterpret_cast<double*>(static_cast<char*>(workspace) + w.bytes);
   const float* part_m = w.part_m;
   const float* part_l = w.part_l;
+  int nsplit = n_items, slots = 1;                  // the tensor-core pass: 2 slots (column halves) per item
   if (use_tc(kv_dtype, d, n_q, hq / hkv)) {
     const size_t tc_bytes = prefill_plan(n_q, hq, hkv, s, n_items, true, false).total;
     if (need + tc_bytes > workspace_bytes)
@@ -513,6 +580,8 @@ int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int k
     if (st) return st;
     part_m = im;
     part_l = il;
+    nsplit = 2 * n_items;
+    slots = 2;
   } else {
   SplitParams p{};
   p.q = q; p.k = k; p.v = k;
@@ -528,10 +597,10 @@ int rk_round_scores(const float* q, int n_q, int hq, int d, const void* k, int k
   st = dispatch_split(kv_dtype, false, true, hq / hkv, sh, grid, cs, p);
   if (st) return st;
   }
-  score_rows_kernel<<<n_q, 128, score_rows_smem(n_bins, hq), cs>>>(
-      part_m, part_l, n_items, 1, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
-  RK_CHECK_LAUNCH("score_rows_kernel");
-  score_sum_rows_kernel<<<(n_bins + 127) / 128, 128, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
+  st = launch_score_rows(n_q, part_m, part_l, nsplit, slots, hq, items, 0, nullptr, n_items, n_bins, nullptr,
+                         rows_mass, cs);
+  if (st) return st;
+  score_sum_rows_kernel<<<n_bins, kSumThreads, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
   RK_CHECK_LAUNCH("score_sum_rows_kernel");
   return RK_OK;
 }
@@ -546,10 +615,8 @@ int rk_round_scores_finalize(int batch, int hq, int hkv, int d, int kv_dtype, in
   const int slots = bulk_supported(kv_dtype, d, hkv, hq / hkv) ? 8 / hkv : 1;
   const int nsplit = items_stride * slots;
   SplitWs w = carve(workspace, batch, hq, hkv, nsplit, d);
-  score_rows_kernel<<<batch, 128, score_rows_smem(n_bins, hq), reinterpret_cast<cudaStream_t>(stream)>>>(
-      w.part_m, w.part_l, nsplit, slots, hq, items, items_stride, n_items, 0, n_bins, active, raw_out);
-  RK_CHECK_LAUNCH("score_rows_kernel");
-  return RK_OK;
+  return launch_score_rows(batch, w.part_m, w.part_l, nsplit, slots, hq, items, items_stride, n_items, 0, n_bins,
+                           active, raw_out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 size_t rk_prefill_workspace_bytes(int n_q, int hq, int hkv, int s, int d, int n_items, int n_bins) {
@@ -590,10 +657,10 @@ int rk_prefill_attention(const float* q, int n_q, int hq, int d, const void* k, 
   if (st) return st;
   if (stats) {
     double* rows_mass = reinterpret_cast<double*>(static_cast<char*>(workspace) + pl.total);
-    score_rows_kernel<<<n_q, 128, score_rows_smem(n_bins, hq), cs>>>(
-        item_m, item_l, n_items, 1, hq, items, 0, nullptr, n_items, n_bins, nullptr, rows_mass);
-    RK_CHECK_LAUNCH("score_rows_kernel");
-    score_sum_rows_kernel<<<(n_bins + 127) / 128, 128, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
+    st = launch_score_rows(n_q, item_m, item_l, 2 * n_items, 2, hq, items, 0, nullptr, n_items, n_bins, nullptr,
+                           rows_mass, cs);
+    if (st) return st;
+    score_sum_rows_kernel<<<n_bins, kSumThreads, 0, cs>>>(rows_mass, n_q, n_bins, active, raw_out);
     RK_CHECK_LAUNCH("score_sum_rows_kernel");
   }
   return RK_OK;

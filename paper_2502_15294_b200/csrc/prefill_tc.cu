@@ -88,7 +88,7 @@ struct Params {
   const int64_t* k_pos;            // [s]
   const uint8_t* allowed;          // [s] or null
   const int32_t* items;            // [n_items][3] (lo, hi, bin) or null (uniform)
-  float* item_m;                   // [n_q][hq][n_items] scoring statistics or null
+  float* item_m;                   // [n_q][hq][n_items][2 column halves] scoring statistics or null
   float* item_l;
   float* part_m;                   // [n_q][hq][n_chunks]
   float* part_l;
@@ -751,23 +751,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
             else bar_arrive_cluster(mapa(&p_full[b], 0));
           }
         }
-        if (p.item_m) {                        // combine the halves' item statistics
-          if (half == 1) {
-            xm_it[r] = m_it;
-            xl_it[r] = l_it;
-          }
-          named_sync(bar_id, 64);
-          if (half == 0 && real) {
-            const float m1 = xm_it[r], l1 = xl_it[r];
-            float M = fmaxf(m_it, m1), L = 0.f;
-            if (M != -INFINITY) {
-              L = (l_it > 0.f ? l_it * fast_exp2(m_it - M) : 0.f) + (l1 > 0.f ? l1 * fast_exp2(m1 - M) : 0.f);
-            }
-            const int64_t o = ((int64_t)qi * p.hq + h) * p.n_items + it;
-            p.item_m[o] = M;
-            p.item_l[o] = L;
-          }
-          named_sync(bar_id, 64);
+        if (p.item_m && real) {                // this column half's statistics: slot (item, half); the
+          // finalisation (score_rows_kernel, 2 slots per item) combines the halves — no barrier here
+          const int64_t o = (((int64_t)qi * p.hq + h) * p.n_items + it) * 2 + half;
+          p.item_m[o] = m_it;
+          p.item_l[o] = l_it;
         }
       }
       if (SCORE_ONLY) continue;
@@ -954,7 +942,7 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
   const size_t rh = (size_t)n_q * hq;
   pl.part_bytes = with_output ? align_up(rh * pl.n_chunks * 4, 256) * 2 + align_up(rh * pl.n_chunks * pf::D * 4, 256)
                               : 0;
-  pl.item_bytes = stats ? align_up(rh * pl.n_items * 4, 256) * 2 : 0;
+  pl.item_bytes = stats ? align_up(rh * pl.n_items * 2 * 4, 256) * 2 : 0;     // (m, l) per (item, column half)
   pl.total = pl.qs_bytes + pl.part_bytes + pl.item_bytes + align_up(rh * 4, 256) * 2;
   return pl;
 }
@@ -989,9 +977,9 @@ int launch_prefill_tc(const float* q, int n_q, int hq, const void* k, const void
   float* item_l = nullptr;
   if (stats) {
     item_m = reinterpret_cast<float*>(b);
-    b += align_up(rh * pl.n_items * 4, 256);
+    b += align_up(rh * pl.n_items * 2 * 4, 256);
     item_l = reinterpret_cast<float*>(b);
-    b += align_up(rh * pl.n_items * 4, 256);
+    b += align_up(rh * pl.n_items * 2 * 4, 256);
   }
   float* stat_m = reinterpret_cast<float*>(b);
   b += align_up(rh * 4, 256);
