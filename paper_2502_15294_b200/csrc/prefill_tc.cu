@@ -904,7 +904,12 @@ PrefillPlan prefill_plan(int n_q, int hq, int hkv, int s, int n_items_in, bool s
   }
   // the scores-only pass (no V / PV) has cheaper units: finer, plain chunking balances it
   // better (C3 512 rows: 0.60 -> 0.58 ms with 12 units per pair and no wave model)
-  const int target = (with_output ? per_pair : 12) * prefill_pairs();   // units per CTA pair
+  static int score_units = -1;                              // RK_SCORE_UNITS overrides (experiments)
+  if (score_units < 0) {
+    const char* e = std::getenv("RK_SCORE_UNITS");
+    score_units = e ? std::max(1, std::atoi(e)) : 12;
+  }
+  const int target = (with_output ? per_pair : score_units) * prefill_pairs();   // units per CTA pair
   int nc = (target + mt_total - 1) / mt_total;
   nc = std::max(1, std::min(nc, pl.n_items));
   pl.items_per_chunk = (pl.n_items + nc - 1) / nc;
