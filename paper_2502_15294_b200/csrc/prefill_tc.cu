@@ -522,6 +522,9 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           for (int hl = 0; hl < (SPLIT ? 2 : 1); ++hl)          // q_hi, q_lo
   #pragma unroll
             for (int k = 0; k < D / 16; ++k) {
+#ifdef PF_MMA_ONE                                       // timing experiment only (wrong scores)
+              if (SCORE_ONLY && (hl | k)) continue;
+#endif
               umma2(dS, a0 + (uint64_t)((((2 * hl + k / 4) * QBOX) + 32 * (k % 4)) >> 4),
                    b0 + (uint64_t)((((k / 4) * KBOX) + 32 * (k % 4)) >> 4), kIdescQK, (hl | k) ? 1u : 0u);
             }
@@ -633,22 +636,35 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
                 if (__shfl_sync(0xffffffffu, kp, i) > qpos) sc[32 * c + i] = -INFINITY;
             }
           }
-          float hmax = -INFINITY;
+          // four independent FMNMX3 chains (one serial chain of 32 sat on the
+          // softmax's per-tile critical path); the max is order-free
+          float hm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int i = 0; i < HK; ++i) hmax = fmaxf(hmax, sc[i]);
+          for (int i = 0; i < HK; i += 8)
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) hm[c4] = fmaxf(fmaxf(hm[c4], sc[i + 2 * c4]), sc[i + 2 * c4 + 1]);
+          const float hmax = fmaxf(fmaxf(hm[0], hm[1]), fmaxf(hm[2], hm[3]));
           if (SCORE_ONLY) {
             // this half's (max, sum) of the tile, folded into the item statistics
+#ifdef PF_EXP_OFF                                   // timing experiment only (wrong masses)
+            if (false) {
+#else
             if (hmax != -INFINITY) {
-              float2 acc2 = make_float2(0.f, 0.f);
+#endif
+              float2 acc[4];                           // four independent sum chains
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) acc[c4] = make_float2(0.f, 0.f);
               const float2 nm = make_float2(-hmax, -hmax), one = make_float2(1.f, 1.f);
 #pragma unroll
               for (int i = 0; i < HK; i += 2) {
                 const float2 dlt = ffma2(make_float2(sc[i], sc[i + 1]), one, nm);
                 const float2 e = ((i >> 1) & 7) < PF_POLY_OF8_SCORE ? exp2_poly2(dlt)
                                                                     : make_float2(fast_exp2(dlt.x), fast_exp2(dlt.y));
-                acc2 = ffma2(e, one, acc2);
+                acc[(i >> 1) & 3] = ffma2(e, one, acc[(i >> 1) & 3]);
               }
-              const float tl = acc2.x + acc2.y;
+              const float2 a01 = ffma2(acc[0], one, acc[1]), a23 = ffma2(acc[2], one, acc[3]);
+              const float2 a2 = ffma2(a01, one, a23);
+              const float tl = a2.x + a2.y;
               if (m_it == -INFINITY) {
                 m_it = hmax;
                 l_it = tl;
@@ -679,7 +695,9 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
           const float mu = (m_new == -INFINITY) ? 0.f : m_new;
           const float fac = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mu);
           const bool rescale = !first && (m_new != m_run);
-          float2 acc2 = make_float2(0.f, 0.f);
+          float2 acc[4];                                 // four independent sum chains
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) acc[c4] = make_float2(0.f, 0.f);
           uint32_t hw[HK / 2], lw[HK / 2];
           const float2 nmu = make_float2(-mu, -mu), one = make_float2(1.f, 1.f), mone = make_float2(-1.f, -1.f);
 #pragma unroll
@@ -687,7 +705,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
             const float2 dlt = ffma2(make_float2(sc[i], sc[i + 1]), one, nmu);
             const float2 e = ((i >> 1) & 7) < PF_POLY_OF8 ? exp2_poly2(dlt)
                                                           : make_float2(fast_exp2(dlt.x), fast_exp2(dlt.y));
-            acc2 = ffma2(e, one, acc2);
+            acc[(i >> 1) & 3] = ffma2(e, one, acc[(i >> 1) & 3]);
             __nv_bfloat162 hb = __floats2bfloat162_rn(e.x, e.y);
             const uint32_t hu = *reinterpret_cast<uint32_t*>(&hb);
             hw[i / 2] = hu;
@@ -698,7 +716,9 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constan
               lw[i / 2] = *reinterpret_cast<uint32_t*>(&lb);
             }
           }
-          const float rs = acc2.x + acc2.y;
+          const float2 a01 = ffma2(acc[0], one, acc[1]), a23 = ffma2(acc[2], one, acc[3]);
+          const float2 a2 = ffma2(a01, one, a23);
+          const float rs = a2.x + a2.y;
           l_half = (rescale ? l_half * fac : l_half) + rs;
           // ---- per-item scoring statistics from the softmax's own sum: this half's
           // tile sum rs is relative to the reference max mu, so (mu, rs) folds into the

@@ -8,7 +8,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2502_15294_b200 import _lib, kernels  # noqa: E402
+from paper_2502_15294_b200 import _lib, kernels, stats  # noqa: E402
+
+SCORE = "--score" in sys.argv     # the scores-only form (multi-row watershed scorer)
 
 hq, hkv, d, nq, R, T = 28, 4, 128, 512, 64, 1024
 hist = R * T
@@ -18,11 +20,21 @@ v = torch.randn(s, hkv, d, device="cuda").bfloat16()
 q = torch.randn(nq, hq, d, device="cuda")
 qp = torch.arange(hist, s, device="cuda")
 kp = torch.arange(s, device="cuda")
+bounds = [(r * T, (r + 1) * T, r) for r in range(R)] + [(hist, s, R)]
+
+
+def run():
+    if SCORE:
+        stats.round_scores(q, k, qp, kp, bounds, R, chunk=1024, exact=False)
+    else:
+        kernels.prefill_attention(q, k, v, qp, kp)
+
+
 for _ in range(3):
-    kernels.prefill_attention(q, k, v, qp, kp)
+    run()
 buf = (C.c_ulonglong * 64)()
 _lib.lib.rk_pf_prof_read(buf)
-kernels.prefill_attention(q, k, v, qp, kp)
+run()
 _lib.lib.rk_pf_prof_read(buf)
 a = np.array(list(buf), dtype=np.float64).reshape(4, 16) / 148.0
 names = {0: ["meta_full", "s_full", "buf_free(rescale)", "buf_free(unit end)", "pair bar"],
