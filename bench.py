@@ -220,7 +220,8 @@ def main():
     import torch.distributed as dist
 
     from paper_2502_15294_b200.decode_engine import EngineConfig, GroupedDecoder
-    from paper_2502_15294_b200.sharding import bind_numa_local, dialogues_for_rank, gpu_for_rank, max_over_ranks
+    from paper_2502_15294_b200.sharding import (bind_numa_local, dialogues_for_rank, gpu_for_rank,
+                                                host_available_bytes, host_sets_that_fit, max_over_ranks)
 
     dev_index, shared = gpu_for_rank(local)
     torch.cuda.set_device(dev_index)
@@ -243,6 +244,20 @@ def main():
     w["upper_tier"] = args.upper_tier
     w["step_kernel"] = args.step_kernel
     cfg = EngineConfig(**w)
+    # pinned host rounds: one set per dialogue unless the node's ranks together would not fit in host
+    # memory (an 8-GPU node pins 8 x the one-GPU footprint); then sets are aliased and config says so
+    host_cap = None
+    if cfg.host_unique <= 0 and cfg.upper_tier == "host":
+        es = 2 if cfg.kv_dtype == "bf16" else 4
+        set_bytes = ((cfg.num_layers - cfg.watershed) * 2 * cfg.rounds * cfg.round_tokens * cfg.hkv
+                     * cfg.head_dim * es)
+        ranks_on_node = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        avail = host_available_bytes()
+        fit = host_sets_that_fit(cfg.batch, set_bytes, ranks_on_node, avail)
+        if fit < cfg.batch:
+            cfg.host_unique = fit
+            host_cap = (f"{fit} host round sets per rank ({ranks_on_node} ranks x {cfg.batch} dialogues x "
+                        f"{set_bytes / 2**30:.2f} GiB would exceed 0.6 x {avail / 2**30:.0f} GiB available)")
     # this rank's dialogues (b mod world == rank): its own HBM tiers, pinned host blocks, copy streams
     shard = dialogues_for_rank(cfg.batch * world, world, rank)
     # dialogue groups in flight: two groups hide one group's per-turn KV gather under the other's decode,
@@ -360,7 +375,8 @@ def main():
                    "model": "reference toy transformer (attention + residual, RoPE, tied logits) at "
                             f"{'Llama-3-8B' if cfg.hq == 32 else 'Qwen2-7B'} shapes, GQA, bf16 weights",
                    "global_batch": cfg.batch * world, "parallelism": f"dialogues x{world} (no collective)",
-                   "l2": "inputs larger than L2 (KV + weights read per token step >> 126 MB)"},
+                   "l2": "inputs larger than L2 (KV + weights read per token step >> 126 MB)",
+                   **({"host_memory_cap": host_cap} if host_cap else {})},
         "gpu_launches": eng.kernel_launches_per_turn() * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,

@@ -84,3 +84,30 @@ def bind_numa_local(device_index: int):
         return node
     except Exception:
         return None
+
+
+def host_available_bytes() -> int:
+    """MemAvailable of this host (bytes), 0 when /proc/meminfo is not readable."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def host_sets_that_fit(wanted: int, set_bytes: int, ranks_on_node: int, available: int,
+                       frac: float = 0.6) -> int:
+    """Distinct pinned host round sets per rank that fit this node.
+
+    Every rank on the node pins `wanted` sets of `set_bytes` (one per dialogue,
+    the reference's one store per conversation, store.py:110-129); when all of
+    them would exceed `frac` of the host's available memory the sets are aliased
+    (the engine's host_unique) down to what fits, at least one.  Returns `wanted`
+    when it fits or the host size is unknown (available == 0)."""
+    if wanted < 1 or set_bytes <= 0 or available <= 0:
+        return wanted
+    fit = int(frac * available) // (set_bytes * max(1, ranks_on_node))
+    return max(1, min(wanted, fit))

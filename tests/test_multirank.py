@@ -120,3 +120,15 @@ def test_bench_reference_arm_under_torchrun():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+
+
+def test_host_sets_that_fit():
+    """Pinned host round sets per rank: unique per dialogue when the node's ranks fit, aliased down otherwise."""
+    from paper_2502_15294_b200.sharding import host_available_bytes, host_sets_that_fit
+    gib = 1 << 30
+    assert host_sets_that_fit(32, 2 * gib, 1, 196 * gib) == 32            # one GPU: 64 GiB of 196
+    assert host_sets_that_fit(32, 2 * gib, 8, 196 * gib) == 7             # 8 ranks: floor(0.6*196/16)
+    assert host_sets_that_fit(32, 2 * gib, 8, 2048 * gib) == 32           # a 2 TiB node keeps them unique
+    assert host_sets_that_fit(32, 200 * gib, 8, 196 * gib) == 1           # never below one set
+    assert host_sets_that_fit(32, 2 * gib, 8, 0) == 32                    # unknown host size: unchanged
+    assert host_available_bytes() >= 0
