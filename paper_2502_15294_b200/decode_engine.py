@@ -348,6 +348,7 @@ class RoundDecodeEngine:
         self.meta_host = torch.empty((3, B), dtype=torch.int32, pin_memory=True)
         self.graph_a = None
         self.graph_b = None
+        self.graphs_b1 = None      # multi-row questions: one graph per upper layer (replayed between gather waits)
         # ---- the persistent whole-step kernel (rk_decode_step) for the answer loop
         supported = self.shard_world == 1 and kernels.decode_step_supported(B, c.hq, c.hkv, c.head_dim, self.dtype)
         if c.step_kernel == "persistent" and not supported:
@@ -584,7 +585,10 @@ class RoundDecodeEngine:
         for l in range(c.watershed, c.num_layers):
             if layer_wait:
                 torch.cuda.current_stream().wait_event(self.layer_events[l - c.watershed])
-            self._prefill_layer(l, items=False)
+            if self.graphs_b1 is not None:
+                self.graphs_b1[l - c.watershed].replay()
+            else:
+                self._prefill_layer(l, items=False)
         self.upper_len.copy_(self.upper_len_q)
 
     def _phase_b1(self, layer_wait: bool):
@@ -730,6 +734,19 @@ class RoundDecodeEngine:
                     self.graph_b = torch.cuda.CUDAGraph()
                     with torch.cuda.graph(self.graph_b, stream=self.compute_stream):
                         self._phase_b2()
+                if self.nq > 1 and self.uniform_k:
+                    # the question's upper layers: ~40 launches per layer (projections, RoPE, one
+                    # prefill per dialogue) whose host launch cost exceeded their GPU time at C3;
+                    # one graph per layer keeps the per-layer wait on its gathered rows between
+                    # replays.  Replayed in capture order on one stream, so they share one pool
+                    pool = torch.cuda.graph_pool_handle()
+                    graphs = []
+                    for l in range(self.cfg.watershed, self.cfg.num_layers):
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g, stream=self.compute_stream, pool=pool):
+                            self._prefill_layer(l, items=False)
+                        graphs.append(g)
+                    self.graphs_b1 = graphs
         torch.cuda.synchronize()
 
     def _select_to_host(self, refine: bool = True):
