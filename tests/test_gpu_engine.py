@@ -169,6 +169,31 @@ def test_engine_prefill_turn_matches_oracle():
         np.testing.assert_allclose(_f(eng.raw[b]), raw, rtol=1e-4, atol=1e-12)
 
 
+def test_engine_prefill_graphs_match_eager():
+    """Multi-row questions: the question's upper layers replayed as per-layer CUDA
+    graphs (captured by prepare, replayed between the gather waits) give the eager
+    turn's kept rounds, raw masses and answer ids bit for bit, over turns whose
+    questions, kept rounds and working-cache slot positions change."""
+    nq = 24
+    cfg = _small_cfg(round_tokens=128, batch=2, decode_steps=4, item_chunk=128, question_rows=nq,
+                     question_variants=3)
+    model = DecodeModel(cfg.shape, "cuda", seed=9, prefill_gemm=True)
+    ref = RoundDecodeEngine(cfg, model=model, dialogues=[4, 5])
+    eng = RoundDecodeEngine(cfg, model=model, dialogues=[4, 5])
+    eng.prepare()                    # one eager warm-up turn, then the graphs
+    assert eng.graphs_b1 is not None and len(eng.graphs_b1) == cfg.num_layers - cfg.watershed
+    with torch.cuda.stream(ref.compute_stream):
+        ref.run_turn_eager()         # the same warm-up turn on the eager engine
+    for _ in range(3):
+        with torch.cuda.stream(ref.compute_stream):
+            kr = ref.run_turn_eager()
+        kg, _ = eng.run_turn()
+        torch.cuda.synchronize()
+        assert [list(map(int, k)) for k in kr] == [list(map(int, k)) for k in kg]
+        assert torch.equal(ref.raw, eng.raw)
+        np.testing.assert_array_equal(ref.answers(), eng.answers())
+
+
 def test_engine_e2e_matches_device_path():
     """The public-API turn (question ids from pinned host memory, answer ids
     back to it) gives the device-resident turn's kept rounds and answers."""
