@@ -5,7 +5,7 @@ exec > gpurun_out/ab_score.log 2>&1
 for rep in 1 2; do
   for v in ${VARIANTS:-old new}; do
     if [ $v = new ]; then L=paper_2502_15294_b200/librk.so; else L=variants_tmp/librk_$v.so; fi
-    echo "== $v"; ROUNDKV_B200_LIB=$L timeout 300 python tools/bench_scoring.py --nq 128,512,1024 | cut -c1-64
+    echo "== $v"; ROUNDKV_B200_LIB=$L timeout 300 python tools/bench_scoring.py --nq 128,512,1024 | cut -c1-96
   done
 done
 echo "== prefill (new)"; timeout 300 python tools/bench_prefill.py --nq 512 | cut -c1-200
