@@ -151,6 +151,22 @@ def build_round_items(bounds, chunk: int = 256):
     return np.asarray(items, dtype=np.int32).reshape(-1, 3)
 
 
+_ITEMS_CACHE: dict = {}          # (bounds, chunk, device) -> device item table (read-only to the kernels)
+
+
+def _device_items(torch, dev, key_bounds, chunk: int):
+    """The round items on the device, uploaded once per distinct (bounds, chunk):
+    the calibration pass scores every layer of a conversation with one table, and
+    a pipeline's turns repeat it until a round is added."""
+    key = (tuple((int(lo), int(hi), int(b)) for lo, hi, b in key_bounds), int(chunk), str(dev))
+    t = _ITEMS_CACHE.get(key)
+    if t is None:
+        if len(_ITEMS_CACHE) >= 64:
+            _ITEMS_CACHE.pop(next(iter(_ITEMS_CACHE)))
+        t = _ITEMS_CACHE[key] = torch.from_numpy(build_round_items(key_bounds, chunk)).to(dev)
+    return t
+
+
 def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: int = 256, exact: bool = True,
                  capture_mode: str = "post"):
     """Fused capture + Eq. 1: raw mass per ACTIVE prior round (float64, device).
@@ -168,7 +184,7 @@ def round_scores(q, k, q_pos, k_pos, key_bounds, n_bins, active=None, *, chunk: 
     torch, dev = _device()
     n_q, hq, d = q.shape
     s, hkv = k.shape[0], k.shape[1]
-    items = torch.from_numpy(build_round_items(key_bounds, chunk)).to(dev)
+    items = _device_items(torch, dev, key_bounds, chunk)
     n_items = items.shape[0]
     act = None
     n_out = n_bins
