@@ -151,14 +151,17 @@ def build_round_items(bounds, chunk: int = 256):
     return np.asarray(items, dtype=np.int32).reshape(-1, 3)
 
 
-_ITEMS_CACHE: dict = {}          # (bounds, chunk, device) -> device item table (read-only to the kernels)
+_ITEMS_CACHE: dict = {}          # (bounds, chunk, device, stream) -> device item table (read-only to the kernels)
 
 
 def _device_items(torch, dev, key_bounds, chunk: int):
     """The round items on the device, uploaded once per distinct (bounds, chunk):
     the calibration pass scores every layer of a conversation with one table, and
-    a pipeline's turns repeat it until a round is added."""
-    key = (tuple((int(lo), int(hi), int(b)) for lo, hi, b in key_bounds), int(chunk), str(dev))
+    a pipeline's turns repeat it until a round is added.  Keyed by the current
+    stream too, so a table is only read on the stream it was allocated on and an
+    evicted one is reused by the caching allocator in stream order."""
+    key = (tuple((int(lo), int(hi), int(b)) for lo, hi, b in key_bounds), int(chunk), str(dev),
+           torch.cuda.current_stream(dev).cuda_stream)
     t = _ITEMS_CACHE.get(key)
     if t is None:
         if len(_ITEMS_CACHE) >= 64:
