@@ -340,8 +340,9 @@ def main():
     step_bw = bytes_tok * eng.turn_tokens * args.steps / (ms / 1000.0) / 1e9
     resident, full = eng.gpu_kv_bytes()
     traffic = None      # DRAM bytes per token-step from the committed ncu capture (same shapes)
-    tp = REPO / "profiles" / "r02_traffic_c2_tokenstep.json"
-    if tp.exists() and args.workload == "c2" and args.kv_dtype == "bf16" and args.step_kernel == "layers":
+    tp = REPO / "profiles" / f"r02_traffic_{args.workload}_tokenstep.json"      # c2, c4: one group's token steps
+    if (tp.exists() and args.kv_dtype == "bf16" and args.step_kernel == "layers" and args.serving == "groups"
+            and args.upper_tier == "host"):
         t = json.loads(tp.read_text())
         if t.get("batch_per_group") == g0.cfg.batch:
             traffic = t["per_token_step_bytes_per_group"] * len(eng.groups)
